@@ -1,0 +1,155 @@
+/*
+ * helmsweep.h -- C ABI of the B200 (sm_100a) hot path of multipreconditioned
+ * GMRES with directional double-sweep preconditioners for the 2D impedance
+ * Helmholtz problem (Bootland & Rees, arXiv 2408.11929).
+ *
+ * Citations: P:Lnn = PAPER.md line nn (section / equation named), D1..D12 and
+ * A1..A27 = SURVEY.md §8(c) definitions / readings (restated in DESIGN.md §3).
+ *
+ * Conventions (all entry points)
+ *   - complex128 values are interleaved {re, im} doubles (cuDoubleComplex /
+ *     double2 layout); passed here as `double*` pointing at 2*len doubles.
+ *   - Node index g = j*(nx+1) + i, x fastest (D1).  Multi-column vectors are
+ *     column-major with leading dimension `ld` (>= n) in complex elements.
+ *   - Pointers marked [dev|host] may be device or host memory: the library
+ *     detects host pointers (cudaPointerGetAttributes) and stages them
+ *     through device buffers itself (this is the end-to-end path).  Pointers
+ *     marked [dev] must be device memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *     Every call is asynchronous on `stream` unless stated otherwise.
+ *   - The caller owns every vector buffer; the library owns the matrix and
+ *     factor storage behind the handles (released by *_destroy).  Handles are
+ *     immutable after setup, so concurrent applies on distinct outputs are safe.
+ *   - Every call returns a status code (HELM_OK = 0) and never aborts; the
+ *     message of the last failure is in helm_last_error().
+ *   - There is no CPU fallback: without a CUDA device every compute call
+ *     returns HELM_ECUDA.
+ */
+#ifndef HELMSWEEP_H
+#define HELMSWEEP_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HELM_OK = 0,
+  HELM_EINVAL = 1,      /* invalid argument (sizes, strips too thin, t out of range, tol) */
+  HELM_EDIM = 2,        /* mismatched dimensions between handles */
+  HELM_ESINGULAR = 3,   /* zero pivot while factoring a strip block */
+  HELM_ECUDA = 4,       /* CUDA runtime error or no device */
+  HELM_ENOMEM = 5,      /* device allocation failed */
+  HELM_ENOCONV = 6,     /* maxit reached; x holds the last iterate */
+  HELM_EEXHAUSTED = 7   /* every new column of a block deflated (search space exhausted) */
+};
+
+typedef struct helm_problem_s* helm_problem_t;  /* device matrix (4 symmetric diagonals) + geometry + c */
+typedef struct helm_sweep_s* helm_sweep_t;      /* device strip factors for one (axis, order, N, overlap) */
+
+/* Grid and medium (D1, D3).  Omega = [0, nx h] x [0, ny h]. */
+typedef struct {
+  int nx, ny;            /* cells per axis (>= 2) */
+  double h;              /* cell size */
+  double omega;          /* angular frequency; k = omega / c */
+  const double* c_nodes; /* [dev|host] (nx+1)(ny+1) nodal wave speed, NULL => c = 1 */
+} helm_grid_desc;
+
+/* helm_assemble -- the P1 matrix of Eq. 1a-1b on the "/" mesh (D2):
+ *   A = -K + sum_T k_T^2 M_T + i sum_{e in dOmega} k_e B_e         (D4, A3)
+ * k_T = omega / mean(c at the triangle's vertices), k_e = omega / mean(c at
+ * the edge's ends) (D3, A5).  A is complex symmetric; it is stored as the 4
+ * upper diagonals (centre, east, north, north-east), n complex each.
+ * Errors: HELM_EINVAL (nx, ny < 2, h <= 0), HELM_ENOMEM, HELM_ECUDA. */
+int helm_assemble(const helm_grid_desc* grid, void* stream, helm_problem_t* out);
+
+/* n = (nx+1)(ny+1), nx, ny of a problem.  Host-only query. */
+int helm_problem_info(helm_problem_t p, long* n, int* nx, int* ny);
+
+/* Copy the 4 stored diagonals to out[4*n] (C, E, N, NE; entry g couples node g
+ * to g, g+1, g+nx+1, g+nx+2).  [dev|host] out.  For parity tests. */
+int helm_get_diagonals(helm_problem_t p, double* out, void* stream);
+
+/* helm_load_vector -- b = M1 f (D5, A4): consistent unit-coefficient P1 mass
+ * times the nodal complex source f.  [dev|host] f (n complex), b (n complex). */
+int helm_load_vector(helm_problem_t p, const double* f, double* b, void* stream);
+
+/* helm_spmv -- Y = A X for ncols columns (col-major, ld = n).  [dev|host]. */
+int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols, void* stream);
+
+/* sweep_setup -- build and factor one directional sweep preconditioner
+ * (Eq. 2-4; strips D6, local matrices D7, transmission D8):
+ *   axis       0 = x (strips are vertical slabs: LRL / RLR), 1 = y (BTB / TBT)
+ *   order      0 = increasing (LRL, BTB), 1 = decreasing (RLR, TBT)
+ *   n_strips   N >= 1; every strip needs >= max(2*overlap+1, 2) cells
+ *   overlap    l >= 0 extra mesh lines per internal boundary (A11)
+ *   is_double  1 = double sweep (2N-1 local solves), 0 = forward sweep only
+ *   gather     0 = "recent" (P:L93 literal rule), 1 = "core" ownership (A16)
+ *   n_segments P >= 1 cross-row segments per strip for the partitioned
+ *              (separator) strip solve; 0 = choose automatically
+ * Each strip's local block-tridiagonal matrix is factored once on the device
+ * (block-Thomas per segment plus the separator Schur complement).
+ * Errors: HELM_EINVAL, HELM_ESINGULAR, HELM_ENOMEM, HELM_ECUDA.  Synchronous. */
+int sweep_setup(helm_problem_t p, int axis, int order, int n_strips, int overlap,
+                int is_double, int gather, int n_segments, void* stream,
+                helm_sweep_t* out);
+
+/* Geometry / size report of a sweep handle (host-only query):
+ *   info[0] n_strips, [1] n_c (cross rows), [2] w_max (nodes per block row),
+ *   [3] n_segments, [4] local solves per apply, [5] factor bytes on device,
+ *   [6] model bytes per apply (sum over solves of
+ *       16*(2 n_c w^2 + 3 n_c w)), [7] axis, [8] order, [9] is_double. */
+int sweep_info(helm_sweep_t s, long* info /* >= 10 */);
+
+/* sweep_apply -- Z[:, d] = M_d^{-1} R[:, d] for the t directions dirs[0..t-1]
+ * ("apply ... in parallel"), all batched in ONE persistent kernel launch.
+ *   R   [dev|host] n x t col-major with leading dim ldr; ldr = 0 broadcasts one
+ *       vector to all t directions (k = 1 and the t >= 3 sum rule).
+ *   Z   [dev|host] n x t col-major, leading dim ldz (>= n).
+ * All handles must belong to the same problem size.  1 <= t <= 8.
+ * Errors: HELM_EINVAL, HELM_EDIM, HELM_ECUDA (incl. grid too large for
+ * co-residency: reduce n_segments). */
+int sweep_apply(const helm_sweep_t* dirs, int t, const double* R, long ldr,
+                double* Z, long ldz, void* stream);
+
+/* Solve statistics of mpgmres_solve. */
+typedef struct {
+  int iterations;        /* outer iterations k (each applies all t preconditioners, D11) */
+  int converged;         /* projected rho_k <= tol */
+  int flags;             /* bit0 maxit reached, bit1 search space exhausted */
+  int deflations;        /* columns dropped by the 1e-10 rule (D10 step 5) */
+  double proj_rel_res;   /* rho_k = ||beta e1 - H y|| / beta at exit */
+  double true_rel_res;   /* ||b - A x|| / ||b|| recomputed */
+  double solve_s;        /* wall seconds of the solve (host clock) */
+  double sweep_ms;       /* device ms spent in sweep_apply launches (CUDA events) */
+  double spmv_ms;        /* device ms in the SpMM launches */
+  double orth_ms;        /* device ms in BCGS2 + block QR launches */
+  long matvecs, prec_applies, inner_products;
+  double* history;       /* optional host array of rho_k, capacity history_cap */
+  int history_cap;
+} mpgmres_stats;
+
+/* mpgmres_solve -- selective MPGMRES with the paper's selection
+ * rules (t = 2 cross rule, t >= 3 sum rule, k = 1 all on r0/||r0||),
+ * block classical Gram-Schmidt with reorthogonalisation (BCGS2) and intra-
+ * block CGS2 with the 1e-10 deflation rule (D10), projected least squares by
+ * Householder QR on the host.  x0 = 0; stops when rho_k <= tol.
+ *   b [dev|host] n complex; x [dev|host] n complex (output).
+ * Host-synchronous (one small device->host copy per iteration).
+ * Errors: HELM_EINVAL (tol not in (0,1), t not in [1,8], maxit < 1),
+ *         HELM_ENOCONV, HELM_EEXHAUSTED, HELM_ENOMEM, HELM_ECUDA. */
+int mpgmres_solve(helm_problem_t p, const helm_sweep_t* dirs, int t,
+                  const double* b, double* x, double tol, int maxit,
+                  mpgmres_stats* stats, void* stream);
+
+void helm_problem_destroy(helm_problem_t p);
+void sweep_destroy(helm_sweep_t s);
+const char* helm_strerror(int code);
+const char* helm_last_error(void);
+
+/* Number of this library's kernel launches since load (host counter). */
+long helm_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELMSWEEP_H */

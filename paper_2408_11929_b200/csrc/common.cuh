@@ -1,0 +1,123 @@
+// common.cuh -- shared device/host helpers of the helmsweep library (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/helmsweep.h"
+
+typedef double2 cplx;
+
+// ------------------------------------------------------------------ complex
+__host__ __device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cmk(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return cmk(a.x, -a.y); }
+// acc += a * b
+__host__ __device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__host__ __device__ __forceinline__ void cfmaconj(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+__host__ __device__ __forceinline__ cplx cinv(cplx a) {
+  double d = 1.0 / cabs2(a);
+  return cmk(a.x * d, -a.y * d);
+}
+
+// ------------------------------------------------------------------ errors
+void helm_set_error(const char* fmt, ...);
+extern long g_helm_launches;
+
+#define HELM_CUDA_TRY(expr)                                                       \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      helm_set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return (_e == cudaErrorMemoryAllocation) ? HELM_ENOMEM : HELM_ECUDA;        \
+    }                                                                             \
+  } while (0)
+
+#define HELM_LAUNCH_CHECK()                                                       \
+  do {                                                                            \
+    g_helm_launches++;                                                            \
+    cudaError_t _e = cudaGetLastError();                                          \
+    if (_e != cudaSuccess) {                                                      \
+      helm_set_error("%s:%d kernel launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \
+      return HELM_ECUDA;                                                          \
+    }                                                                             \
+  } while (0)
+
+#define HELM_TRY(expr)            \
+  do {                            \
+    int _rc = (expr);             \
+    if (_rc != HELM_OK) return _rc; \
+  } while (0)
+
+// ------------------------------------------------------------------ handles
+struct helm_problem_s {
+  int nx, ny;
+  long n;
+  double h, omega;
+  double* c;      // [dev] nodal wave speed (n)
+  cplx* dC;       // [dev] diagonals: centre, east (g,g+1), north (g,g+nx+1), north-east (g,g+nx+2)
+  cplx* dE;
+  cplx* dN;
+  cplx* dNE;
+};
+
+// One sweep preconditioner (one direction): strips + factors, all on device.
+struct helm_sweep_s {
+  helm_problem_s* prob;
+  int axis, order, N, overlap, is_double, gather;
+  int nc;          // cross rows per strip (ny+1 for axis 0, nx+1 for axis 1)
+  int wmax;        // max nodes per block row over strips
+  int P;           // segments per strip
+  // host copies of geometry
+  std::vector<int> a, b, w;        // per strip: first/last along line, width
+  std::vector<int> own_lo, own_hi; // per strip: gathered position range (core/recent)
+  std::vector<int> seg_lo, seg_hi; // per segment: cross-row range (same for all strips)
+  // device geometry (int arrays, N each)
+  int* d_a; int* d_w; int* d_own_lo; int* d_own_hi;
+  int* d_seg_lo; int* d_seg_hi;    // P each
+  // strip bands (local matrix A_s, D7): per strip s, per row c, per position q:
+  //   dg[s][c][q] = diagonal, al[s][c][q] = along coupling (q,q+1),
+  //   cr[s][c][q] = cross coupling (c,q)-(c+1,q), ne[s][c][q] = (c,q)-(c+1,q+1)
+  //   stored with stride wmax per row and nc*wmax per strip.
+  cplx* d_dg; cplx* d_al; cplx* d_cr; cplx* d_ne;
+  // transmission-correction coefficients (D8): [s][side][c][5]
+  cplx* d_tc;
+  // factors: per strip s, row c: Sinv (w_s x w_s row-major) at fac_off[s] + c*w_s^2
+  cplx* d_fac; std::vector<long> fac_off; long* d_fac_off;
+  // reduced (separator) system: per strip s, separator k (0..P-2): Rinv, G, F
+  cplx* d_red; std::vector<long> red_off; long* d_red_off;
+  long factor_bytes;
+};
+
+// ------------------------------------------------------------------ staging
+// Ensure `ptr` is device-accessible; for host pointers allocate a device
+// buffer (and copy in when `copy_in`).  `dev` receives the device pointer.
+struct Staged {
+  void* dev = nullptr;
+  const void* host = nullptr;
+  size_t bytes = 0;
+  bool owned = false;
+};
+int helm_stage_in(const void* ptr, size_t bytes, bool copy_in, cudaStream_t st, Staged& out);
+int helm_stage_out(Staged& s, cudaStream_t st);  // copy back to host if staged, then free
+void helm_stage_free(Staged& s, cudaStream_t st);
+bool helm_is_device_ptr(const void* p);

@@ -1,0 +1,151 @@
+// dense.cuh -- CTA-wide dense complex w x w block helpers for the strip
+// factorisation (setup only; the hot path is sweep_apply.cu).
+// All blocks are row-major w x w; every helper must be called by the whole CTA
+// and ends with __syncthreads().
+#pragma once
+#include "common.cuh"
+
+// Bidiagonal coupling U of a strip (D7 block structure): row c couples to row
+// c+1 through U_c with U[p][p] = cr[p], U[p][p+1] = ne[p].  L_{c+1} = U_c^T.
+enum BidiMode { BD_NONE = 0, BD_U = 1, BD_UT = 2 };
+
+struct Bidi {
+  int mode;
+  const cplx* cr;
+  const cplx* ne;
+};
+
+// (L X)[p][s] for a left bidiagonal factor
+__device__ __forceinline__ cplx bidi_left(const Bidi& L, const cplx* X, int w, int p, int s) {
+  if (L.mode == BD_NONE) return X[p * w + s];
+  cplx acc = cmul(L.cr[p], X[p * w + s]);
+  if (L.mode == BD_U) {
+    if (p + 1 < w) cfma(acc, L.ne[p], X[(p + 1) * w + s]);
+  } else {
+    if (p >= 1) cfma(acc, L.ne[p - 1], X[(p - 1) * w + s]);
+  }
+  return acc;
+}
+
+// out[p][q] (+)= alpha * (L X R)[p][q]; R applied on the right:
+//   R = U : (Y U)[p][q] = cr[q] Y[p][q] + ne[q-1] Y[p][q-1]
+//   R = UT: (Y U^T)[p][q] = cr[q] Y[p][q] + ne[q] Y[p][q+1]
+__device__ inline void blk_lxr(cplx* out, const cplx* X, Bidi L, Bidi R, int w, double alpha,
+                               bool accumulate) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    int p = e / w, q = e % w;
+    cplx v;
+    if (R.mode == BD_NONE) {
+      v = bidi_left(L, X, w, p, q);
+    } else {
+      v = cmul(R.cr[q], bidi_left(L, X, w, p, q));
+      if (R.mode == BD_U) {
+        if (q >= 1) cfma(v, R.ne[q - 1], bidi_left(L, X, w, p, q - 1));
+      } else {
+        if (q + 1 < w) cfma(v, R.ne[q], bidi_left(L, X, w, p, q + 1));
+      }
+    }
+    v = cscale(v, alpha);
+    out[e] = accumulate ? cadd(out[e], v) : v;
+  }
+  __syncthreads();
+}
+
+// C (+)= alpha * op(A) * B, op(A) = A or A^T; C must not alias A or B.
+__device__ inline void blk_matmul(cplx* C, const cplx* A, bool transA, const cplx* B, int w,
+                                  double alpha, bool accumulate) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    int p = e / w, q = e % w;
+    cplx acc = cmk(0.0, 0.0);
+    if (!transA) {
+      for (int r = 0; r < w; ++r) cfma(acc, A[p * w + r], B[r * w + q]);
+    } else {
+      for (int r = 0; r < w; ++r) cfma(acc, A[r * w + p], B[r * w + q]);
+    }
+    acc = cscale(acc, alpha);
+    C[e] = accumulate ? cadd(C[e], acc) : acc;
+  }
+  __syncthreads();
+}
+
+__device__ inline void blk_copy(cplx* dst, const cplx* src, int w) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) dst[e] = src[e];
+  __syncthreads();
+}
+
+// In-place Gauss-Jordan inversion with partial (row) pivoting of a w x w block
+// in shared memory.  piv: smem int[w]; col: smem cplx[w]; red: smem scratch of
+// >= 2*32 doubles/ints.  Returns (to all threads) 0 on success, 1 if a pivot is 0.
+__device__ inline int gj_invert(cplx* A, int w, int* piv, cplx* col, double* redv, int* redi,
+                                int* flag) {
+  const int tid = threadIdx.x;
+  if (tid == 0) *flag = 0;
+  __syncthreads();
+  for (int k = 0; k < w; ++k) {
+    // pivot search in column k (warp 0)
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < w; i += 32) {
+        double v = cabs2(A[i * w + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        double ob = __shfl_down_sync(0xffffffffu, best, off);
+        int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        piv[k] = bi;
+        redv[0] = best;
+        if (!(best > 0.0)) *flag = 1;
+      }
+    }
+    __syncthreads();
+    if (*flag) return 1;
+    const int p = piv[k];
+    if (p != k) {
+      for (int j = tid; j < w; j += blockDim.x) {
+        cplx t = A[k * w + j];
+        A[k * w + j] = A[p * w + j];
+        A[p * w + j] = t;
+      }
+      __syncthreads();
+    }
+    // save column k (multipliers), then scale row k
+    for (int i = tid; i < w; i += blockDim.x) col[i] = A[i * w + k];
+    __syncthreads();
+    const cplx dinv = cinv(col[k]);
+    for (int j = tid; j < w; j += blockDim.x) {
+      cplx v = (j == k) ? cmk(1.0, 0.0) : A[k * w + j];
+      A[k * w + j] = cmul(v, dinv);
+    }
+    __syncthreads();
+    // eliminate column k from all other rows
+    for (int e = tid; e < w * w; e += blockDim.x) {
+      int i = e / w, j = e % w;
+      if (i == k) continue;
+      cplx f = col[i];
+      cplx a = (j == k) ? cmk(0.0, 0.0) : A[e];
+      cplx r = A[k * w + j];
+      a.x -= f.x * r.x - f.y * r.y;
+      a.y -= f.x * r.y + f.y * r.x;
+      A[e] = a;
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, in reverse order
+  for (int k = w - 1; k >= 0; --k) {
+    int p = piv[k];
+    if (p != k) {
+      for (int i = tid; i < w; i += blockDim.x) {
+        cplx t = A[i * w + k];
+        A[i * w + k] = A[i * w + p];
+        A[i * w + p] = t;
+      }
+      __syncthreads();
+    }
+  }
+  (void)redi;
+  return 0;
+}

@@ -1,0 +1,445 @@
+// strip_setup.cu -- sweep_setup (hot-path row a2): strip geometry (D6), local
+// block-tridiagonal matrices (D7), transmission-correction stencils (D8), and
+// the factorisation of every strip, "factored once" (P:L152 uses `\`; the
+// north star asks for a banded / block-tridiagonal LU).
+//
+// Strip s, generic coordinates: block row c = cross index (n_c rows), position
+// q = 0..w_s-1 along the axis (line a_s + q).  A_s is block tridiagonal:
+//   D_c = tridiag(al[c][q-1], dg[c][q], al[c][q]),  U_c = bidiag(cr[c][q], ne[c][q]),
+//   L_{c+1} = U_c^T  (A_s complex symmetric).
+// Partitioned factorisation: the n_c rows are split into P
+// segments separated by P-1 single separator rows.  Each segment is factored
+// by block-Thomas with explicit inverses  S_lo = D_lo,
+//   S_c = D_c - U_{c-1}^T S_{c-1}^{-1} U_{c-1},  Sinv_c = S_c^{-1}
+// (unpivoted between blocks, Gauss-Jordan with partial pivoting inside a
+// block; stable here).  The separator Schur complement
+// (block tridiagonal with dense couplings) is factored by block-Thomas too and
+// stored as Rinv_k, G_k = Rinv_k R_{k,k-1}, F_k = Rinv_k R_{k,k+1}.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "p1_entries.cuh"
+
+// ------------------------------------------------------------------ bands + corrections
+struct StripGeo {
+  const int* a;   // first line of each strip
+  const int* w;   // width
+  int N, nc, wmax, axis;
+};
+
+__global__ void k_strip_bands(GridView g, StripGeo sg, cplx* dg, cplx* al, cplx* cr, cplx* ne, cplx* tc) {
+  const int s = blockIdx.y;
+  const int a = sg.a[s], w = sg.w[s], b = a + w - 1;
+  CellSel loc{sg.axis, a, b, s > 0 ? 1 : 0, s < sg.N - 1 ? 1 : 0};
+  CellSel all = sel_all();
+  const int nc = sg.nc;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nc * sg.wmax; e += gridDim.x * blockDim.x) {
+    int c = e / sg.wmax, q = e % sg.wmax;
+    long idx = ((long)s * nc + c) * sg.wmax + q;
+    if (q >= w) {
+      dg[idx] = al[idx] = cr[idx] = ne[idx] = cmk(0, 0);
+      continue;
+    }
+    int pa = a + q;
+    dg[idx] = gen_diag(g, loc, sg.axis, pa, c);
+    al[idx] = (q + 1 < w) ? gen_along(g, loc, sg.axis, pa, c) : cmk(0, 0);
+    cr[idx] = (c + 1 < nc) ? gen_cross(g, loc, sg.axis, pa, c) : cmk(0, 0);
+    ne[idx] = (c + 1 < nc && q + 1 < w) ? gen_ne(g, loc, sg.axis, pa, c) : cmk(0, 0);
+  }
+  // transmission-correction stencil (D8): (Atilde_s - A) on the interface rows.
+  // tc[((s*2 + side)*nc + c)*5 + k], k: 0 v(L,c-1), 1 v(L,c), 2 v(L,c+1), 3 v(O,c), 4 v(O,c+dd)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nc; e += gridDim.x * blockDim.x) {
+    int side = e / nc, c = e % nc;
+    cplx* o = tc + (((long)s * 2 + side) * nc + c) * 5;
+    bool has = side == 0 ? (s > 0) : (s < sg.N - 1);
+    if (!has) {
+      for (int k = 0; k < 5; ++k) o[k] = cmk(0, 0);
+      continue;
+    }
+    int L = side == 0 ? a : b;
+    o[0] = (c >= 1) ? csub(gen_cross(g, loc, sg.axis, L, c - 1), gen_cross(g, all, sg.axis, L, c - 1)) : cmk(0, 0);
+    o[1] = csub(gen_diag(g, loc, sg.axis, L, c), gen_diag(g, all, sg.axis, L, c));
+    o[2] = (c + 1 < nc) ? csub(gen_cross(g, loc, sg.axis, L, c), gen_cross(g, all, sg.axis, L, c)) : cmk(0, 0);
+    if (side == 0) {
+      o[3] = cscale(gen_along(g, all, sg.axis, L - 1, c), -1.0);
+      o[4] = (c >= 1) ? cscale(gen_ne(g, all, sg.axis, L - 1, c - 1), -1.0) : cmk(0, 0);
+    } else {
+      o[3] = cscale(gen_along(g, all, sg.axis, L, c), -1.0);
+      o[4] = (c + 1 < nc) ? cscale(gen_ne(g, all, sg.axis, L, c), -1.0) : cmk(0, 0);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ segment factorisation
+struct FacArgs {
+  const int* w;
+  const long* fac_off;
+  const int* seg_lo;
+  const int* seg_hi;
+  const cplx *dg, *al, *cr, *ne;
+  int nc, wmax, P;
+  cplx* fac;
+  cplx* scratch;   // per (s,p): 4 w^2: ping, pong, XLL, XLH
+  long scratch_stride;
+  int* status;     // first failure: (s*nc + c) + 1
+};
+
+__device__ inline void build_D(cplx* S, const cplx* dg, const cplx* al, int w) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    int p = e / w, q = e % w;
+    cplx v = cmk(0, 0);
+    if (p == q) v = dg[p];
+    else if (q == p + 1) v = al[p];
+    else if (p == q + 1) v = al[q];
+    S[e] = v;
+  }
+  __syncthreads();
+}
+
+__global__ void k_factor_segments(FacArgs fa) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.y, pseg = blockIdx.x;
+  const int w = fa.w[s];
+  cplx* S = reinterpret_cast<cplx*>(smem_raw);
+  cplx* colv = S + w * w;
+  double* redv = reinterpret_cast<double*>(colv + w);
+  int* flag = reinterpret_cast<int*>(redv + 4);
+  int* piv = flag + 4;
+  const int lo = fa.seg_lo[pseg], hi = fa.seg_hi[pseg];
+  const long band = (long)s * fa.nc * fa.wmax;
+  cplx* fac = fa.fac + fa.fac_off[s];
+  const long w2 = (long)w * w;
+  auto Ub = [&](int c, int mode) { return Bidi{mode, fa.cr + band + (long)c * fa.wmax, fa.ne + band + (long)c * fa.wmax}; };
+  const Bidi NONE{BD_NONE, nullptr, nullptr};
+
+  // top-down block-Thomas over the segment
+  for (int c = lo; c <= hi; ++c) {
+    build_D(S, fa.dg + band + (long)c * fa.wmax, fa.al + band + (long)c * fa.wmax, w);
+    if (c > lo) blk_lxr(S, fac + (long)(c - 1) * w2, Ub(c - 1, BD_UT), Ub(c - 1, BD_U), w, -1.0, true);
+    if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
+      if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
+      return;
+    }
+    blk_copy(fac + (long)c * w2, S, w);
+  }
+  if (fa.P == 1) return;
+  cplx* scr = fa.scratch + ((long)s * fa.P + pseg) * fa.scratch_stride;
+  cplx* ping = scr;
+  cplx* pong = scr + w2;
+  cplx* XLL = scr + 2 * w2;
+  cplx* XLH = scr + 3 * w2;
+  // bottom-up block-Thomas: S'_hi = D_hi, S'_c = D_c - U_c S'^{-1}_{c+1} U_c^T;
+  // X[lo,lo] = S'^{-1}_lo (corner block of the segment inverse)
+  for (int c = hi; c >= lo; --c) {
+    build_D(S, fa.dg + band + (long)c * fa.wmax, fa.al + band + (long)c * fa.wmax, w);
+    if (c < hi) blk_lxr(S, ping, Ub(c, BD_U), Ub(c, BD_UT), w, -1.0, true);
+    if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
+      if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
+      return;
+    }
+    blk_copy(c == lo ? XLL : ping, S, w);
+  }
+  // X[lo,hi]: Y_hi = Sinv_hi; Y_c = -Sinv_c U_c Y_{c+1}
+  blk_copy(ping, fac + (long)hi * w2, w);
+  cplx* cur = ping;
+  cplx* nxt = pong;
+  for (int c = hi - 1; c >= lo; --c) {
+    // tmp = U_c Y_{c+1}  (into XLH as scratch), then nxt = -Sinv_c tmp
+    blk_lxr(XLH, cur, Ub(c, BD_U), NONE, w, 1.0, false);
+    blk_matmul(nxt, fac + (long)c * w2, false, XLH, w, -1.0, false);
+    cplx* t = cur; cur = nxt; nxt = t;
+  }
+  blk_copy(XLH, cur, w);
+}
+
+// ------------------------------------------------------------------ separator system
+struct RedArgs {
+  const int* w;
+  const long* fac_off;
+  const long* red_off;
+  const int* seg_lo;
+  const int* seg_hi;
+  const cplx *dg, *al, *cr, *ne;
+  int nc, wmax, P;
+  const cplx* fac;
+  const cplx* scratch;
+  long scratch_stride;
+  cplx* red;
+  cplx* rscratch;  // per strip: 2 w^2 (R_{k,k+1} of the previous separator, temp)
+  int* status;
+};
+
+__global__ void k_reduced(RedArgs ra) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.x;
+  const int w = ra.w[s];
+  const long w2 = (long)w * w;
+  cplx* S = reinterpret_cast<cplx*>(smem_raw);
+  cplx* colv = S + w * w;
+  double* redv = reinterpret_cast<double*>(colv + w);
+  int* flag = reinterpret_cast<int*>(redv + 4);
+  int* piv = flag + 4;
+  const long band = (long)s * ra.nc * ra.wmax;
+  const cplx* fac = ra.fac + ra.fac_off[s];
+  cplx* red = ra.red + ra.red_off[s];
+  cplx* Rprev = ra.rscratch + (long)s * 2 * ra.wmax * ra.wmax;  // R_{k-1,k}
+  cplx* Tmp = Rprev + (long)ra.wmax * ra.wmax;
+  auto Ub = [&](int c, int mode) { return Bidi{mode, ra.cr + band + (long)c * ra.wmax, ra.ne + band + (long)c * ra.wmax}; };
+  auto scr = [&](int p) { return ra.scratch + ((long)s * ra.P + p) * ra.scratch_stride; };
+  const Bidi NONE{BD_NONE, nullptr, nullptr};
+  const int P = ra.P;
+  for (int k = 0; k <= P - 2; ++k) {
+    const int hk = ra.seg_hi[k];          // last row of segment k
+    const int sk = hk + 1;                // separator row
+    const int hk1 = ra.seg_hi[k + 1];     // last row of segment k+1
+    cplx* Rinv = red + (long)k * 3 * w2;
+    cplx* G = Rinv + w2;
+    cplx* F = Rinv + 2 * w2;
+    // R_kk = D_sk - U_hk^T X_k[hi,hi] U_hk - U_sk X_{k+1}[lo,lo] U_sk^T
+    build_D(S, ra.dg + band + (long)sk * ra.wmax, ra.al + band + (long)sk * ra.wmax, w);
+    blk_lxr(S, fac + (long)hk * w2, Ub(hk, BD_UT), Ub(hk, BD_U), w, -1.0, true);
+    blk_lxr(S, scr(k + 1) + 2 * w2, Ub(sk, BD_U), Ub(sk, BD_UT), w, -1.0, true);
+    if (k >= 1) {
+      // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
+      blk_matmul(S, Rprev, true, red + (long)(k - 1) * 3 * w2 + 2 * w2, w, -1.0, true);
+    }
+    if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
+      if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
+      return;
+    }
+    blk_copy(Rinv, S, w);
+    if (k >= 1) {
+      // G_k = Rinv_k R_{k,k-1} = Rinv_k R_{k-1,k}^T  (Tmp = R_{k-1,k}^T)
+      for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+        int p = e / w, q = e % w;
+        Tmp[e] = Rprev[q * w + p];
+      }
+      __syncthreads();
+      blk_matmul(G, Rinv, false, Tmp, w, 1.0, false);
+    }
+    if (k <= P - 3) {
+      // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1}
+      blk_lxr(Rprev, scr(k + 1) + 3 * w2, Ub(sk, BD_U), Ub(hk1, BD_U), w, -1.0, false);
+      blk_matmul(F, Rinv, false, Rprev, w, 1.0, false);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+static int choose_segments(int nc, int requested) {
+  if (requested > 0) return requested;
+  int P = 32;
+  while (P > 1 && (nc - (P - 1)) / P < 8) P /= 2;
+  return P;
+}
+
+extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strips, int overlap,
+                           int is_double, int gather, int n_segments, void* stream, helm_sweep_t* out) {
+  if (!prob || !out) { helm_set_error("sweep_setup: null argument"); return HELM_EINVAL; }
+  *out = nullptr;
+  if ((axis != 0 && axis != 1) || (order != 0 && order != 1) || n_strips < 1 || overlap < 0 ||
+      (gather != 0 && gather != 1) || n_segments < 0) {
+    helm_set_error("sweep_setup: bad axis/order/n_strips/overlap/gather/n_segments");
+    return HELM_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_axis = axis == 0 ? prob->nx : prob->ny;
+  const int nc = (axis == 0 ? prob->ny : prob->nx) + 1;
+  // partition lines p_0 = 0 < ... < p_N = n_axis, larger runs first (D6, A12)
+  std::vector<int> pl(n_strips + 1, 0);
+  int base = n_axis / n_strips, extra = n_axis % n_strips;
+  for (int s = 0; s < n_strips; ++s) pl[s + 1] = pl[s] + base + (s < extra ? 1 : 0);
+  if (n_strips > 1 && base < std::max(2 * overlap + 1, 2)) {
+    helm_set_error("sweep_setup: strips of %d cells are too thin for overlap %d (need >= %d)", base,
+                   overlap, std::max(2 * overlap + 1, 2));
+    return HELM_EINVAL;
+  }
+  if (n_strips > n_axis) { helm_set_error("sweep_setup: more strips than cells"); return HELM_EINVAL; }
+  helm_sweep_s* h = new helm_sweep_s();
+  h->prob = prob;
+  h->axis = axis; h->order = order; h->N = n_strips; h->overlap = overlap;
+  h->is_double = is_double ? 1 : 0; h->gather = gather; h->nc = nc;
+  h->a.resize(n_strips); h->b.resize(n_strips); h->w.resize(n_strips);
+  h->own_lo.resize(n_strips); h->own_hi.resize(n_strips);
+  int wmax = 0;
+  for (int s = 0; s < n_strips; ++s) {
+    h->a[s] = std::max(pl[s] - overlap, 0);
+    h->b[s] = std::min(pl[s + 1] + overlap, n_axis);
+    h->w[s] = h->b[s] - h->a[s] + 1;
+    wmax = std::max(wmax, h->w[s]);
+    if (gather == 0) {
+      h->own_lo[s] = 0; h->own_hi[s] = h->w[s] - 1;
+    } else {  // core: lines p_s .. p_{s+1}-1 (last strip also p_N)
+      h->own_lo[s] = pl[s] - h->a[s];
+      h->own_hi[s] = (s == n_strips - 1 ? pl[s + 1] : pl[s + 1] - 1) - h->a[s];
+    }
+  }
+  h->wmax = wmax;
+  int P = choose_segments(nc, n_segments);
+  if (P < 1 || nc - (P - 1) < P) {
+    helm_set_error("sweep_setup: %d segments do not fit %d cross rows", P, nc);
+    delete h;
+    return HELM_EINVAL;
+  }
+  h->P = P;
+  {
+    int rows = nc - (P - 1), sb = rows / P, se = rows % P, c = 0;
+    for (int p = 0; p < P; ++p) {
+      int m = sb + (p < se ? 1 : 0);
+      h->seg_lo.push_back(c);
+      h->seg_hi.push_back(c + m - 1);
+      c += m + 1;  // skip the separator row
+    }
+  }
+  // factor storage
+  h->fac_off.resize(n_strips);
+  h->red_off.resize(n_strips);
+  long fac_total = 0, red_total = 0;
+  for (int s = 0; s < n_strips; ++s) {
+    h->fac_off[s] = fac_total;
+    fac_total += (long)nc * h->w[s] * h->w[s];
+    h->red_off[s] = red_total;
+    red_total += (long)std::max(P - 1, 0) * 3 * h->w[s] * h->w[s];
+  }
+  const long bandN = (long)n_strips * nc * wmax;
+  h->factor_bytes = (fac_total + red_total) * (long)sizeof(cplx);
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes > 0 ? bytes : 16);
+  };
+  h->d_a = h->d_w = h->d_own_lo = h->d_own_hi = h->d_seg_lo = h->d_seg_hi = nullptr;
+  h->d_dg = h->d_al = h->d_cr = h->d_ne = h->d_tc = h->d_fac = h->d_red = nullptr;
+  h->d_fac_off = h->d_red_off = nullptr;
+  alloc((void**)&h->d_a, sizeof(int) * n_strips);
+  alloc((void**)&h->d_w, sizeof(int) * n_strips);
+  alloc((void**)&h->d_own_lo, sizeof(int) * n_strips);
+  alloc((void**)&h->d_own_hi, sizeof(int) * n_strips);
+  alloc((void**)&h->d_seg_lo, sizeof(int) * P);
+  alloc((void**)&h->d_seg_hi, sizeof(int) * P);
+  alloc((void**)&h->d_fac_off, sizeof(long) * n_strips);
+  alloc((void**)&h->d_red_off, sizeof(long) * n_strips);
+  alloc((void**)&h->d_dg, sizeof(cplx) * bandN);
+  alloc((void**)&h->d_al, sizeof(cplx) * bandN);
+  alloc((void**)&h->d_cr, sizeof(cplx) * bandN);
+  alloc((void**)&h->d_ne, sizeof(cplx) * bandN);
+  alloc((void**)&h->d_tc, sizeof(cplx) * n_strips * 2 * nc * 5);
+  alloc((void**)&h->d_fac, sizeof(cplx) * fac_total);
+  alloc((void**)&h->d_red, sizeof(cplx) * std::max(red_total, 1L));
+  if (e != cudaSuccess) {
+    helm_set_error("sweep_setup: cudaMalloc (%.2f GB factors): %s", h->factor_bytes / 1e9, cudaGetErrorString(e));
+    sweep_destroy(h);
+    return HELM_ENOMEM;
+  }
+  auto h2d = [&](void* d, const void* s, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, s, bytes, cudaMemcpyHostToDevice, st);
+  };
+  h2d(h->d_a, h->a.data(), sizeof(int) * n_strips);
+  h2d(h->d_w, h->w.data(), sizeof(int) * n_strips);
+  h2d(h->d_own_lo, h->own_lo.data(), sizeof(int) * n_strips);
+  h2d(h->d_own_hi, h->own_hi.data(), sizeof(int) * n_strips);
+  h2d(h->d_seg_lo, h->seg_lo.data(), sizeof(int) * P);
+  h2d(h->d_seg_hi, h->seg_hi.data(), sizeof(int) * P);
+  h2d(h->d_fac_off, h->fac_off.data(), sizeof(long) * n_strips);
+  h2d(h->d_red_off, h->red_off.data(), sizeof(long) * n_strips);
+  if (e != cudaSuccess) {
+    helm_set_error("sweep_setup: copy geometry: %s", cudaGetErrorString(e));
+    sweep_destroy(h);
+    return HELM_ECUDA;
+  }
+  GridView g{prob->nx, prob->ny, prob->h, prob->omega, prob->c};
+  StripGeo sg{h->d_a, h->d_w, n_strips, nc, wmax, axis};
+  {
+    dim3 grid((nc * wmax + 255) / 256, n_strips);
+    k_strip_bands<<<grid, 256, 0, st>>>(g, sg, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc);
+    HELM_LAUNCH_CHECK();
+  }
+  // factorisation
+  int* d_status = nullptr;
+  cplx* scratch = nullptr;
+  cplx* rscratch = nullptr;
+  const long sstride = 4L * wmax * wmax;
+  if (e == cudaSuccess) e = cudaMalloc(&d_status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, sizeof(int), st);
+  if (P > 1) {
+    alloc((void**)&scratch, sizeof(cplx) * sstride * n_strips * P);
+    alloc((void**)&rscratch, sizeof(cplx) * 2L * wmax * wmax * n_strips);
+  }
+  if (e != cudaSuccess) {
+    helm_set_error("sweep_setup: scratch: %s", cudaGetErrorString(e));
+    cudaFree(d_status); cudaFree(scratch); cudaFree(rscratch);
+    sweep_destroy(h);
+    return HELM_ENOMEM;
+  }
+  size_t smem = sizeof(cplx) * ((size_t)wmax * wmax + wmax) + sizeof(int) * (wmax + 4) + 64;
+  cudaFuncSetAttribute(k_factor_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int threads = wmax * wmax >= 1024 ? 512 : 256;
+  FacArgs fa{h->d_w, h->d_fac_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr, h->d_ne,
+             nc, wmax, P, h->d_fac, scratch, sstride, d_status};
+  k_factor_segments<<<dim3(P, n_strips), threads, smem, st>>>(fa);
+  g_helm_launches++;
+  e = cudaGetLastError();
+  if (e == cudaSuccess && P > 1) {
+    RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
+               h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
+    k_reduced<<<n_strips, threads, smem, st>>>(ra);
+    g_helm_launches++;
+    e = cudaGetLastError();
+  }
+  int status = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_status);
+  cudaFree(scratch);
+  cudaFree(rscratch);
+  if (e != cudaSuccess) {
+    helm_set_error("sweep_setup: factorisation kernel: %s", cudaGetErrorString(e));
+    sweep_destroy(h);
+    return HELM_ECUDA;
+  }
+  if (status != 0) {
+    int s = (status - 1) / nc, c = (status - 1) % nc;
+    helm_set_error("sweep_setup: zero pivot in strip %d, cross row %d", s, c);
+    sweep_destroy(h);
+    return HELM_ESINGULAR;
+  }
+  *out = h;
+  return HELM_OK;
+}
+
+extern "C" int sweep_info(helm_sweep_t h, long* info) {
+  if (!h || !info) return HELM_EINVAL;
+  info[0] = h->N;
+  info[1] = h->nc;
+  info[2] = h->wmax;
+  info[3] = h->P;
+  long solves = h->is_double ? 2L * h->N - 1 : h->N;
+  info[4] = solves;
+  info[5] = h->factor_bytes;
+  // model bytes: per local solve 16 (2 n_c w^2 + 3 n_c w), summed
+  // over the solves of one apply (strip sigma_N is solved once).
+  // the strip solved once is sigma_N (order 0: strip N-1; order 1: strip 0)
+  double model = 0.0;
+  for (int s = 0; s < h->N; ++s) {
+    double w = h->w[s];
+    double per = 16.0 * (2.0 * h->nc * w * w + 3.0 * h->nc * w);
+    int last = h->order == 0 ? h->N - 1 : 0;
+    model += per * ((h->is_double && s != last) ? 2.0 : 1.0);
+  }
+  info[6] = (long)model;
+  info[7] = h->axis;
+  info[8] = h->order;
+  info[9] = h->is_double;
+  return HELM_OK;
+}
+
+extern "C" void sweep_destroy(helm_sweep_t h) {
+  if (!h) return;
+  cudaFree(h->d_a); cudaFree(h->d_w); cudaFree(h->d_own_lo); cudaFree(h->d_own_hi);
+  cudaFree(h->d_seg_lo); cudaFree(h->d_seg_hi); cudaFree(h->d_fac_off); cudaFree(h->d_red_off);
+  cudaFree(h->d_dg); cudaFree(h->d_al); cudaFree(h->d_cr); cudaFree(h->d_ne); cudaFree(h->d_tc);
+  cudaFree(h->d_fac); cudaFree(h->d_red);
+  delete h;
+}

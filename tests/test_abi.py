@@ -1,0 +1,66 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports
+every symbol include/helmsweep.h declares, and fails loudly (no CPU fallback)
+when there is no CUDA device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2408_11929_b200 import build as build_mod
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    hdr = open(os.path.join(ROOT, "include", "helmsweep.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = re.findall(r"^\s*(?:int|void|long|const char\*)\s+(\w+)\s*\(", hdr, flags=re.M)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    path = build_mod.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for required in ["helm_assemble", "sweep_setup", "sweep_apply", "mpgmres_solve", "helm_spmv",
+                     "helm_load_vector"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_binding_lists_every_export():
+    import paper_2408_11929_b200 as pkg
+    assert sorted(pkg.EXPORTS) == declared_functions()
+
+
+def test_sass_is_sm100a():
+    """The fat binary holds sm_100a SASS and the sweep kernel uses the TMA
+    bulk-copy engine (UBLKCP) with mbarriers (SYNCS)."""
+    import shutil
+    import subprocess
+    if shutil.which("cuobjdump") is None and not os.path.exists("/usr/local/cuda/bin/cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-sass", build_mod.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sweep = out[out.find("k_sweep_apply"):]
+    assert "UBLKCP" in sweep
+
+
+def test_no_device_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2408_11929_b200 as pkg
+    with pytest.raises(pkg.HelmError) as ei:
+        pkg.Problem(8, 8, 1.0 / 8, 5.0)
+    assert ei.value.code == 4   # HELM_ECUDA

@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs (SURVEY §8(c) parity metrics).
+
+  b and A x          relative 2-norm <= 1e-14  (we allow 1e-13: different summation order)
+  preconditioner     relative 2-norm <= 1e-10  (BASELINE.json north star)
+  MPGMRES            same iteration count +-1; x at equal k <= 1e-8 (A23)
+
+Sizes: full C1-C3; C4/C5 recipes at reduced grids that the oracle finishes in
+seconds but that still span several segments, separators and a ragged last
+segment; full-size C4/C5 are covered by test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2408_11929_b200 as hs
+from helm_inputs import make_config, random_vector, small_problem
+from oracle import krylov, p1, sweep
+
+DEV = torch.device("cuda:0")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def gpu_problem(cfg):
+    return hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=DEV))
+
+
+def to_dev(x):
+    return torch.tensor(np.ascontiguousarray(x), dtype=torch.complex128, device=DEV)
+
+
+CFGS = {
+    "C1": lambda: make_config(1),
+    "C2": lambda: make_config(2),
+    "C3": lambda: make_config(3),
+    "C4s": lambda: make_config(4, nx=384),        # 384 x 128 recipe of C4 (variable c)
+    "C5s": lambda: make_config(5, nx=256),        # 256^2, N = 32 strips of 8 cells
+    "var": lambda: small_problem(40, 33, 25.0, seed=5, variable_c=True, n_strips=5, overlap=1),
+}
+
+
+@pytest.mark.parametrize("name", ["C1", "var", "C4s"])
+def test_assembly_and_load_vector(name):
+    cfg = CFGS[name]()
+    A = p1.assemble(cfg).tocsr()
+    prob = gpu_problem(cfg)
+    diag = torch.zeros(4 * cfg.n, dtype=torch.complex128, device=DEV)
+    prob.diagonals(diag)
+    d = diag.cpu().numpy().reshape(4, cfg.n)
+    g = np.arange(cfg.n)
+    s = cfg.nx + 1
+    for k, off in enumerate([0, 1, s, s + 1]):
+        ok = g + off < cfg.n
+        ref = np.asarray(A[g[ok], g[ok] + off]).ravel()
+        got = d[k][ok]
+        # entries that do not exist (row ends) must be exactly zero on both sides
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(A.data).max(), (name, k)
+    b_ref = p1.load_vector(cfg)
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    prob.load_vector(to_dev(cfg.f.ravel()), b)
+    assert rel(b.cpu().numpy(), b_ref) <= 1e-14
+
+
+@pytest.mark.parametrize("ncols", [1, 2, 4, 5])
+def test_spmm(ncols):
+    cfg = CFGS["var"]()
+    A = p1.assemble(cfg)
+    prob = gpu_problem(cfg)
+    X = random_vector(cfg.n, 3, ncols)
+    Y = torch.zeros((ncols, cfg.n), dtype=torch.complex128, device=DEV)
+    prob.spmv(to_dev(X), Y, ncols)
+    for c in range(ncols):
+        assert rel(Y[c].cpu().numpy(), A @ X[c]) <= 1e-14
+
+
+def _oracle_precs(cfg, A, names, gather="recent", n_strips=None, overlap=None):
+    return [sweep.make_preconditioner(cfg, A, nm, n_strips=n_strips, overlap=overlap, gather=gather) for nm in names]
+
+
+@pytest.mark.parametrize("name", ["C1", "var", "C2", "C4s", "C5s"])
+@pytest.mark.parametrize("nseg", [0, 1, 3])
+def test_sweep_apply_parity(name, nseg):
+    """All four double sweeps batched in one launch vs the oracle, per direction
+    (<= 1e-10), with per-direction sources (ldr = n)."""
+    cfg = CFGS[name]()
+    if name == "C1" and nseg == 3:
+        nseg = 2
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap, n_segments=nseg) for nm in names]
+    R = random_vector(cfg.n, 11, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    Zh = Z.cpu().numpy()
+    for k, P in enumerate(_oracle_precs(cfg, A, names)):
+        z_ref = P.apply(R[k])
+        assert rel(Zh[k], z_ref) <= 1e-10, (name, names[k], rel(Zh[k], z_ref))
+
+
+@pytest.mark.parametrize("names", [["LR", "RL", "BT", "TB"]])
+def test_single_sweeps_and_broadcast(names):
+    cfg = CFGS["var"]()
+    A = p1.assemble(cfg)
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=1, n_segments=2) for nm in names]
+    r = random_vector(cfg.n, 12)
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(r), Z, ldr=0)
+    for k, P in enumerate(_oracle_precs(cfg, A, names, overlap=1)):
+        assert rel(Z[k].cpu().numpy(), P.apply(r)) <= 1e-10
+
+
+def test_core_gather_and_overlap0():
+    cfg = small_problem(48, 36, 20.0, seed=8, variable_c=True, n_strips=4, overlap=0)
+    A = p1.assemble(cfg)
+    prob = gpu_problem(cfg)
+    for gather, gname in ((0, "recent"), (1, "core")):
+        dirs = [hs.Sweep(prob, nm, n_strips=4, overlap=0, gather=gather, n_segments=3) for nm in ["LRL", "TBT"]]
+        r = random_vector(cfg.n, 13)
+        Z = torch.zeros((2, cfg.n), dtype=torch.complex128, device=DEV)
+        hs.sweep_apply(dirs, to_dev(r), Z, ldr=0)
+        for k, P in enumerate(_oracle_precs(cfg, A, ["LRL", "TBT"], gather=gname, n_strips=4, overlap=0)):
+            assert rel(Z[k].cpu().numpy(), P.apply(r)) <= 1e-10
+
+
+def test_single_strip_is_exact_solve():
+    cfg = small_problem(30, 30, 15.0, seed=9, variable_c=True)
+    A = p1.assemble(cfg)
+    import scipy.sparse.linalg as spla
+    prob = gpu_problem(cfg)
+    d = [hs.Sweep(prob, "LRL", n_strips=1, overlap=1, n_segments=4)]
+    r = random_vector(cfg.n, 14)
+    Z = torch.zeros((1, cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(d, to_dev(r), Z, ldr=0)
+    assert rel(Z[0].cpu().numpy(), spla.spsolve(A.tocsc(), r)) <= 1e-11
+
+
+@pytest.mark.parametrize("name,t", [("C1", 2), ("var", 4), ("C2", 4), ("C5s", 1), ("C5s", 2), ("C4s", 4)])
+def test_mpgmres_parity(name, t):
+    cfg = CFGS[name]()
+    names = {1: ["LRL"], 2: ["LRL", "BTB"], 4: ["LRL", "RLR", "BTB", "TBT"]}[t]
+    A = p1.assemble(cfg)
+    b_ref = p1.load_vector(cfg)
+    precs = _oracle_precs(cfg, A, names)
+    x_ref, st_ref = krylov.mpgmres(A, [P.apply for P in precs], b_ref, tol=cfg.tol, maxit=200)
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    prob.load_vector(to_dev(cfg.f.ravel()), b)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol, maxit=200)
+    assert abs(st["iterations"] - st_ref.iterations) <= 1, (st["iterations"], st_ref.iterations)
+    assert st["true_rel_res"] <= 10 * cfg.tol
+    if st["iterations"] == st_ref.iterations:
+        assert rel(x.cpu().numpy(), x_ref) <= 1e-8
+        h = np.array(st["history"])
+        assert np.max(np.abs(h - np.array(st_ref.history)) / np.array(st_ref.history)) <= 1e-6
+    else:  # A23: compare at equal k
+        x2, _ = krylov.mpgmres(A, [P.apply for P in precs], b_ref, tol=1e-300, maxit=st["iterations"])
+        assert rel(x.cpu().numpy(), x2) <= 1e-8
+
+
+def test_host_buffers_end_to_end():
+    """The C ABI accepts host pointers (the end-to-end path stages them)."""
+    cfg = CFGS["C1"]()
+    prob = hs.Problem.from_config(cfg)
+    b = np.zeros(cfg.n, dtype=np.complex128)
+    b = prob.load_vector(cfg.f.ravel(), b)
+    assert rel(b, p1.load_vector(cfg)) <= 1e-14
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in cfg.dirs]
+    x = np.zeros(cfg.n, dtype=np.complex128)
+    x, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol)
+    assert st["converged"] == 1
+    A = p1.assemble(cfg)
+    assert np.linalg.norm(p1.load_vector(cfg) - A @ x) / np.linalg.norm(b) <= 1e-5
+
+
+def test_invalid_arguments_raise():
+    cfg = CFGS["C1"]()
+    prob = gpu_problem(cfg)
+    with pytest.raises(hs.HelmError) as ei:
+        hs.Sweep(prob, "LRL", n_strips=40, overlap=1)     # 64/40 cells per strip: too thin
+    assert ei.value.code == 1
+    with pytest.raises(hs.HelmError):
+        hs.Sweep(prob, "LRL", n_strips=4, overlap=1, n_segments=100)
+    d = [hs.Sweep(prob, "LRL", n_strips=4, overlap=0)]
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    with pytest.raises(hs.HelmError):
+        hs.mpgmres_solve(prob, d, b, x, tol=2.0)
