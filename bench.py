@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (BASELINE.json metric) on synthetic C5 inputs.
+
+One step = one whole time-to-solution of config C5 (1024^2 P1 grid, k = 400,
+32 strips, l = 1, t = 4 double sweeps LRL+RLR+BTB+TBT, MPGMRES to 1e-6):
+helm_assemble -> sweep_setup x 4 -> mpgmres_solve (every iteration: sources,
+one batched 4-direction sweep_apply launch, SpMM, BCGS2 + block QR, host LSQ)
+-> x.  `value` = sweep-preconditioner applies per second over the whole step
+(t x iterations / step time, setup included); ms_per_step is the
+time-to-solution.  Inputs (c, f) are resident in HBM when the timed region
+starts; the factor set (1.3 GB) is larger than L2, so no explicit flush.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5]
+
+N > 1 (torchrun): independent replicas per rank ("replicas only", DESIGN.md
+§8; scaling weak), timed by CUDA events, max over ranks.
+--impl reference: the CPU oracle (oracle/) timed on this host on a bounded
+sample of the same workload, extrapolated to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sweep-precond applies/s + MPGMRES time-to-solve; HBM GB/s as % of peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2408_11929_b200 as hs
+    from helm_inputs import make_config
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    cfg = make_config(args.config)
+    names = cfg.dirs
+    t = len(names)
+    c_dev = torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev)
+    f_dev = torch.tensor(cfg.f.ravel(), dtype=torch.complex128, device=dev)
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=dev)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    last = {}
+
+    def step():
+        prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, c_dev)
+        t0 = time.perf_counter()
+        dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+        t1 = time.perf_counter()
+        prob.load_vector(f_dev, b)
+        _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol, maxit=cfg.maxit)
+        last.update(st=st, setup_s=t1 - t0, dirs_info=[d.info() for d in dirs])
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    l0 = hs.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    its, sweep_ms, spmv_ms, orth_ms, setup_s = [], 0.0, 0.0, 0.0, 0.0
+    for _ in range(args.steps):
+        st = step()
+        its.append(st["iterations"])
+        sweep_ms += st["sweep_ms"]
+        spmv_ms += st["spmv_ms"]
+        orth_ms += st["orth_ms"]
+        setup_s += last["setup_s"]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = hs.kernel_launches() - l0
+    clocks = sampler.stop()
+    total_ms = ev0.elapsed_time(ev1)
+    if pg:
+        tt = torch.tensor([total_ms], device=dev)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    applies = sum(its) * t * ws
+    value = applies / (total_ms / 1e3)
+    ms_step = total_ms / args.steps
+    st = last["st"]
+    # roofline of the dominant kernel (k_sweep_apply, one launch per iteration)
+    model_bytes = sum(i.model_bytes_per_apply for i in last["dirs_info"])
+    n_sweeps = sum(its)
+    avg_sweep_ms = sweep_ms / max(n_sweeps, 1)
+    achieved = model_bytes / (avg_sweep_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            tr = json.load(fh)
+        if tr.get("config") == cfg.name:
+            traffic = tr.get("dram_bytes_per_launch")
+    out = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "applies/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128 (f64 complex)",
+        "data": "synthetic (helm_inputs seeded recipe of " + cfg.name + ")",
+        "config": {"workload": f"{cfg.name}: P1 {cfg.nx}x{cfg.ny} k={cfg.omega:g}, N={cfg.n_strips} strips l={cfg.overlap}, "
+                               f"t={t} ({'+'.join(names)}), MPGMRES tol {cfg.tol:g}, x0=0; step = assemble + "
+                               "4 sweep setups + solve",
+                   "n_unknowns": cfg.n, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2_policy": "no flush: factor set %.2f GB >> 126 MB L2" % (sum(i.factor_bytes for i in last["dirs_info"]) / 1e9)},
+        "time_to_solution_ms": round(ms_step, 3),
+        "iterations": its[-1],
+        "setup_ms_avg": round(setup_s / args.steps * 1e3, 3),
+        "sweep_apply_ms_avg": round(avg_sweep_ms, 4),
+        "spmm_ms_avg": round(spmv_ms / max(n_sweeps, 1), 4),
+        "orth_ms_avg": round(orth_ms / max(n_sweeps, 1), 4),
+        "true_rel_res": st["true_rel_res"],
+        "roofline": {"kernel": "k_sweep_apply (t=4 batched double sweeps, one launch/iteration)",
+                     "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "model_bytes_per_launch": model_bytes,
+                     "model": "SURVEY 8(d): sum over local solves of 16(2 n_c w^2 + 3 n_c w)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if not args.no_e2e and ws == 1:
+        out["e2e"] = run_e2e(args, cfg, names)
+    if rank == 0 and not args.no_cpu_baseline and ws == 1:
+        out["cpu_baseline"] = oracle_baseline(cfg, names, its[-1], sample_solves=3)
+    if rank == 0:
+        print(json.dumps(out))
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def run_e2e(args, cfg, names):
+    """Same metric through the C ABI with HOST buffers: pinned host c and f are
+    copied in, x is copied back, every step, inside the timed region."""
+    import numpy as np
+    import torch
+
+    import paper_2408_11929_b200 as hs
+
+    t = len(names)
+    c_h = torch.tensor(cfg.c.ravel(), dtype=torch.float64).pin_memory()
+    f_h = torch.tensor(cfg.f.ravel(), dtype=torch.complex128).pin_memory()
+    x_h = torch.zeros(cfg.n, dtype=torch.complex128).pin_memory()
+    b_d = torch.zeros(cfg.n, dtype=torch.complex128, device="cuda")
+
+    def step():
+        prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, c_h.numpy())
+        dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+        prob.load_vector(f_h.numpy(), b_d)
+        _, st = hs.mpgmres_solve(prob, dirs, b_d, x_h.numpy(), tol=cfg.tol, maxit=cfg.maxit)
+        return st["iterations"]
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    its = [step() for _ in range(max(1, min(args.steps, 3)))]
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"value": round(sum(its) * t / dt, 3), "unit": "applies/s",
+            "h2d_bytes_per_step": 8 * cfg.n + 16 * cfg.n, "d2h_bytes_per_step": 16 * cfg.n,
+            "ms_per_step": round(dt / len(its) * 1e3, 3),
+            "path": "helm_assemble(host c) + sweep_setup x4 + helm_load_vector(host f) + mpgmres_solve(x to host)"}
+
+
+def oracle_baseline(cfg, names, iterations, sample_solves=3):
+    """The CPU oracle as it stands, timed on this host on a bounded sample of
+    the same workload: factor (splu) and solve a few C5 strips, extrapolate
+    to the metric (setup of all strips + iterations x t double sweeps of
+    2N-1 strip solves each)."""
+    import numpy as np
+
+    from helm_inputs import random_vector
+    from oracle import p1, sweep
+    from oracle import strips as st_mod
+
+    t0 = time.perf_counter()
+    A = p1.assemble(cfg)
+    t_asm = time.perf_counter() - t0
+    _, strips_x = st_mod.strips(cfg, 0, cfg.n_strips, cfg.overlap)
+    mid = cfg.n_strips // 2
+    picks = [strips_x[mid + k] for k in range(2)]
+    fac_t, sol_t = [], []
+    r = random_vector(cfg.n, 77)
+    for stp in picks:
+        t1 = time.perf_counter()
+        S = sweep.StripSolver(cfg, 0, stp, A)
+        fac_t.append(time.perf_counter() - t1)
+        rl = r[stp.nodes]
+        for _ in range(sample_solves):
+            t2 = time.perf_counter()
+            S.solve(rl)
+            sol_t.append(time.perf_counter() - t2)
+    N = cfg.n_strips
+    t = len(names)
+    setup = t_asm + 2 * N * float(np.mean(fac_t))       # both axes (LRL/RLR, BTB/TBT share strips)
+    apply_s = (2 * N - 1) * float(np.mean(sol_t))
+    total = setup + iterations * t * apply_s
+    sample_s = time.perf_counter() - t0
+    return {"value": round(iterations * t / total, 6), "unit": "applies/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle assembly of {cfg.name} + splu factor of 2 interior x-strips + "
+                      f"{sample_solves} solves each ({sample_s:.1f} s of CPU work), extrapolated to "
+                      f"setup of 2N={2*N} strips + {iterations} iterations x t={t} x (2N-1)={2*N-1} strip solves",
+            "oracle_apply_s": round(apply_s, 3), "oracle_setup_s": round(setup, 3),
+            "oracle_time_to_solution_s": round(total, 3)}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from helm_inputs import make_config
+    cfg = make_config(args.config)
+    names = cfg.dirs
+    iters_assumed = 13    # the oracle's own count on C5 t=4 is not run here (bounded sample); DESIGN.md §7
+    vals = []
+    t_all = time.perf_counter()
+    for k in range(args.warmup + args.steps):
+        b = oracle_baseline(cfg, names, iters_assumed, sample_solves=1)
+        if k >= args.warmup:
+            vals.append(b)
+    dt = time.perf_counter() - t_all
+    v = sum(x["value"] for x in vals) / len(vals)
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "applies/s", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(1e3 * sum(x["oracle_time_to_solution_s"] for x in vals) / len(vals), 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
+           "data": "synthetic (helm_inputs seeded recipe of " + cfg.name + ")",
+           "config": {"workload": f"{cfg.name}: same workload as the GPU arm; CPU oracle (numpy/scipy splu)",
+                      "n_unknowns": cfg.n},
+           "cpu_baseline": {"value": round(v, 6), "unit": "applies/s", "cores": 1, "kind": "oracle",
+                            "sample": vals[-1]["sample"] + f"; assumes {iters_assumed} iterations"},
+           "e2e": {"value": round(v, 6), "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": round(dt, 1)}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -279,6 +279,7 @@ extern "C" int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols
 
 extern "C" void helm_problem_destroy(helm_problem_t p) {
   if (!p) return;
+  helm_problem_free_ws(p);
   cudaFree(p->c);
   cudaFree(p->dC);
   cudaFree(p->dE);

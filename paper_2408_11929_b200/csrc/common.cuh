@@ -78,7 +78,9 @@ struct helm_problem_s {
   cplx* dE;
   cplx* dN;
   cplx* dNE;
+  void* ws = nullptr;  // cached MPGMRES workspace (krylov.cu), grown on demand
 };
+void helm_problem_free_ws(helm_problem_s* p);
 
 // One sweep preconditioner (one direction): strips + factors, all on device.
 struct helm_sweep_s {

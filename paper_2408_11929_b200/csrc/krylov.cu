@@ -250,6 +250,108 @@ struct HouseholderLSQ {
 
 }  // namespace
 
+// ------------------------------------------------------------------ device-side block QR helpers
+// scale[i] = keep ? 1/||w_i|| : 0 with the deflation rule of D10 step 5
+// (drop if ||w_i|| <= 1e-10 ||A z_i||, ||A z_i|| from the Gram diagonal).
+__global__ void k_decide(const cplx* nn, const cplx* gram, int t, int i, double* scale, double* nrm_out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double nrm = sqrt(fmax(nn[0].x, 0.0));
+    double naz = sqrt(fmax(gram[i * t + i].x, 0.0));
+    bool keep = nrm > 1e-10 * naz;
+    scale[i] = keep ? 1.0 / nrm : 0.0;
+    nrm_out[i] = nrm;
+  }
+}
+
+__global__ void k_scale_dev(long n, const cplx* __restrict__ x, const double* __restrict__ s, int i,
+                            cplx* __restrict__ y) {
+  const double a = s[i];
+  for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < n; r += (long)gridDim.x * blockDim.x)
+    y[r] = cscale(x[r], a);
+}
+
+// ------------------------------------------------------------------ workspace
+// The solve workspace lives with the problem handle and is reused across
+// solves (grown on demand): V (n x (1 + icap t)), Z (n x icap t), W, sources,
+// dot partials and pinned host mirrors.  No per-solve allocation.
+struct KrylovWS {
+  long n = 0;
+  int icap = 0, tcap = 0;
+  cplx *V = nullptr, *Z = nullptr, *W = nullptr, *Rsrc = nullptr, *tmp = nullptr, *partial = nullptr;
+  cplx *dC1 = nullptr, *dC2 = nullptr, *dsm = nullptr, *dy = nullptr;
+  double* dscal = nullptr;
+  cplx* hsmall = nullptr;
+  size_t small_cap = 0;
+  long partial_cap = 0;
+};
+
+static void ws_free(KrylovWS* w) {
+  if (!w) return;
+  cudaFree(w->V); cudaFree(w->Z); cudaFree(w->W); cudaFree(w->Rsrc); cudaFree(w->tmp);
+  cudaFree(w->partial); cudaFree(w->dC1); cudaFree(w->dC2); cudaFree(w->dsm); cudaFree(w->dy);
+  cudaFree(w->dscal);
+  if (w->hsmall) cudaFreeHost(w->hsmall);
+  delete w;
+}
+
+void helm_problem_free_ws(helm_problem_s* p) {
+  ws_free(reinterpret_cast<KrylovWS*>(p->ws));
+  p->ws = nullptr;
+}
+
+// ensure capacity for `iters` iterations of t columns; preserves the first
+// `keepV` V columns and `keepZ` Z columns
+static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keepZ, cudaStream_t st) {
+  KrylovWS* w = reinterpret_cast<KrylovWS*>(p->ws);
+  if (!w) { w = new KrylovWS(); p->ws = w; w->n = p->n; }
+  const long n = p->n;
+  cudaError_t e = cudaSuccess;
+  if (t > w->tcap) {
+    cudaFree(w->W); cudaFree(w->Rsrc); cudaFree(w->tmp); cudaFree(w->dscal);
+    w->W = w->Rsrc = w->tmp = nullptr; w->dscal = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc(&w->W, sizeof(cplx) * n * t);
+    if (e == cudaSuccess) e = cudaMalloc(&w->Rsrc, sizeof(cplx) * n * t);
+    if (e == cudaSuccess) e = cudaMalloc(&w->tmp, sizeof(cplx) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&w->dscal, sizeof(double) * 16);
+    w->tcap = t;
+    w->icap = 0;   // column capacities depend on t
+  }
+  if (e == cudaSuccess && (long)iters * t > (long)w->icap * w->tcap) {
+    const long vc = 1 + (long)iters * t, zc = (long)iters * t;
+    cplx *V2 = nullptr, *Z2 = nullptr;
+    e = cudaMalloc(&V2, sizeof(cplx) * n * vc);
+    if (e == cudaSuccess) e = cudaMalloc(&Z2, sizeof(cplx) * n * zc);
+    if (e == cudaSuccess && keepV > 0) e = cudaMemcpyAsync(V2, w->V, sizeof(cplx) * n * keepV, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && keepZ > 0) e = cudaMemcpyAsync(Z2, w->Z, sizeof(cplx) * n * keepZ, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      cudaFree(V2); cudaFree(Z2);
+      helm_set_error("mpgmres_solve: basis of %ld columns: %s", vc, cudaGetErrorString(e));
+      return HELM_ENOMEM;
+    }
+    cudaFree(w->V); cudaFree(w->Z);
+    w->V = V2; w->Z = Z2;
+    cudaFree(w->dC1); cudaFree(w->dC2); cudaFree(w->dsm); cudaFree(w->dy); cudaFree(w->partial);
+    w->dC1 = w->dC2 = w->dsm = w->dy = w->partial = nullptr;
+    if (w->hsmall) cudaFreeHost(w->hsmall);
+    w->hsmall = nullptr;
+    w->partial_cap = ((n + kDotChunk - 1) / kDotChunk) * kMaxT * vc * t;
+    w->small_cap = 4 * vc * t + 64;
+    e = cudaMalloc(&w->dC1, sizeof(cplx) * vc * t);
+    if (e == cudaSuccess) e = cudaMalloc(&w->dC2, sizeof(cplx) * vc * t);
+    if (e == cudaSuccess) e = cudaMalloc(&w->dsm, sizeof(cplx) * w->small_cap);
+    if (e == cudaSuccess) e = cudaMalloc(&w->dy, sizeof(cplx) * zc);
+    if (e == cudaSuccess) e = cudaMalloc(&w->partial, sizeof(cplx) * w->partial_cap);
+    if (e == cudaSuccess) e = cudaMallocHost(&w->hsmall, sizeof(cplx) * w->small_cap);
+    w->icap = (int)(zc / t);
+  }
+  if (e != cudaSuccess) {
+    helm_set_error("mpgmres_solve: workspace: %s", cudaGetErrorString(e));
+    return HELM_ENOMEM;
+  }
+  return HELM_OK;
+}
+
 extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int t, const double* b_in,
                              double* x_out, double tol, int maxit, mpgmres_stats* stats, void* stream) {
   typedef std::complex<double> C;
@@ -269,17 +371,17 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
   const cplx* b = (const cplx*)sb.dev;
   cplx* x = (cplx*)sx.dev;
 
-  const long vcols = 1 + (long)maxit * t;
-  const long zcols = (long)maxit * t;
-  cplx *V = nullptr, *Z = nullptr, *W = nullptr, *Rsrc = nullptr, *tmp = nullptr;
-  cplx *dC1 = nullptr, *dC2 = nullptr, *dc = nullptr, *dy = nullptr;
+  int rc = ws_reserve(prob, t, std::min(maxit, 24), 0, 0, st);
+  if (rc != HELM_OK) { helm_stage_free(sb, st); helm_stage_free(sx, st); return rc; }
+  KrylovWS* ws = reinterpret_cast<KrylovWS*>(prob->ws);
   Work wk;
   wk.n = n;
   wk.st = st;
-  wk.nblk = (int)((n + kDotChunk - 1) / kDotChunk) * kMaxT;  // upper bound over t
-  cudaEvent_t ev[8];
+  wk.partial = ws->partial;
+  wk.hsmall = ws->hsmall;
+  wk.small_cap = ws->small_cap;
+  cudaEvent_t ev[4];
   for (auto& e : ev) cudaEventCreate(&e);
-  int rc = HELM_OK;
   double sweep_ms = 0, spmv_ms = 0, orth_ms = 0;
   long inner = 0;
   int deflations = 0;
@@ -287,25 +389,8 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
   int k_done = 0;
   bool converged = false, exhausted = false;
   double rho = 1.0, true_res = NAN;
-
-  auto fail = [&](int code) { rc = code; };
   cudaError_t e = cudaSuccess;
-  e = cudaMallocAsync((void**)&V, sizeof(cplx) * n * vcols, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&Z, sizeof(cplx) * n * zcols, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&W, sizeof(cplx) * n * t, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&Rsrc, sizeof(cplx) * n * t, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&tmp, sizeof(cplx) * n, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&wk.partial, sizeof(cplx) * (size_t)wk.nblk * vcols * t, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&dC1, sizeof(cplx) * vcols * t, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&dC2, sizeof(cplx) * vcols * t, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&dc, sizeof(cplx) * 64, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&dy, sizeof(cplx) * zcols, st);
-  wk.small_cap = (size_t)vcols * t + zcols + 64;
-  if (e == cudaSuccess) e = cudaMallocHost((void**)&wk.hsmall, sizeof(cplx) * wk.small_cap);
-  if (e != cudaSuccess) {
-    helm_set_error("mpgmres_solve: allocation (%ld x %ld complex basis): %s", n, vcols, cudaGetErrorString(e));
-    rc = HELM_ENOMEM;
-  }
+
   std::vector<C> hv;
   HouseholderLSQ lsq;
   std::vector<int> tags;        // origin tag of each V column (-1 for v1)
@@ -313,28 +398,41 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
   long nz = 0;                  // #Z columns
   double beta = 0;
   std::vector<C> y;
+  // small device results, packed in ws->dsm: [gram t*t][cv 2*t*t][nn t]
+  cplx* d_gram = ws->dsm;
+  cplx* d_cv = d_gram + t * t;
+  cplx* d_nn = d_cv + 2 * t * t;
+  double* d_nrm = ws->dscal + 8;
+  // beta = ||b||, V1 = b / beta
+  rc = dots(wk, b, n, 1, b, n, 1, d_nn, false);
+  if (rc == HELM_OK) rc = to_host(wk, d_nn, 1, hv);
   if (rc == HELM_OK) {
-    // beta = ||b||, V1 = b / beta
-    rc = dots(wk, b, n, 1, b, n, 1, dc, false);
-    if (rc == HELM_OK) rc = to_host(wk, dc, 1, hv);
-    if (rc == HELM_OK) {
-      beta = std::sqrt(hv[0].real());
-      if (beta == 0.0) {
-        cudaMemsetAsync(x, 0, sizeof(cplx) * n, st);
-        converged = true;
-        rho = 0.0;
-        true_res = 0.0;
-      } else {
-        k_scale<<<grid_for(n), 256, 0, st>>>(n, b, cmk(1.0 / beta, 0.0), V);
-        g_helm_launches++;
-        tags.push_back(-1);
-        mV = 1;
-        blk_start = 0;
-        lsq.init(beta);
-      }
+    beta = std::sqrt(hv[0].real());
+    if (beta == 0.0) {
+      cudaMemsetAsync(x, 0, sizeof(cplx) * n, st);
+      converged = true;
+      rho = 0.0;
+      true_res = 0.0;
+    } else {
+      k_scale<<<grid_for(n), 256, 0, st>>>(n, b, cmk(1.0 / beta, 0.0), ws->V);
+      g_helm_launches++;
+      tags.push_back(-1);
+      mV = 1;
+      blk_start = 0;
+      lsq.init(beta);
     }
   }
   for (int k = 1; rc == HELM_OK && !converged && k <= maxit; ++k) {
+    if (k > ws->icap) {
+      rc = ws_reserve(prob, t, std::min(maxit, 2 * ws->icap), mV, nz, st);
+      if (rc != HELM_OK) break;
+      wk.partial = ws->partial; wk.hsmall = ws->hsmall; wk.small_cap = ws->small_cap;
+      d_gram = ws->dsm; d_cv = d_gram + t * t; d_nn = d_cv + 2 * t * t;
+    }
+    cplx* V = ws->V;
+    cplx* Z = ws->Z;
+    cplx* W = ws->W;
+    cplx* Rsrc = ws->Rsrc;
     // ---- a3: source selection (A19)
     const cplx* src = nullptr;
     long ldr = 0;
@@ -362,7 +460,7 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
       g_helm_launches++;
       src = Rsrc;
     }
-    // ---- a4: Z_k = [M_i^{-1} src_i]
+    // ---- a4: Z_k = [M_i^{-1} src_i], one batched launch
     cplx* Zk = Z + nz * n;
     cudaEventRecord(ev[0], st);
     rc = sweep_apply_dev(dirs, t, src, ldr, Zk, n, st);
@@ -372,61 +470,65 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
     rc = helm_spmm_dev(prob, Zk, W, t, n, st);
     if (rc != HELM_OK) break;
     cudaEventRecord(ev[2], st);
-    // ---- a6: norms of A z_i, BCGS2 against V_1..k
-    rc = dots(wk, W, n, t, W, n, t, dc, false);
-    if (rc != HELM_OK) break;
+    // ---- a6: Gram of A Z_k (for ||A z_i||), BCGS2 against V_1..k
     const int m = (int)mV;
-    rc = dots(wk, V, n, m, W, n, t, dC1, false);
-    if (rc == HELM_OK) rc = update(wk, V, n, m, dC1, W, n, t);
-    if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, dC2, false);
-    if (rc == HELM_OK) rc = update(wk, V, n, m, dC2, W, n, t);
+    rc = dots(wk, W, n, t, W, n, t, d_gram, false);
+    if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, ws->dC1, false);
+    if (rc == HELM_OK) rc = update(wk, V, n, m, ws->dC1, W, n, t);
+    if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, ws->dC2, false);
+    if (rc == HELM_OK) rc = update(wk, V, n, m, ws->dC2, W, n, t);
     if (rc != HELM_OK) break;
     inner += 2L * m * t;
-    std::vector<C> gram, h1, h2;
-    if ((rc = to_host(wk, dc, (size_t)t * t, gram)) != HELM_OK) break;
-    std::vector<double> nAz(t);
-    for (int i = 0; i < t; ++i) nAz[i] = std::sqrt(std::max(gram[i * t + i].real(), 0.0));
-    // intra-block CGS2 with the 1e-10 deflation rule (D10 step 5)
-    std::vector<std::vector<C>> Rb(t, std::vector<C>(t, C(0)));
-    std::vector<int> kept;
+    // intra-block CGS2 on the device: new column i is projected (twice) against
+    // slots V[:, m .. m+i); a dropped column leaves a zero slot, so later
+    // projections onto it vanish exactly as if it were skipped.
     for (int i = 0; i < t && rc == HELM_OK; ++i) {
       cplx* wi = W + (long)i * n;
-      const int nk = (int)kept.size();
-      for (int pass = 0; pass < 2 && nk > 0; ++pass) {
-        rc = dots(wk, V + mV * n, n, nk, wi, n, 1, dc, false);
-        if (rc == HELM_OK) rc = update(wk, V + mV * n, n, nk, dc, wi, n, 1);
+      for (int pass = 0; pass < 2 && i > 0; ++pass) {
+        cplx* cvi = d_cv + (long)pass * t * t + (long)i * t;
+        rc = dots(wk, V + mV * n, n, i, wi, n, 1, cvi, false);
+        if (rc == HELM_OK) rc = update(wk, V + mV * n, n, i, cvi, wi, n, 1);
         if (rc != HELM_OK) break;
-        std::vector<C> cv;
-        if ((rc = to_host(wk, dc, nk, cv)) != HELM_OK) break;
-        for (int j = 0; j < nk; ++j) Rb[kept[j]][i] += cv[j];
-        inner += nk;
       }
       if (rc != HELM_OK) break;
-      rc = dots(wk, wi, n, 1, wi, n, 1, dc, false);
-      std::vector<C> nn;
-      if (rc == HELM_OK) rc = to_host(wk, dc, 1, nn);
+      rc = dots(wk, wi, n, 1, wi, n, 1, d_nn + i, false);
       if (rc != HELM_OK) break;
-      inner += 1;
-      double nrm = std::sqrt(std::max(nn[0].real(), 0.0));
-      if (!(nrm > 1e-10 * nAz[i])) {
-        deflations++;
-        continue;
-      }
-      Rb[i][i] = nrm;
-      k_scale<<<grid_for(n), 256, 0, st>>>(n, wi, cmk(1.0 / nrm, 0.0), V + (mV + nk) * n);
-      g_helm_launches++;
-      kept.push_back(i);
+      k_decide<<<1, 32, 0, st>>>(d_nn + i, d_gram, t, i, ws->dscal, d_nrm);
+      k_scale_dev<<<grid_for(n), 256, 0, st>>>(n, wi, ws->dscal, i, V + (mV + i) * n);
+      g_helm_launches += 2;
     }
     if (rc != HELM_OK) break;
     cudaEventRecord(ev[3], st);
-    // H block column: rows 0..m-1 = C1 + C2, then one row per kept column
-    if ((rc = to_host(wk, dC1, (size_t)m * t, h1)) != HELM_OK) break;
-    if ((rc = to_host(wk, dC2, (size_t)m * t, h2)) != HELM_OK) break;
+    // ---- one device->host copy per iteration: H block, intra-block coefficients, norms
+    std::vector<C> h1, h2, small;
+    if ((rc = to_host(wk, ws->dC1, (size_t)m * t, h1)) != HELM_OK) break;
+    if ((rc = to_host(wk, ws->dC2, (size_t)m * t, h2)) != HELM_OK) break;
+    if ((rc = to_host(wk, d_gram, (size_t)(3 * t * t + t), small)) != HELM_OK) break;
+    std::vector<double> nrm(t);
+    HELM_CUDA_TRY(cudaMemcpyAsync(nrm.data(), d_nrm, sizeof(double) * t, cudaMemcpyDeviceToHost, st));
+    HELM_CUDA_TRY(cudaStreamSynchronize(st));
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[0], ev[1]); sweep_ms += ms;
     cudaEventElapsedTime(&ms, ev[1], ev[2]); spmv_ms += ms;
     cudaEventElapsedTime(&ms, ev[2], ev[3]); orth_ms += ms;
+    const C* gram = small.data();
+    const C* cv = gram + t * t;
+    std::vector<int> kept;
+    std::vector<std::vector<C>> Rb(t, std::vector<C>(t, C(0)));
+    for (int i = 0; i < t; ++i) {
+      double naz = std::sqrt(std::max(gram[i * t + i].real(), 0.0));
+      for (int j = 0; j < i; ++j) Rb[j][i] = cv[i * t + j] + cv[t * t + i * t + j];
+      inner += 2L * i + 1;
+      if (!(nrm[i] > 1e-10 * naz)) { deflations++; continue; }
+      Rb[i][i] = nrm[i];
+      kept.push_back(i);
+    }
     const int nk = (int)kept.size();
+    // compact the kept slots to V[:, m .. m+nk)
+    for (int jj = 0; jj < nk; ++jj)
+      if (kept[jj] != jj)
+        cudaMemcpyAsync(V + (mV + jj) * n, V + (mV + kept[jj]) * n, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st);
+    // H block column: rows 0..m-1 = C1 + C2, then one row per kept column
     const int new_rows = (int)mV + nk;
     for (int i = 0; i < t; ++i) {
       std::vector<C> col(new_rows, C(0));
@@ -450,31 +552,28 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
   if (rc == HELM_OK && beta > 0.0 && nz > 0) {
     std::vector<cplx> yh(nz);
     for (long j = 0; j < nz; ++j) yh[j] = cmk(y[j].real(), y[j].imag());
-    e = cudaMemcpyAsync(dy, yh.data(), sizeof(cplx) * nz, cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(ws->dy, yh.data(), sizeof(cplx) * nz, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
-      k_gemv<<<grid_for(n), 256, 0, st>>>(n, Z, n, (int)nz, dy, x);
+      k_gemv<<<grid_for(n), 256, 0, st>>>(n, ws->Z, n, (int)nz, ws->dy, x);
       g_helm_launches++;
-      rc = helm_spmm_dev(prob, x, tmp, 1, n, st);
+      rc = helm_spmm_dev(prob, x, ws->tmp, 1, n, st);
       if (rc == HELM_OK) {
-        k_axpy_sub<<<grid_for(n), 256, 0, st>>>(n, b, tmp, tmp);
+        k_axpy_sub<<<grid_for(n), 256, 0, st>>>(n, b, ws->tmp, ws->tmp);
         g_helm_launches++;
-        rc = dots(wk, tmp, n, 1, tmp, n, 1, dc, false);
+        rc = dots(wk, ws->tmp, n, 1, ws->tmp, n, 1, d_nn, false);
         std::vector<C> rr;
-        if (rc == HELM_OK) rc = to_host(wk, dc, 1, rr);
+        if (rc == HELM_OK) rc = to_host(wk, d_nn, 1, rr);
         if (rc == HELM_OK) true_res = std::sqrt(std::max(rr[0].real(), 0.0)) / beta;
       }
     } else {
-      fail(HELM_ECUDA);
+      helm_set_error("mpgmres_solve: %s", cudaGetErrorString(e));
+      rc = HELM_ECUDA;
     }
   }
   if (rc == HELM_OK) {
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { helm_set_error("mpgmres_solve: %s", cudaGetErrorString(e)); rc = HELM_ECUDA; }
   }
-  cudaFreeAsync(V, st); cudaFreeAsync(Z, st); cudaFreeAsync(W, st); cudaFreeAsync(Rsrc, st);
-  cudaFreeAsync(tmp, st); cudaFreeAsync(wk.partial, st); cudaFreeAsync(dC1, st); cudaFreeAsync(dC2, st);
-  cudaFreeAsync(dc, st); cudaFreeAsync(dy, st);
-  if (wk.hsmall) cudaFreeHost(wk.hsmall);
   for (auto& ev_ : ev) cudaEventDestroy(ev_);
   helm_stage_free(sb, st);
   if (rc == HELM_OK) rc = helm_stage_out(sx, st);

@@ -54,10 +54,20 @@ struct DirArgs {
 struct ApplyArgs {
   DirArgs d[HELM_MAXDIR];
   int t;
-  int rows_per_tile;  // R_t = blockDim/8
+  int rows_per_tile;  // R_t = consumer threads / 8
   int nstage;
   int stage_elems;    // cplx per stage
-  int vec_elems;      // cplx per vector area (bseg / yseg)
+  int vec_elems;      // cplx per vector area (bseg / yseg / staged couplings)
+  int pmax;           // max segments over directions
+  int nsolve_max;     // max local solves per apply over directions
+  int vec_global;     // vector areas in global scratch (shared memory too small)
+  cplx* vec_scratch;  // per-CTA 4 * vec_elems when vec_global
+  long long* prof;    // optional per-CTA cycle counters (8 per CTA), NULL = off
+};
+
+// per-thread profiling accumulators (thread 0 reports)
+struct Prof {
+  long long peek = 0, comp = 0, bar = 0, steps = 0, xwait = 0;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -91,6 +101,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// relaxed poll (no L1 invalidation per iteration); callers fence once after success
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
@@ -134,98 +150,126 @@ __device__ __forceinline__ cplx correction(const DirArgs& D, int t, int side, in
 }
 
 // ------------------------------------------------------------------ tile pipeline
+// Warp-specialised ring: the last warp of the CTA is the TMA producer (one
+// elected lane walks the exact tile sequence the consumers will ask for and
+// issues cp.async.bulk into stage f % NS after waiting for the consumers'
+// release of fill f - NS); the consumer warps wait on full[stage], compute,
+// sync among themselves with named barrier 1, and one thread releases the
+// stage through empty[stage].  The producer therefore runs up to NS tiles
+// ahead across step, phase and solve boundaries, off the dependent chain.
 struct Ring {
-  uint64_t* bar;     // nstage mbarriers
+  uint64_t* full;    // nstage mbarriers (tx-count)
+  uint64_t* empty;   // nstage mbarriers (consumer release)
   cplx* stage;       // nstage * stage_elems
   int nstage, stage_elems, R_t;
   uint32_t kc;       // consumer tile counter
-  uint32_t kp;       // producer tile counter (thread 0)
 };
 
-__device__ __forceinline__ void ring_issue(Ring& rg, const cplx* src, uint32_t bytes) {
-  // thread 0 only
-  int sidx = rg.kp % rg.nstage;
-  mbar_expect_tx(&rg.bar[sidx], bytes);
-  bulk_g2s(rg.stage + (long)sidx * rg.stage_elems, src, bytes, &rg.bar[sidx]);
-  rg.kp++;
+__device__ __forceinline__ void cbar(int ncons) {
+  asm volatile("bar.sync 1, %0;" ::"r"(ncons) : "memory");
 }
-__device__ __forceinline__ const cplx* ring_wait(Ring& rg) {
-  int sidx = rg.kc % rg.nstage;
-  mbar_wait(&rg.bar[sidx], (rg.kc / rg.nstage) & 1);
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ const cplx* ring_peek(const Ring& rg, uint32_t k) {
+  int sidx = k % rg.nstage;
+  mbar_wait(&rg.full[sidx], (k / rg.nstage) & 1);
   return rg.stage + (long)sidx * rg.stage_elems;
 }
+// consumers: after cbar(), release `count` consumed tiles
+__device__ __forceinline__ void ring_release(Ring& rg, int count) {
+  if (threadIdx.x == 0)
+    for (int c = 0; c < count; ++c) mbar_arrive(&rg.empty[(rg.kc + c) % rg.nstage]);
+  rg.kc += count;
+}
 
-// Producer cursors: the exact tile sequence the consumer will ask for.
+// Producer cursors: the exact tile sequence the consumer will ask for.  All
+// geometry comes from registers and a per-solve table in shared memory
+// (strip width and factor base of solve i), so the producer warp issues a
+// tile in a few tens of cycles.
+struct SolveTab {
+  const cplx* fac;   // factor base of the strip solved at solve i
+  const cplx* red;   // separator-system base
+  int w;
+  int pad;
+};
 struct SegCursor {
   int i, ph, j, tt;   // solve, phase index, step, tile
+  int lo, hi, m, nph, nsolve, R_t;
+  int w, nt;
+  const cplx* fac;
   bool done;
 };
 struct RedCursor {
   int i, part, k, tt, sub;  // solve, part (0 fwd, 1 bwd), separator, tile, sub-block
+  int P, nsolve, R_t, w, nt;
+  const cplx* red;
   bool done;
 };
 
 __device__ __forceinline__ int ntile_of(int w, int R_t) { return (w + R_t - 1) / R_t; }
 
-__device__ bool seg_next_tile(const DirArgs& D, int p, int R_t, SegCursor& c, const cplx** src, uint32_t* bytes) {
+__device__ __forceinline__ void seg_load_solve(SegCursor& c, const SolveTab* tab) {
+  c.w = tab[c.i].w;
+  c.fac = tab[c.i].fac;
+  c.nt = ntile_of(c.w, c.R_t);
+}
+
+__device__ __forceinline__ bool seg_next_tile(SegCursor& c, const SolveTab* tab, const cplx** src, uint32_t* bytes) {
   if (c.done) return false;
-  const int lo = D.seg_lo[p], hi = D.seg_hi[p], m = hi - lo + 1;
-  const int nph = D.P > 1 ? 2 : 1;
-  const int s = sigma(D, step_of(D, c.i));
-  const int w = D.w[s];
-  const int nt = ntile_of(w, R_t);
-  int row = c.j < m ? lo + c.j : hi - 1 - (c.j - m);
-  int r0 = c.tt * R_t;
-  int rows = min(R_t, w - r0);
-  *src = D.fac + D.fac_off[s] + (long)row * w * w + (long)r0 * w;
+  const int w = c.w;
+  int row = c.j < c.m ? c.lo + c.j : c.hi - 1 - (c.j - c.m);
+  int r0 = c.tt * c.R_t;
+  int rows = min(c.R_t, w - r0);
+  *src = c.fac + (long)row * w * w + (long)r0 * w;
   *bytes = (uint32_t)(rows * w * sizeof(cplx));
-  // advance
-  if (++c.tt == nt) {
+  if (++c.tt == c.nt) {
     c.tt = 0;
-    if (++c.j == 2 * m - 1) {
+    if (++c.j == 2 * c.m - 1) {
       c.j = 0;
-      if (++c.ph == nph) {
+      if (++c.ph == c.nph) {
         c.ph = 0;
-        if (++c.i == n_solves(D)) c.done = true;
+        if (++c.i == c.nsolve) c.done = true;
+        else seg_load_solve(c, tab);
       }
     }
   }
   return true;
 }
 
-__device__ bool red_next_tile(const DirArgs& D, int R_t, RedCursor& c, const cplx** src, uint32_t* bytes) {
+__device__ __forceinline__ void red_load_solve(RedCursor& c, const SolveTab* tab) {
+  c.w = tab[c.i].w;
+  c.red = tab[c.i].red;
+  c.nt = ntile_of(c.w, c.R_t);
+}
+
+__device__ __forceinline__ bool red_next_tile(RedCursor& c, const SolveTab* tab, const cplx** src, uint32_t* bytes) {
   if (c.done) return false;
-  const int P = D.P;
-  const int s = sigma(D, step_of(D, c.i));
-  const int w = D.w[s];
-  const int nt = ntile_of(w, R_t);
+  const int w = c.w;
   const long w2 = (long)w * w;
-  const cplx* base = D.red + D.red_off[s];
-  int blk;  // 0 Rinv, 1 G, 2 F
-  if (c.part == 0) blk = c.sub;  // sub 0 = Rinv_k, sub 1 = G_k
-  else blk = 2;
-  int r0 = c.tt * R_t;
-  int rows = min(R_t, w - r0);
-  *src = base + ((long)c.k * 3 + blk) * w2 + (long)r0 * w;
+  const int blk = c.part == 0 ? c.sub : 2;  // 0 Rinv, 1 G, 2 F
+  int r0 = c.tt * c.R_t;
+  int rows = min(c.R_t, w - r0);
+  *src = c.red + ((long)c.k * 3 + blk) * w2 + (long)r0 * w;
   *bytes = (uint32_t)(rows * w * sizeof(cplx));
-  // advance: part 0: for k in 0..P-2: for tt: [Rinv tt, (k>=1) G tt]; part 1: for k = P-3..0: F tt
+  // part 0: for k in 0..P-2: for tt: [Rinv tt, (k>=1) G tt]; part 1: for k = P-3..0: F tt
   if (c.part == 0) {
     if (c.sub == 0 && c.k >= 1) { c.sub = 1; return true; }
     c.sub = 0;
-    if (++c.tt < nt) return true;
+    if (++c.tt < c.nt) return true;
     c.tt = 0;
-    if (++c.k <= P - 2) return true;
+    if (++c.k <= c.P - 2) return true;
     c.part = 1;
-    c.k = P - 3;
+    c.k = c.P - 3;
     if (c.k >= 0) return true;
   } else {
-    if (++c.tt < nt) return true;
+    if (++c.tt < c.nt) return true;
     c.tt = 0;
     if (--c.k >= 0) return true;
   }
-  // next solve
   c.part = 0; c.k = 0; c.tt = 0; c.sub = 0;
-  if (++c.i == n_solves(D)) c.done = true;
+  if (++c.i == c.nsolve) c.done = true;
+  else red_load_solve(c, tab);
   return true;
 }
 
@@ -233,53 +277,60 @@ __device__ bool red_next_tile(const DirArgs& D, int R_t, RedCursor& c, const cpl
 // One dependent block step over the tiles of a w x w block:
 //   acc[r] = sum_k B[r][k] * (tA[k] + tB[k])
 //   out[r] = acc (mode 0: forward, y = S^{-1} t) or ybase[r] - acc (mode 1: x = y - S^{-1} t)
-// and, in the producer lanes, the next step's input
+// and, in the writer lanes, the next step's input
 //   next 0: none; next 1 (forward-style): tA'[r] = bn[r] - crn[r] out[r], tB'[r+1] = -nen[r] out[r]
 //   next 2 (backward-style): tA'[r] = crn[r] out[r], tB'[r-1] = nen[r-1] out[r]
 struct StepIO {
-  const cplx* tA; const cplx* tB;    // inputs (smem)
-  cplx* out;                          // output row vector (smem), length w
-  const cplx* ybase;                  // mode 1 base (smem)
+  const cplx* tA; const cplx* tB;    // inputs
+  cplx* out;                          // output row vector, length w
+  const cplx* ybase;                  // mode 1 base
   int mode;
   int next;                           // 0 none, 1 fwd-style, 2 bwd-style
-  const cplx* bn;                     // next fwd rhs (smem)
-  const cplx* crn; const cplx* nen;   // next couplings (global)
-  cplx* tAn; cplx* tBn;               // next inputs (smem)
+  const cplx* bn;                     // next fwd rhs
+  const cplx* crn; const cplx* nen;   // next couplings (staged)
+  cplx* tAn; cplx* tBn;               // next inputs
 };
 
-template <class Refill>
-__device__ __forceinline__ void block_step(Ring& rg, int w, const StepIO& io, Refill refill) {
+__device__ __forceinline__ void block_step(Ring& rg, int w, int ncons, const StepIO& io, Prof& pf) {
   const int tid = threadIdx.x;
   const int ri = tid >> 3, q = tid & 7;
   const int nt = ntile_of(w, rg.R_t);
-  // prefetch next-step coefficients (independent of this step's data)
   for (int tt = 0; tt < nt; ++tt) {
     const int r0 = tt * rg.R_t;
     const int rows = min(rg.R_t, w - r0);
     const int r = r0 + ri;
-    cplx crv = cmk(0, 0), nev = cmk(0, 0), nem = cmk(0, 0), bnv = cmk(0, 0);
-    if (q == 0 && ri < rows && io.next) {
-      crv = __ldg(io.crn + r);
-      if (io.next == 1) { nev = __ldg(io.nen + r); bnv = io.bn[r]; }
-      else if (r >= 1) nem = __ldg(io.nen + r - 1);
-    }
-    const cplx* B = ring_wait(rg);
-    cplx acc = cmk(0, 0);
-    if (ri < rows) {
-      const cplx* Br = B + ri * w;
-#pragma unroll 4
-      for (int k = q; k < w; k += 8) {
-        cplx v = cadd(io.tA[k], io.tB[k]);
-        cfma(acc, Br[k], v);
+    const bool writer = (q == 0 && ri < rows);
+    // operands of the writer lanes, independent of this step's data
+    cplx crv = cmk(0, 0), nev = cmk(0, 0), nem = cmk(0, 0), bnv = cmk(0, 0), ybv = cmk(0, 0);
+    if (writer) {
+      if (io.mode == 1) ybv = io.ybase[r];
+      if (io.next) {
+        crv = io.crn[r];
+        if (io.next == 1) { nev = io.nen[r]; bnv = io.bn[r]; }
+        else if (r >= 1) nem = io.nen[r - 1];
       }
     }
+    long long c0 = clock64();
+    const cplx* B = ring_peek(rg, rg.kc);
+    long long c1 = clock64();
+    cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
+    if (ri < rows) {
+      const cplx* Br = B + ri * w;
+      int k = q;
+      for (; k + 8 < w; k += 16) {
+        cfma(acc0, Br[k], cadd(io.tA[k], io.tB[k]));
+        cfma(acc1, Br[k + 8], cadd(io.tA[k + 8], io.tB[k + 8]));
+      }
+      if (k < w) cfma(acc0, Br[k], cadd(io.tA[k], io.tB[k]));
+    }
+    cplx acc = cadd(acc0, acc1);
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
-    if (q == 0 && ri < rows) {
-      cplx o = io.mode == 0 ? acc : csub(io.ybase[r], acc);
+    if (writer) {
+      cplx o = io.mode == 0 ? acc : csub(ybv, acc);
       io.out[r] = o;
       if (io.next == 1) {
         io.tAn[r] = csub(bnv, cmul(crv, o));
@@ -291,105 +342,134 @@ __device__ __forceinline__ void block_step(Ring& rg, int w, const StepIO& io, Re
         if (r == w - 1) io.tBn[w - 1] = cmk(0, 0);
       }
     }
-    __syncthreads();
-    refill();
+    long long c2 = clock64();
+    cbar(ncons);
+    ring_release(rg, 1);
+    long long c3 = clock64();
+    pf.peek += c1 - c0; pf.comp += c2 - c1; pf.bar += c3 - c2; pf.steps++;
   }
 }
 
 // two-block step for the reducer forward chain: out = A*u - B*v  (tile-interleaved A, B)
-template <class Refill>
-__device__ __forceinline__ void block_step2(Ring& rg, int w, const cplx* u, const cplx* v, bool hasB,
-                                            cplx* out, Refill refill) {
+__device__ __forceinline__ void block_step2(Ring& rg, int w, int ncons, const cplx* u, const cplx* v, bool hasB,
+                                            cplx* out, Prof& pf) {
   const int tid = threadIdx.x;
   const int ri = tid >> 3, q = tid & 7;
   const int nt = ntile_of(w, rg.R_t);
   for (int tt = 0; tt < nt; ++tt) {
     const int r0 = tt * rg.R_t;
     const int rows = min(rg.R_t, w - r0);
-    const cplx* A = ring_wait(rg);
-    rg.kc++;
-    const cplx* B = nullptr;
-    if (hasB) B = ring_wait(rg);
-    rg.kc--;  // restore: refill() advances kc per consumed tile
-    cplx acc = cmk(0, 0);
+    long long c0 = clock64();
+    const cplx* A = ring_peek(rg, rg.kc);
+    const cplx* B = hasB ? ring_peek(rg, rg.kc + 1) : nullptr;
+    long long c1 = clock64();
+    cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
     if (ri < rows) {
       const cplx* Ar = A + ri * w;
-      for (int k = q; k < w; k += 8) cfma(acc, Ar[k], u[k]);
+      for (int k = q; k < w; k += 8) cfma(acc0, Ar[k], u[k]);
       if (hasB) {
         const cplx* Br = B + ri * w;
-        for (int k = q; k < w; k += 8) cfma(acc, Br[k], cscale(v[k], -1.0));
+        for (int k = q; k < w; k += 8) cfma(acc1, Br[k], v[k]);
       }
     }
+    cplx acc = csub(acc0, acc1);
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
     if (q == 0 && ri < rows) out[r0 + ri] = acc;
-    __syncthreads();
-    refill();
-    if (hasB) refill();
+    long long c2 = clock64();
+    cbar(ncons);
+    ring_release(rg, hasB ? 2 : 1);
+    long long c3 = clock64();
+    pf.peek += c1 - c0; pf.comp += c2 - c1; pf.bar += c3 - c2; pf.steps++;
   }
 }
 
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ ApplyArgs A) {
+// blockDim = ncons consumer threads (8 lanes per block row) + 1 producer warp.
+__global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ ApplyArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x;
+  const int ncons = blockDim.x - 32;
   // which direction / role
   int d = 0;
   while (d + 1 < A.t && (int)blockIdx.x >= A.d[d + 1].cta_base) ++d;
   const DirArgs& D = A.d[d];
   const int role = blockIdx.x - D.cta_base;  // 0..P-1 segments, P = reducer
   const bool reducer = (D.P > 1 && role == D.P);
+  const int p = role;
 
   Ring rg;
-  rg.bar = reinterpret_cast<uint64_t*>(smem_raw);
-  rg.stage = reinterpret_cast<cplx*>(smem_raw + 128);
+  rg.full = reinterpret_cast<uint64_t*>(smem_raw);
+  rg.empty = rg.full + 16;
+  rg.stage = reinterpret_cast<cplx*>(smem_raw + 256);
   rg.nstage = A.nstage;
   rg.stage_elems = A.stage_elems;
   rg.R_t = A.rows_per_tile;
   rg.kc = 0;
-  rg.kp = 0;
-  cplx* vec0 = rg.stage + (long)A.nstage * A.stage_elems;  // bseg / g
-  cplx* vec1 = vec0 + A.vec_elems;                           // yseg / z
-  cplx* tbuf = vec1 + A.vec_elems;                           // 4 * wmax: tA0 tB0 tA1 tB1
-  cplx* xlo = tbuf + 4 * D.wmax;                             // separator x above (p-1)
-  cplx* xhi = xlo + D.wmax;                                  // separator x below (p)
-  cplx* cnx = xhi + D.wmax;                                  // reducer: next-side corrections (P-1)
+  cplx* sm_tail = rg.stage + (long)A.nstage * A.stage_elems;
+  cplx* tbuf = sm_tail;                  // 4 * wmax: tA0 tB0 tA1 tB1
+  cplx* xlo = tbuf + 4 * D.wmax;         // separator x above (p-1)
+  cplx* xhi = xlo + D.wmax;              // separator x below (p)
+  cplx* cnx = xhi + D.wmax;              // reducer: next-side corrections (P-1)
+  SolveTab* tab = reinterpret_cast<SolveTab*>(cnx + A.pmax);   // per-solve table (nsolve_max)
+  cplx* vbase = reinterpret_cast<cplx*>(tab + A.nsolve_max);      // vector areas (smem) ...
+  if (A.vec_global) vbase = A.vec_scratch + (long)blockIdx.x * 4 * A.vec_elems;  // ... or global
+  cplx* vec0 = vbase;                    // bseg / g
+  cplx* vec1 = vec0 + A.vec_elems;       // yseg / z
+  cplx* bcr = vec1 + A.vec_elems;        // staged U couplings, rows lo-1..hi
+  cplx* bne = bcr + A.vec_elems;
 
   if (tid == 0) {
-    for (int s = 0; s < A.nstage; ++s) mbar_init(&rg.bar[s], 1);
+    for (int s = 0; s < A.nstage; ++s) {
+      mbar_init(&rg.full[s], 1);
+      mbar_init(&rg.empty[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < n_solves(D); i += blockDim.x) {
+    const int s = sigma(D, step_of(D, i));
+    tab[i].fac = D.fac + D.fac_off[s];
+    tab[i].red = D.red + D.red_off[s];
+    tab[i].w = D.w[s];
   }
   __syncthreads();
 
-  const int nsolve = n_solves(D);
-  SegCursor sc{0, 0, 0, 0, false};
-  RedCursor rc{0, 0, 0, 0, 0, false};
-  const int p = role;
-  auto next_tile = [&](const cplx** src, uint32_t* bytes) -> bool {
-    return reducer ? red_next_tile(D, rg.R_t, rc, src, bytes) : seg_next_tile(D, p, rg.R_t, sc, src, bytes);
-  };
-  if (tid == 0) {
-    const cplx* src;
-    uint32_t bytes;
-    for (int s = 0; s < A.nstage; ++s) {
-      if (!next_tile(&src, &bytes)) break;
-      ring_issue(rg, src, bytes);
-    }
-  }
-  auto refill = [&]() {
-    // called by all threads after the __syncthreads that ends a tile's use
-    if (tid == 0) {
+  if (tid >= ncons) {
+    // ================================================================ TMA producer warp
+    if (tid == ncons) {
+      SegCursor sc;
+      RedCursor rc;
+      if (!reducer) {
+        sc.i = sc.ph = sc.j = sc.tt = 0;
+        sc.lo = D.seg_lo[p]; sc.hi = D.seg_hi[p]; sc.m = sc.hi - sc.lo + 1;
+        sc.nph = D.P > 1 ? 2 : 1; sc.nsolve = n_solves(D); sc.R_t = rg.R_t; sc.done = false;
+        seg_load_solve(sc, tab);
+      } else {
+        rc.i = rc.part = rc.k = rc.tt = rc.sub = 0;
+        rc.P = D.P; rc.nsolve = n_solves(D); rc.R_t = rg.R_t; rc.done = false;
+        red_load_solve(rc, tab);
+      }
       const cplx* src;
       uint32_t bytes;
-      if (next_tile(&src, &bytes)) ring_issue(rg, src, bytes);
+      for (uint32_t f = 0;; ++f) {
+        bool more = reducer ? red_next_tile(rc, tab, &src, &bytes) : seg_next_tile(sc, tab, &src, &bytes);
+        if (!more) break;
+        const int sidx = f % rg.nstage;
+        if (f >= (uint32_t)rg.nstage) mbar_wait(&rg.empty[sidx], ((f / rg.nstage) - 1) & 1);
+        mbar_expect_tx(&rg.full[sidx], bytes);
+        bulk_g2s(rg.stage + (long)sidx * rg.stage_elems, src, bytes, &rg.full[sidx]);
+      }
     }
-    rg.kc++;
-  };
+    return;
+  }
 
+  const int nsolve = n_solves(D);
   const long band_stride = (long)D.nc * D.wmax;
+  Prof pf;
+  const long long t_start = clock64();
 
   if (!reducer) {
     // ================================================================ segment CTA
@@ -405,54 +485,63 @@ __global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ 
       const int qn = next_side(D) == 0 ? 0 : w - 1;
       const bool has_prev = st > 0;
       const bool has_next = bwd;  // backward solves carry C^next(u_{s(m+1)})
-      const cplx* rsrc = D.R;
       const cplx* cband = D.cr + s * band_stride;
       const cplx* nband = D.ne + s * band_stride;
-      // ---- RHS: R_s r + corrections (rows lo..hi)
-      for (int e = tid; e < m * w; e += blockDim.x) {
+      // ---- RHS: R_s r + corrections (rows lo..hi); couplings of rows lo-1..hi
+      for (int e = tid; e < m * w; e += ncons) {
         int cl = e / w, q = e % w, c = lo + cl;
-        cplx v = __ldg(rsrc + node_of(D, a, c, q));
+        cplx v = __ldg(D.R + node_of(D, a, c, q));
         if (has_prev && q == qp) v = cadd(v, D.corr_prev[(long)st * D.nc + c]);
         if (has_next && q == qn) v = cadd(v, D.corr_next[c]);
         bseg[cl * w + q] = v;
       }
-      __syncthreads();
+      for (int e = tid; e < (m + 1) * w; e += ncons) {
+        int cl = e / w, q = e % w, c = lo - 1 + cl;
+        bcr[e] = c >= 0 ? __ldg(cband + (long)c * D.wmax + q) : cmk(0, 0);
+        bne[e] = c >= 0 ? __ldg(nband + (long)c * D.wmax + q) : cmk(0, 0);
+      }
+      cbar(ncons);
+      // staged couplings of row c: bcr + (c - lo + 1) * w
+      auto crow = [&](int c) { return bcr + (long)(c - lo + 1) * w; };
+      auto nrow = [&](int c) { return bne + (long)(c - lo + 1) * w; };
 
       // block-Thomas over the segment: fwd y_c = Sinv_c (b_c - L_c y_{c-1}); bwd x_c = y_c - Sinv_c U_c x_{c+1}
       auto thomas = [&]() {
-        cplx* tA[2] = {tbuf, tbuf + 2 * D.wmax};
-        cplx* tB[2] = {tbuf + D.wmax, tbuf + 3 * D.wmax};
-        for (int e = tid; e < w; e += blockDim.x) { tA[0][e] = bseg[e]; tB[0][e] = cmk(0, 0); }
-        __syncthreads();
+        cplx* tA0 = tbuf;
+        cplx* tB0 = tbuf + D.wmax;
+        cplx* tA1 = tbuf + 2 * D.wmax;
+        cplx* tB1 = tbuf + 3 * D.wmax;
+        for (int e = tid; e < w; e += ncons) { tA0[e] = bseg[e]; tB0[e] = cmk(0, 0); }
+        cbar(ncons);
         int cur = 0;
         for (int j = 0; j < m; ++j) {  // forward
           const int c = lo + j;
           StepIO io;
-          io.tA = tA[cur]; io.tB = tB[cur];
+          io.tA = cur ? tA1 : tA0; io.tB = cur ? tB1 : tB0;
+          io.tAn = cur ? tA0 : tA1; io.tBn = cur ? tB0 : tB1;
           io.out = yseg + j * w; io.ybase = nullptr; io.mode = 0;
           if (j + 1 < m) {
-            io.next = 1; io.bn = bseg + (j + 1) * w; io.crn = cband + (long)c * D.wmax; io.nen = nband + (long)c * D.wmax;
+            io.next = 1; io.bn = bseg + (j + 1) * w; io.crn = crow(c); io.nen = nrow(c);
           } else if (m > 1) {
-            io.next = 2; io.bn = nullptr; io.crn = cband + (long)(hi - 1) * D.wmax; io.nen = nband + (long)(hi - 1) * D.wmax;
+            io.next = 2; io.bn = nullptr; io.crn = crow(hi - 1); io.nen = nrow(hi - 1);
           } else {
             io.next = 0; io.bn = nullptr; io.crn = nullptr; io.nen = nullptr;
           }
-          io.tAn = tA[cur ^ 1]; io.tBn = tB[cur ^ 1];
-          block_step(rg, w, io, refill);
+          block_step(rg, w, ncons, io, pf);
           cur ^= 1;
         }
         for (int c = hi - 1; c >= lo; --c) {  // backward
           const int j = c - lo;
           StepIO io;
-          io.tA = tA[cur]; io.tB = tB[cur];
+          io.tA = cur ? tA1 : tA0; io.tB = cur ? tB1 : tB0;
+          io.tAn = cur ? tA0 : tA1; io.tBn = cur ? tB0 : tB1;
           io.out = yseg + j * w; io.ybase = yseg + j * w; io.mode = 1;
           if (c > lo) {
-            io.next = 2; io.bn = nullptr; io.crn = cband + (long)(c - 1) * D.wmax; io.nen = nband + (long)(c - 1) * D.wmax;
+            io.next = 2; io.bn = nullptr; io.crn = crow(c - 1); io.nen = nrow(c - 1);
           } else {
             io.next = 0; io.bn = nullptr; io.crn = nullptr; io.nen = nullptr;
           }
-          io.tAn = tA[cur ^ 1]; io.tBn = tB[cur ^ 1];
-          block_step(rg, w, io, refill);
+          block_step(rg, w, ncons, io, pf);
           cur ^= 1;
         }
       };
@@ -461,55 +550,57 @@ __global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ 
         // ---- phase 1: y_p = A_p^{-1} b_p; publish y[lo], y[hi]
         thomas();
         cplx* yb = D.yb + (long)p * 2 * D.wmax;
-        for (int e = tid; e < w; e += blockDim.x) {
+        for (int e = tid; e < w; e += ncons) {
           yb[e] = yseg[e];
           yb[D.wmax + e] = yseg[(m - 1) * w + e];
         }
-        __syncthreads();
+        cbar(ncons);
+        long long cw0 = clock64();
         if (tid == 0) {
           __threadfence();
           red_release_add(&D.cnt[0], 1u);
-          while (ld_acquire(&D.cnt[1]) < (unsigned)(i + 1)) __nanosleep(64);
-          __threadfence();
+          while (ld_relaxed(&D.cnt[1]) < (unsigned)(i + 1)) __nanosleep(20);
+          (void)ld_acquire(&D.cnt[1]);
         }
-        __syncthreads();
+        cbar(ncons);
+        pf.xwait += clock64() - cw0;
         // ---- phase 3 RHS: b_lo -= U_{lo-1}^T x_sep[p-1]; b_hi -= U_hi x_sep[p]
-        for (int e = tid; e < w; e += blockDim.x) {
+        for (int e = tid; e < w; e += ncons) {
           xlo[e] = p > 0 ? ldcg(D.xs + (long)(p - 1) * D.wmax + e) : cmk(0, 0);
           xhi[e] = p < D.P - 1 ? ldcg(D.xs + (long)p * D.wmax + e) : cmk(0, 0);
         }
-        __syncthreads();
-        for (int q = tid; q < w; q += blockDim.x) {
+        cbar(ncons);
+        for (int q = tid; q < w; q += ncons) {
           if (p > 0) {
-            const cplx* crr = cband + (long)(lo - 1) * D.wmax;
-            const cplx* ner = nband + (long)(lo - 1) * D.wmax;
-            cplx t = cmul(__ldg(crr + q), xlo[q]);
-            if (q >= 1) cfma(t, __ldg(ner + q - 1), xlo[q - 1]);
+            const cplx* crr = crow(lo - 1);
+            const cplx* ner = nrow(lo - 1);
+            cplx t = cmul(crr[q], xlo[q]);
+            if (q >= 1) cfma(t, ner[q - 1], xlo[q - 1]);
             bseg[q] = csub(bseg[q], t);
           }
           if (p < D.P - 1) {
-            const cplx* crr = cband + (long)hi * D.wmax;
-            const cplx* ner = nband + (long)hi * D.wmax;
-            cplx t = cmul(__ldg(crr + q), xhi[q]);
-            if (q + 1 < w) cfma(t, __ldg(ner + q), xhi[q + 1]);
+            const cplx* crr = crow(hi);
+            const cplx* ner = nrow(hi);
+            cplx t = cmul(crr[q], xhi[q]);
+            if (q + 1 < w) cfma(t, ner[q], xhi[q + 1]);
             bseg[(m - 1) * w + q] = csub(bseg[(m - 1) * w + q], t);
           }
         }
-        __syncthreads();
+        cbar(ncons);
       }
       // ---- phase 3 (or the whole solve when P == 1)
       thomas();
       // ---- epilogue: gather, boundary rows, next correction
       if (writes_Z(D, i)) {
         const int olo = D.own_lo[s], ohi = D.own_hi[s], ow = ohi - olo + 1;
-        for (int e = tid; e < m * ow; e += blockDim.x) {
+        for (int e = tid; e < m * ow; e += ncons) {
           int cl = e / ow, q = olo + e % ow;
           D.Z[node_of(D, a, lo + cl, q)] = yseg[cl * w + q];
         }
       }
       if (D.P > 1) {
         cplx* xb = D.xb + (long)p * 2 * D.wmax;
-        for (int e = tid; e < w; e += blockDim.x) {
+        for (int e = tid; e < w; e += ncons) {
           xb[e] = yseg[e];
           xb[D.wmax + e] = yseg[(m - 1) * w + e];
         }
@@ -529,9 +620,9 @@ __global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ 
           if (cc > hi) return xhi[q];
           return yseg[(cc - lo) * w + q];
         };
-        for (int c = lo + tid; c <= hi; c += blockDim.x) target[c] = correction(D, tdst, side, c, a, X);
+        for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction(D, tdst, side, c, a, X);
       }
-      __syncthreads();
+      cbar(ncons);
     }
   } else {
     // ================================================================ reducer CTA
@@ -547,33 +638,33 @@ __global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ 
       const int qn = next_side(D) == 0 ? 0 : w - 1;
       const cplx* cband = D.cr + s * band_stride;
       const cplx* nband = D.ne + s * band_stride;
+      long long cw0 = clock64();
       if (tid == 0) {
-        while (ld_acquire(&D.cnt[0]) < (unsigned)(P * (i + 1))) __nanosleep(32);
-        __threadfence();
+        while (ld_relaxed(&D.cnt[0]) < (unsigned)(P * (i + 1))) __nanosleep(20);
+        (void)ld_acquire(&D.cnt[0]);
       }
-      __syncthreads();
+      cbar(ncons);
+      pf.xwait += clock64() - cw0;
       // (a) separator-row corrections from the previous solve's solution
       if (i >= 1) {
         const int sprev = sigma(D, step_of(D, i - 1));
         const int aprev = D.a[sprev];
-        const int wprev = D.w[sprev];
         const int side = bwd ? next_side(D) : prev_side(D);
-        for (int k = tid; k < K; k += blockDim.x) {
+        for (int k = tid; k < K; k += ncons) {
           const int sk = D.seg_hi[k] + 1;
           auto X = [&](int cc, int q) -> cplx {
             if (cc == sk) return z[k * D.wmax + q];
             if (cc == sk - 1) return ldcg(D.xb + (long)k * 2 * D.wmax + D.wmax + q);
             return ldcg(D.xb + (long)(k + 1) * 2 * D.wmax + q);  // cc == sk + 1
           };
-          (void)wprev;
           cplx cv = correction(D, s, side, sk, aprev, X);
           if (!bwd) D.corr_prev[(long)st * D.nc + sk] = cv;
           else cnx[k] = cv;
         }
-        __syncthreads();
+        cbar(ncons);
       }
       // (b) reduced RHS g_k = b_{s_k} - U_{h_k}^T y_k[hi] - U_{s_k} y_{k+1}[lo]
-      for (int e = tid; e < K * w; e += blockDim.x) {
+      for (int e = tid; e < K * w; e += ncons) {
         const int k = e / w, q = e % w;
         const int hk = D.seg_hi[k], sk = hk + 1;
         cplx v = __ldg(D.R + node_of(D, a, sk, q));
@@ -587,30 +678,25 @@ __global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ 
         if (q + 1 < w) cfma(t, __ldg(nband + (long)sk * D.wmax + q), ldcg(yl + q + 1));
         g[k * D.wmax + q] = csub(v, t);
       }
-      __syncthreads();
+      for (int e = tid; e < w; e += ncons) tbuf[e] = cmk(0, 0);
+      cbar(ncons);
       // (c) block-Thomas on the separator system
-      for (int k = 0; k < K; ++k) {
-        block_step2(rg, w, g + k * D.wmax, k >= 1 ? z + (k - 1) * D.wmax : nullptr, k >= 1,
-                    z + k * D.wmax, refill);
-      }
+      for (int k = 0; k < K; ++k)
+        block_step2(rg, w, ncons, g + k * D.wmax, k >= 1 ? z + (k - 1) * D.wmax : nullptr, k >= 1, z + k * D.wmax, pf);
       for (int k = K - 2; k >= 0; --k) {
         StepIO io;
         io.tA = z + (k + 1) * D.wmax;
         io.tB = tbuf;  // zeros
-        if (k == K - 2) {
-          for (int e = tid; e < w; e += blockDim.x) tbuf[e] = cmk(0, 0);
-          __syncthreads();
-        }
         io.out = z + k * D.wmax; io.ybase = z + k * D.wmax; io.mode = 1;
         io.next = 0; io.bn = nullptr; io.crn = nullptr; io.nen = nullptr; io.tAn = nullptr; io.tBn = nullptr;
-        block_step(rg, w, io, refill);
+        block_step(rg, w, ncons, io, pf);
       }
       // (d) publish x_sep
-      for (int e = tid; e < K * w; e += blockDim.x) {
+      for (int e = tid; e < K * w; e += ncons) {
         const int k = e / w, q = e % w;
         D.xs[(long)k * D.wmax + q] = z[k * D.wmax + q];
       }
-      __syncthreads();
+      cbar(ncons);
       if (tid == 0) {
         __threadfence();
         st_release(&D.cnt[1], (unsigned)(i + 1));
@@ -618,18 +704,28 @@ __global__ void __launch_bounds__(288, 1) k_sweep_apply(const __grid_constant__ 
       // (e) gather separator rows
       if (writes_Z(D, i)) {
         const int olo = D.own_lo[s], ohi = D.own_hi[s], ow = ohi - olo + 1;
-        for (int e = tid; e < K * ow; e += blockDim.x) {
+        for (int e = tid; e < K * ow; e += ncons) {
           const int k = e / ow, q = olo + e % ow;
           D.Z[node_of(D, a, D.seg_hi[k] + 1, q)] = z[k * D.wmax + q];
         }
       }
-      __syncthreads();
+      cbar(ncons);
     }
+  }
+  if (A.prof && tid == 0) {
+    long long* o = A.prof + (long)blockIdx.x * 8;
+    o[0] = pf.peek; o[1] = pf.comp; o[2] = pf.bar; o[3] = pf.steps; o[4] = pf.xwait;
+    o[5] = clock64() - t_start; o[6] = reducer ? 1 : 0; o[7] = d;
   }
 }
 
 // ------------------------------------------------------------------ host
 static constexpr int kSmemMax = 227 * 1024;
+static long long* g_sweep_prof = nullptr;   // set by helm_sweep_profile (diagnostics)
+
+// Diagnostics (not part of the ABI header): when `buf` (device, 8 long long per
+// CTA) is non-null, every subsequent sweep_apply records per-CTA cycle counters.
+extern "C" void helm_sweep_profile(long long* buf) { g_sweep_prof = buf; }
 
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                     cudaStream_t st);
@@ -669,33 +765,45 @@ extern "C" int sweep_apply(const helm_sweep_t* dirs, int t, const double* Rin, l
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                     cudaStream_t st) {
   const helm_problem_s* prob = dirs[0]->prob;
-  // launch geometry
-  int wmax = 0;
-  for (int d = 0; d < t; ++d) wmax = std::max(wmax, dirs[d]->wmax);
-  int threads = std::min(1024, ((8 * std::min(wmax, 36) + 31) / 32) * 32);
-  const int R_t = threads / 8;
+  // launch geometry: 8 consumer lanes per block row (<= 36 rows per tile) + 1 TMA producer warp
+  int wmax = 0, pmax = 1;
+  for (int d = 0; d < t; ++d) {
+    wmax = std::max(wmax, dirs[d]->wmax);
+    pmax = std::max(pmax, dirs[d]->P);
+  }
+  const int ncons = ((8 * std::min(wmax, 36) + 31) / 32) * 32;
+  const int threads = ncons + 32;
+  const int R_t = ncons / 8;
   long vec_elems = 0, stage_elems = 0;
   int ctas = 0;
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     int mmax = 0;
     for (int p = 0; p < h->P; ++p) mmax = std::max(mmax, h->seg_hi[p] - h->seg_lo[p] + 1);
-    int vr = std::max(mmax, std::max(h->P - 1, 1));
+    int vr = std::max(mmax + 1, std::max(h->P - 1, 1));
     vec_elems = std::max(vec_elems, (long)vr * h->wmax);
     stage_elems = std::max(stage_elems, (long)std::min(R_t, h->wmax) * h->wmax);
     ctas += h->P + (h->P > 1 ? 1 : 0);
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
   stage_elems = (stage_elems + 7) / 8 * 8;
-  int pmax = 1;
-  for (int d = 0; d < t; ++d) pmax = std::max(pmax, dirs[d]->P);
-  long fixed = 128 + sizeof(cplx) * (2 * vec_elems + 7L * wmax + pmax + 8);
-  int nstage = (int)std::min<long>(8, (kSmemMax - fixed) / (long)(sizeof(cplx) * stage_elems));
+  int nsolve_max = 1;
+  for (int d = 0; d < t; ++d) nsolve_max = std::max(nsolve_max, dirs[d]->is_double ? 2 * dirs[d]->N - 1 : dirs[d]->N);
+  nsolve_max = (nsolve_max + 1) & ~1;  // keeps the vector areas after the table 16-byte aligned
+  const long tail = sizeof(cplx) * (7L * wmax + pmax + 8) + 24L * nsolve_max + 32;
+  const long stage_bytes = sizeof(cplx) * stage_elems;
+  int vec_global = 0;
+  long fixed = 256 + tail + sizeof(cplx) * 4 * vec_elems;
+  if (kSmemMax - fixed < 2 * stage_bytes) {
+    vec_global = 1;
+    fixed = 256 + tail;
+  }
+  int nstage = (int)std::min<long>(8, (kSmemMax - fixed) / stage_bytes);
   if (nstage < 2) {
     helm_set_error("sweep_apply: shared memory too small (w=%d)", wmax);
     return HELM_EINVAL;
   }
-  size_t smem = fixed + sizeof(cplx) * (size_t)nstage * stage_elems;
+  size_t smem = fixed + (size_t)nstage * stage_bytes;
   // per-direction scratch
   std::vector<size_t> off(t);
   size_t total = 0;
@@ -709,6 +817,8 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
     total += al(sizeof(cplx) * (long)h->N * h->nc);                // corr_prev
     total += al(sizeof(cplx) * (long)h->nc);                       // corr_next
   }
+  size_t vec_off = total;
+  if (vec_global) total += al(sizeof(cplx) * 4L * vec_elems * ctas);
   unsigned char* scratch = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&scratch, total, st);
   if (e != cudaSuccess) {
@@ -722,6 +832,11 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   A.nstage = nstage;
   A.stage_elems = (int)stage_elems;
   A.vec_elems = (int)vec_elems;
+  A.pmax = pmax;
+  A.nsolve_max = nsolve_max;
+  A.vec_global = vec_global;
+  A.vec_scratch = vec_global ? (cplx*)(scratch + vec_off) : nullptr;
+  A.prof = g_sweep_prof;
   int base = 0;
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];

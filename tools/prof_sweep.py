@@ -1,0 +1,62 @@
+"""Profile driver: C5 (or --config k) batched sweep apply, t directions.
+Warm-up applies, then timed applies with CUDA events; prints ms and model GB/s.
+Use under ncu with  -k regex:k_sweep_apply -s <warm> -c 1."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2408_11929_b200 as hs
+from helm_inputs import make_config
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=5)
+ap.add_argument("--t", type=int, default=4)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--warm", type=int, default=2)
+ap.add_argument("--nseg", type=int, default=0)
+a = ap.parse_args()
+
+cfg = make_config(a.config)
+names = {1: ["LRL"], 2: ["LRL", "BTB"], 4: ["LRL", "RLR", "BTB", "TBT"]}[a.t]
+dev = torch.device("cuda:0")
+prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev))
+dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap, n_segments=a.nseg) for nm in names]
+info = [d.info() for d in dirs]
+r = torch.randn(cfg.n, dtype=torch.complex128, device=dev)
+Z = torch.zeros((len(dirs), cfg.n), dtype=torch.complex128, device=dev)
+for _ in range(a.warm):
+    hs.sweep_apply(dirs, r, Z, ldr=0)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.reps):
+    hs.sweep_apply(dirs, r, Z, ldr=0)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.reps
+model = sum(i.model_bytes_per_apply for i in info)
+print(f"config C{a.config} t={a.t} P={info[0].n_segments} w={info[0].wmax}: {ms:.3f} ms/apply, "
+      f"model {model/1e9:.2f} GB -> {model/ms/1e6:.0f} GB/s, applies/s {a.t*1e3/ms:.1f}")
+
+if os.environ.get("HELM_CYCLES"):
+    import ctypes
+    L = hs.load()
+    ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)
+    buf = torch.zeros(ctas * 8, dtype=torch.int64, device=dev)
+    L.helm_sweep_profile.argtypes = [ctypes.c_void_p]
+    L.helm_sweep_profile(ctypes.c_void_p(buf.data_ptr()))
+    hs.sweep_apply(dirs, r, Z, ldr=0)
+    torch.cuda.synchronize()
+    L.helm_sweep_profile(ctypes.c_void_p(0))
+    b = buf.view(ctas, 8).cpu().numpy()
+    for role in (0, 1):
+        sel = b[b[:, 6] == role]
+        if len(sel) == 0:
+            continue
+        st = sel[:, 3].mean()
+        print(f"{'reducer' if role else 'segment'} CTAs={len(sel)} steps={st:.0f} total={sel[:,5].mean():.3e} cyc | "
+              f"per step: peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
+              f"xwait total {sel[:,4].mean():.3e} ({sel[:,4].mean()/sel[:,5].mean()*100:.1f}%)")
