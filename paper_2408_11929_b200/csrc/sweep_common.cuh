@@ -1,0 +1,124 @@
+// sweep_common.cuh -- arguments and device helpers shared by the two sweep
+// kernels (sweep_apply.cu: general TMA-ring kernel; sweep_fast.cu: register-
+// streaming kernel for block rows of <= 36 nodes).
+#pragma once
+#include "common.cuh"
+
+#define HELM_MAXDIR 8
+
+struct DirArgs {
+  int axis, order, N, P, nc, nxp1, is_double, ntile_max;
+  const int *a, *w, *own_lo, *own_hi, *seg_lo, *seg_hi;
+  const cplx *cr, *ne;   // bands: U_c couplings, stride wmax per row, nc*wmax per strip
+  const cplx* tc;        // transmission stencils [s][side][c][5]
+  const cplx* fac;
+  const long* fac_off;
+  const cplx* red;
+  const long* red_off;
+  const cplx* R;         // source column
+  cplx* Z;               // output column
+  cplx *yb, *xs, *xb, *corr_prev, *corr_next;
+  unsigned* cnt;         // [0] segment arrivals, [1] reducer releases
+  int wmax;
+  int cta_base;
+  int vec_rows;
+};
+
+struct ApplyArgs {
+  DirArgs d[HELM_MAXDIR];
+  int t;
+  int rows_per_tile;  // R_t = consumer threads / 8
+  int nstage;
+  int stage_elems;    // cplx per stage
+  int vec_elems;      // cplx per vector area (bseg / yseg / staged couplings)
+  int pmax;           // max segments over directions
+  int nsolve_max;     // max local solves per apply over directions
+  int vec_global;     // vector areas in global scratch (shared memory too small)
+  cplx* vec_scratch;  // per-CTA 4 * vec_elems when vec_global
+  long long* prof;    // optional per-CTA cycle counters (8 per CTA), NULL = off
+};
+
+// per-thread profiling accumulators (thread 0 reports)
+struct Prof {
+  long long peek = 0, comp = 0, bar = 0, steps = 0, xwait = 0;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// relaxed poll (no L1 invalidation per iteration); callers fence once after success
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ cplx ldcg(const cplx* p) { return __ldcg(p); }
+
+// ------------------------------------------------------------------ geometry helpers
+__device__ __forceinline__ int sigma(const DirArgs& D, int m) { return D.order == 0 ? m : D.N - 1 - m; }
+__device__ __forceinline__ int n_solves(const DirArgs& D) { return D.is_double ? 2 * D.N - 1 : D.N; }
+// sweep step m and pass of solve i
+__device__ __forceinline__ int step_of(const DirArgs& D, int i) { return i < D.N ? i : 2 * D.N - 2 - i; }
+__device__ __forceinline__ bool is_bwd(const DirArgs& D, int i) { return i >= D.N; }
+__device__ __forceinline__ bool writes_Z(const DirArgs& D, int i) { return D.is_double ? (i >= D.N - 1) : true; }
+__device__ __forceinline__ long node_of(const DirArgs& D, int a, int c, int q) {
+  return D.axis == 0 ? (long)c * D.nxp1 + (a + q) : (long)(a + q) * D.nxp1 + c;
+}
+// interface positions inside strip s: prev side / next side (0 = low line a_s, w-1 = high line b_s)
+__device__ __forceinline__ int prev_side(const DirArgs& D) { return D.order == 0 ? 0 : 1; }
+__device__ __forceinline__ int next_side(const DirArgs& D) { return D.order == 0 ? 1 : 0; }
+
+// Correction (D8) for destination strip t, side, row c, from a source solution
+// x_s accessed by a functor X(c', q).  Positions of the interface line and the
+// outer line in the source strip (a_src).
+template <class XF>
+__device__ __forceinline__ cplx correction(const DirArgs& D, int t, int side, int c, int a_src, XF X) {
+  const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * 5;
+  int at = D.a[t], bt = at + D.w[t] - 1;
+  int qi, qo, dd;
+  if (side == 0) { qi = at - a_src; qo = at - 1 - a_src; dd = -1; }
+  else { qi = bt - a_src; qo = bt + 1 - a_src; dd = 1; }
+  cplx acc = cmul(__ldg(k + 1), X(c, qi));
+  cfma(acc, __ldg(k + 3), X(c, qo));
+  if (c >= 1) cfma(acc, __ldg(k + 0), X(c - 1, qi));
+  if (c + 1 < D.nc) cfma(acc, __ldg(k + 2), X(c + 1, qi));
+  if (c + dd >= 0 && c + dd < D.nc) cfma(acc, __ldg(k + 4), X(c + dd, qo));
+  return acc;
+}
+

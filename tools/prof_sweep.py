@@ -58,5 +58,5 @@ if os.environ.get("HELM_CYCLES"):
             continue
         st = sel[:, 3].mean()
         print(f"{'reducer' if role else 'segment'} CTAs={len(sel)} steps={st:.0f} total={sel[:,5].mean():.3e} cyc | "
-              f"per step: peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
+              f"per step: pre|peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
               f"xwait total {sel[:,4].mean():.3e} ({sel[:,4].mean()/sel[:,5].mean()*100:.1f}%)")
