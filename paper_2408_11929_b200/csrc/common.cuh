@@ -107,6 +107,9 @@ struct helm_sweep_s {
   cplx* d_fac; std::vector<long> fac_off; long* d_fac_off;
   // reduced (separator) system: per strip s, separator k (0..P-2): Rinv, G, F
   cplx* d_red; std::vector<long> red_off; long* d_red_off;
+  // explicit rows of the separator inverse (w <= 36 only): per strip, separator k:
+  // w x (K w) row-major at xinv_off[s] + k * w * K * w
+  cplx* d_xinv = nullptr; std::vector<long> xinv_off; long* d_xinv_off = nullptr;
   long factor_bytes;
 };
 

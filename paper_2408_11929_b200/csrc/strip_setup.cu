@@ -22,6 +22,8 @@
 #include "dense.cuh"
 #include "p1_entries.cuh"
 
+static constexpr int kXinvMaxW = 36;   // explicit separator inverse for the register-streaming kernel
+
 // ------------------------------------------------------------------ bands + corrections
 struct StripGeo {
   const int* a;   // first line of each strip
@@ -227,6 +229,73 @@ __global__ void k_reduced(RedArgs ra) {
   }
 }
 
+// ------------------------------------------------------------------ explicit separator inverse
+// Rows of R^{-1} (R = the separator Schur complement, block tridiagonal with
+// K = P-1 dense w x w blocks) for the register-streaming sweep kernel: the
+// segment CTAs then obtain x_sep = R^{-1} g by a parallel dense mat-vec
+// instead of a K-step dependent chain.  Computed from the block-Thomas
+// factors (Rinv_k, G_k, F_k) applied to the identity, one CTA per
+// (strip, column block j):  Z_j = Rinv_j E_j, Z_k = -G_k Z_{k-1} (k > j),
+// X_{K-1} = Z_{K-1}, X_k = Z_k - F_k X_{k+1}.  Storage per strip:
+// X[k] is w x (K w) row-major (the rows of separator k), contiguous.
+__global__ void k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.y, j = blockIdx.x;
+  const int K = ra.P - 1;
+  if (j >= K) return;
+  const int w = ra.w[s];
+  const long w2 = (long)w * w, Kw = (long)K * w;
+  const cplx* red = ra.red + ra.red_off[s];
+  cplx* X = xinv + xinv_off[s];
+  cplx* cur = reinterpret_cast<cplx*>(smem_raw);   // w x w: column block j of Z_k / X_k
+  cplx* M = cur + w2;                               // w x w factor
+  cplx* nxt = M + w2;
+  auto blkX = [&](int k, int r, int c) -> cplx& { return X[(long)k * w * Kw + (long)r * Kw + (long)j * w + c]; };
+  // forward: rows k < j are zero; k = j: Rinv_j; k > j: -G_k Z_{k-1}
+  for (int k = 0; k < j; ++k)
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) blkX(k, e / w, e % w) = cmk(0, 0);
+  for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+    cur[e] = red[(long)j * 3 * w2 + e];
+    blkX(j, e / w, e % w) = cur[e];
+  }
+  __syncthreads();
+  for (int k = j + 1; k < K; ++k) {
+    const cplx* G = red + ((long)k * 3 + 1) * w2;
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) M[e] = G[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+      const int r = e / w, c = e % w;
+      cplx acc = cmk(0, 0);
+      for (int t = 0; t < w; ++t) cfma(acc, M[r * w + t], cur[t * w + c]);
+      nxt[e] = cscale(acc, -1.0);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+      cur[e] = nxt[e];
+      blkX(k, e / w, e % w) = nxt[e];
+    }
+    __syncthreads();
+  }
+  // backward: cur holds X_{K-1}[:, j] = Z_{K-1}[:, j]
+  for (int k = K - 2; k >= 0; --k) {
+    const cplx* F = red + ((long)k * 3 + 2) * w2;
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) M[e] = F[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+      const int r = e / w, c = e % w;
+      cplx acc = cmk(0, 0);
+      for (int t = 0; t < w; ++t) cfma(acc, M[r * w + t], cur[t * w + c]);
+      nxt[e] = csub(blkX(k, r, c), acc);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+      cur[e] = nxt[e];
+      blkX(k, e / w, e % w) = nxt[e];
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ host
 static int choose_segments(int nc, int requested) {
   if (requested > 0) return requested;
@@ -312,6 +381,8 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h->d_a = h->d_w = h->d_own_lo = h->d_own_hi = h->d_seg_lo = h->d_seg_hi = nullptr;
   h->d_dg = h->d_al = h->d_cr = h->d_ne = h->d_tc = h->d_fac = h->d_red = nullptr;
   h->d_fac_off = h->d_red_off = nullptr;
+  h->d_xinv = nullptr;
+  h->d_xinv_off = nullptr;
   alloc((void**)&h->d_a, sizeof(int) * n_strips);
   alloc((void**)&h->d_w, sizeof(int) * n_strips);
   alloc((void**)&h->d_own_lo, sizeof(int) * n_strips);
@@ -387,6 +458,27 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     k_reduced<<<n_strips, threads, smem, st>>>(ra);
     g_helm_launches++;
     e = cudaGetLastError();
+    if (e == cudaSuccess && wmax <= kXinvMaxW) {
+      // explicit separator inverse rows for the register-streaming kernel
+      h->xinv_off.resize(n_strips);
+      long tot = 0;
+      for (int s2 = 0; s2 < n_strips; ++s2) {
+        h->xinv_off[s2] = tot;
+        tot += (long)(P - 1) * h->w[s2] * (long)(P - 1) * h->w[s2];
+      }
+      e = cudaMalloc(&h->d_xinv, sizeof(cplx) * tot);
+      if (e == cudaSuccess) e = cudaMalloc(&h->d_xinv_off, sizeof(long) * n_strips);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->d_xinv_off, h->xinv_off.data(), sizeof(long) * n_strips, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) {
+        size_t sm3 = sizeof(cplx) * 3 * wmax * wmax;
+        cudaFuncSetAttribute(k_reduced_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+        k_reduced_inverse<<<dim3(P - 1, n_strips), 256, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        g_helm_launches++;
+        e = cudaGetLastError();
+        h->factor_bytes += tot * (long)sizeof(cplx);
+      }
+    }
   }
   int status = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -441,5 +533,6 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
   cudaFree(h->d_seg_lo); cudaFree(h->d_seg_hi); cudaFree(h->d_fac_off); cudaFree(h->d_red_off);
   cudaFree(h->d_dg); cudaFree(h->d_al); cudaFree(h->d_cr); cudaFree(h->d_ne); cudaFree(h->d_tc);
   cudaFree(h->d_fac); cudaFree(h->d_red);
+  cudaFree(h->d_xinv); cudaFree(h->d_xinv_off);
   delete h;
 }

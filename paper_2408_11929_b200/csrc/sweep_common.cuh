@@ -19,6 +19,8 @@ struct DirArgs {
   cplx* Z;               // output column
   cplx *yb, *xs, *xb, *corr_prev, *corr_next;
   unsigned* cnt;         // [0] segment arrivals, [1] reducer releases
+  const cplx* xinv;      // explicit separator-inverse rows (fast kernel), NULL if absent
+  const long* xinv_off;
   int wmax;
   int cta_base;
   int vec_rows;

@@ -1,24 +1,29 @@
 // sweep_fast.cu -- hot-path row a4 for block rows of <= 36 nodes (C1, C2, C3,
-// C5 and the y-sweeps of C4): the same batched, partitioned double sweep as
-// sweep_apply.cu (segment CTAs + reducer CTA per direction, one persistent
-// cooperative launch for all t directions), with a data path designed from
-// B200 measurements (tools/bench_*.cu):
+// C5 and the y-sweeps of C4): the batched, partitioned double sweep of
+// sweep_apply.cu (one persistent cooperative launch for all t directions),
+// with a data path designed from B200 measurements (tools/bench_*.cu,
+// DESIGN.md §5):
 //
+//  * No reducer CTA.  After phase 1 the P segment CTAs of a direction do one
+//    all-gather of their boundary rows; every CTA then forms the separator
+//    right-hand side g itself and obtains its two separator values as rows of
+//    R^{-1} g, a parallel dense mat-vec with the explicit separator-inverse
+//    rows precomputed at setup (strip_setup.cu, k_reduced_inverse).  This
+//    replaces the (2P-3)-step dependent chain of the reduced block-Thomas
+//    solve by ~1 MB of streamed reads per CTA.
 //  * Factor blocks are streamed L2 -> registers with plain 128-bit loads,
-//    D = 3 block steps ahead (each thread holds only the 9 complex entries of
-//    its row slice), so every factor byte crosses the L1/shared-memory data
-//    path once (the TMA ring crosses it twice and saturated it).  A helper
-//    warp keeps the blocks of the next ~12 steps warm in L2
-//    (cp.async.bulk.prefetch.L2) so the first (HBM) touch is hidden too.
+//    D = 3 block steps ahead (each thread holds the 9 complex entries of its
+//    row slice), so every factor byte crosses the L1/shared-memory data path
+//    once.  A helper warp keeps the next ~12 blocks (and the separator-inverse
+//    rows of the next solve) warm in L2 with cp.async.bulk.prefetch.L2.
 //  * 4 lanes per block row, 8 row slots per warp: 7 owned rows + 1 halo row.
-//    The halo row gives the writer lanes the neighbour value they need to
-//    form the COMPLETE next input (b - L y or U x) with one shuffle, so each
-//    step reads a single input vector and needs one 2-level butterfly and
-//    one named barrier.  The halo sits below (forward-style next input) or
-//    above (backward-style) the owned rows, chosen per step.
-//  * The reducer computes h_k = Rinv_k g_k for all separators off the
-//    dependent chain (no barriers), then runs z_k = h_k - G_k z_{k-1} and
-//    x_k = z_k - F_k x_{k+1}: one block per chain step.
+//    The halo gives the writer lanes the neighbour value they need to form
+//    the COMPLETE next input (b - L y or U x) with one shuffle: one input
+//    vector, one 2-level butterfly and one named barrier per block step.
+//    Forward rows are kept read-only during the backward pass (xsg holds the
+//    final rows) so a halo slot never observes an owner's update.
+//  * Exchange arrays are double-buffered by solve parity, so a CTA one solve
+//    ahead never overwrites data a slower CTA still reads.
 #include <algorithm>
 #include <cstring>
 
@@ -45,117 +50,36 @@ struct FastArgs {
 
 struct FastTab {
   const cplx* fac;
-  const cplx* red;
+  const cplx* xinv;
   int w, a, s, pad;
 };
 
-// decoded block step
-struct Step {
-  int i;        // solve
-  int kind;     // 0 seg fwd, 1 seg bwd, 2 red h (Rinv), 3 red fwd chain (G), 4 red bwd chain (F)
-  int row;      // seg: block row; red: separator k
-  int high;     // halo mapping: 1 = neighbour row r+1 available, 0 = r-1
-  int js;       // step within the solve (red) or phase (seg)
-  int ph;       // seg: 0 phase 1, 1 phase 3
-};
-
-__device__ __forceinline__ Step seg_decode(int j, int lo, int hi, int P) {
-  const int m = hi - lo + 1, spp = 2 * m - 1, nph = P > 1 ? 2 : 1;
-  Step s;
-  s.i = j / (nph * spp);
-  const int r1 = j - s.i * nph * spp;
-  const int ph = r1 / spp;
-  s.ph = nph == 2 ? ph : 1;
-  s.js = r1 - ph * spp;
-  if (s.js < m) {
-    s.kind = 0;
-    s.row = lo + s.js;
-    s.high = (s.js == m - 1 && m > 1) ? 1 : 0;
-  } else {
-    s.kind = 1;
-    s.row = hi - 1 - (s.js - m);
-    s.high = 1;
-  }
-  return s;
-}
-
-__device__ __forceinline__ Step red_decode(int j, int K) {
-  const int sps = 3 * K - 2;
-  Step s;
-  s.i = j / sps;
-  s.js = j - s.i * sps;
-  s.high = 0;
-  s.ph = 0;
-  if (s.js < K) { s.kind = 2; s.row = s.js; }
-  else if (s.js < 2 * K - 1) { s.kind = 3; s.row = s.js - K + 1; }
-  else { s.kind = 4; s.row = K - 2 - (s.js - (2 * K - 1)); }
-  return s;
-}
-
-// Per-CTA schedule of one solve (identical for every solve of the apply, only
-// the strip changes): built once in shared memory; the per-step cursor is a
-// table lookup plus a solve counter (no division, little uniform arithmetic).
+// one entry of the per-CTA schedule of a solve
 struct StepEnt {
-  int blk;      // block index inside the strip's factor array (seg: row; red: 3k + {0,1,2})
-  int row;      // seg: block row c; red: separator k
-  int kind;     // 0 seg fwd, 1 seg bwd, 2 red h, 3 red fwd chain, 4 red bwd chain
-  int flags;    // bit0 high-halo mapping, bits 8.. js (in phase/solve), bit4 phase (seg: 0/1)
+  int row;      // block row c
+  int kind;     // 0 forward step, 1 backward step
+  int flags;    // bit0 high-halo mapping, bit4 phase 3, bits 8.. step within the phase
+  int pad;
 };
 
-// Incremental step cursor (no integer division on the per-step path).
-struct Cursor {
-  Step s;
-  int m, spp, nph, K, lo, hi, P;
-  bool red;
-  int w;
-  const cplx* base;   // factor (or reduced-system) base of the current solve
-  __device__ __forceinline__ void derive(const FastTab* tab) {
-    if (!red) {
-      if (s.js < m) { s.kind = 0; s.row = lo + s.js; s.high = (s.js == m - 1 && m > 1) ? 1 : 0; }
-      else { s.kind = 1; s.row = hi - 1 - (s.js - m); s.high = 1; }
-    } else {
-      s.high = 0;
-      if (s.js < K) { s.kind = 2; s.row = s.js; }
-      else if (s.js < 2 * K - 1) { s.kind = 3; s.row = s.js - K + 1; }
-      else { s.kind = 4; s.row = K - 2 - (s.js - (2 * K - 1)); }
-    }
+__device__ __forceinline__ StepEnt seg_entry(int e, int lo, int hi, int P) {
+  const int m = hi - lo + 1, spp = 2 * m - 1, nph = P > 1 ? 2 : 1;
+  const int ph = e / spp, js = e - ph * spp;
+  StepEnt en;
+  const int phase3 = nph == 2 ? ph : 1;
+  int high;
+  if (js < m) {
+    en.kind = 0;
+    en.row = lo + js;
+    high = (js == m - 1 && m > 1) ? 1 : 0;
+  } else {
+    en.kind = 1;
+    en.row = hi - 1 - (js - m);
+    high = 1;
   }
-  __device__ __forceinline__ void load_solve(const FastTab* tab, int nsolve) {
-    if (s.i < nsolve) {
-      w = tab[s.i].w;
-      base = red ? tab[s.i].red : tab[s.i].fac;
-    }
-  }
-  __device__ __forceinline__ void init(int j0, bool red_, int lo_, int hi_, int P_, const FastTab* tab, int nsolve) {
-    red = red_; lo = lo_; hi = hi_; P = P_; K = P_ - 1;
-    m = hi - lo + 1; spp = 2 * m - 1; nph = P > 1 ? 2 : 1;
-    s = red ? red_decode(j0, K) : seg_decode(j0, lo, hi, P);
-    load_solve(tab, nsolve);
-  }
-  __device__ __forceinline__ void advance(const FastTab* tab, int nsolve) {
-    if (!red) {
-      if (++s.js == spp) {
-        s.js = 0;
-        if (nph == 2 && s.ph == 0) s.ph = 1;
-        else { s.ph = nph == 2 ? 0 : 1; ++s.i; load_solve(tab, nsolve); }
-      }
-    } else {
-      if (++s.js == 3 * K - 2) { s.js = 0; ++s.i; load_solve(tab, nsolve); }
-    }
-    derive(tab);
-  }
-  __device__ __forceinline__ const cplx* block() const {
-    const long w2 = (long)w * w;
-    if (!red) return base + (long)s.row * w2;
-    return base + ((long)s.row * 3 + (s.kind - 2)) * w2;
-  }
-};
-
-__device__ __forceinline__ const cplx* step_block(const Step& s, const FastTab* tab) {
-  const int w = tab[s.i].w;
-  const long w2 = (long)w * w;
-  if (s.kind <= 1) return tab[s.i].fac + (long)s.row * w2;
-  return tab[s.i].red + ((long)s.row * 3 + (s.kind - 2)) * w2;
+  en.flags = high | (phase3 << 4) | (js << 8);
+  en.pad = 0;
+  return en;
 }
 
 // thread's block row for a step mapping
@@ -185,48 +109,61 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
   int d = 0;
   while (d + 1 < A.t && (int)blockIdx.x >= A.d[d + 1].cta_base) ++d;
   const DirArgs& D_ = A.d[d];
-  const int role = blockIdx.x - D_.cta_base;
-  const bool reducer = (D_.P > 1 && role == D_.P);
-  const int p = role;
+  const int p = blockIdx.x - D_.cta_base;
   const int P = D_.P, K = P - 1;
 
   cplx* vbuf = reinterpret_cast<cplx*>(smem_raw);   // [2][WM]
-  cplx* xlo = vbuf + 2 * WM;
-  cplx* xhi = xlo + WM;
-  cplx* cnx = xhi + WM;                                // pmax
-  FastTab* tab = reinterpret_cast<FastTab*>(cnx + A.pmax);
+  cplx* xlo = vbuf + 2 * WM;                        // x_sep[p-1]
+  cplx* xhi = xlo + WM;                             // x_sep[p]
+  cplx* cpv = xhi + WM;                             // [pmax] prev-side separator corrections
+  cplx* cnv = cpv + A.pmax;                         // [pmax] next-side separator corrections
+  FastTab* tab = reinterpret_cast<FastTab*>(cnv + A.pmax);
   volatile int* prog = reinterpret_cast<volatile int*>(tab + A.nsolve_max);
   cplx* vec0 = reinterpret_cast<cplx*>(smem_raw + ((((char*)(prog + 4) - (char*)smem_raw) + 127) / 128) * 128);
-  cplx* vec1 = vec0 + A.vec_elems;
-  cplx* bcr = vec1 + A.vec_elems;
+  cplx* bseg = vec0;                                // RHS rows lo..hi
+  cplx* yseg = bseg + A.vec_elems;                  // forward rows y
+  cplx* bcr = yseg + A.vec_elems;                   // staged U couplings, rows lo-1..hi
   cplx* bne = bcr + A.vec_elems;
-  cplx* xsg = bne + A.vec_elems;    // segment: final solution x of the block sweep
+  cplx* xsg = bne + A.vec_elems;                    // final rows x
+  cplx* gsm = xsg + A.vec_elems;                    // separator RHS g (K x w)
+  StepEnt* sched = reinterpret_cast<StepEnt*>(gsm + A.vec_elems);
 
   const int nsolve = n_solves(D_);
   for (int i = tid; i < nsolve; i += blockDim.x) {
     const int s = sigma(D_, step_of(D_, i));
     tab[i].fac = D_.fac + D_.fac_off[s];
-    tab[i].red = D_.red + D_.red_off[s];
+    tab[i].xinv = D_.xinv ? D_.xinv + D_.xinv_off[s] : nullptr;
     tab[i].w = D_.w[s];
     tab[i].a = D_.a[s];
     tab[i].s = s;
   }
   if (tid == 0) *prog = 0;
-  __syncthreads();
-
-  const int lo = reducer ? 0 : D_.seg_lo[p];
-  const int hi = reducer ? 0 : D_.seg_hi[p];
+  const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
   const int m = hi - lo + 1;
-  const int total = reducer ? nsolve * (3 * K - 2) : nsolve * (P > 1 ? 2 : 1) * (2 * m - 1);
+  const int sps = (P > 1 ? 2 : 1) * (2 * m - 1);
+  const int total = nsolve * sps;
+  for (int e = tid; e < sps; e += blockDim.x) sched[e] = seg_entry(e, lo, hi, P);
+  __syncthreads();
 
   if (tid >= ncons) {
     // ================================================================ L2 prefetch helper warp
     if (tid == ncons) {
+      int pi = 0, ppos = 0;
       for (int jp = 0; jp < total; ++jp) {
         while (*prog + PF < jp) __nanosleep(500);
-        Step s = reducer ? red_decode(jp, K) : seg_decode(jp, lo, hi, P);
-        const int w = tab[s.i].w;
-        prefetch_l2(step_block(s, tab), (uint32_t)(w * w * sizeof(cplx)));
+        const int w = tab[pi].w;
+        const StepEnt en = sched[ppos];
+        if (false && ppos == 0 && P > 1 && tab[pi].xinv) {
+          // separator-inverse rows this CTA will need after phase 1 of solve pi
+          const long rowblk = (long)w * K * w;   // cplx per separator
+          for (int sk = max(p - 1, 0); sk <= min(p, K - 1); ++sk) {
+            const char* b0 = reinterpret_cast<const char*>(tab[pi].xinv + sk * rowblk);
+            const long bytes = rowblk * (long)sizeof(cplx);
+            for (long o = 0; o < bytes; o += 65536) prefetch_l2(b0 + o, (uint32_t)min(65536L, bytes - o));
+          }
+        }
+        prefetch_l2(tab[pi].fac + (long)en.row * w * w, (uint32_t)(w * w * sizeof(cplx)));
+        if (++ppos == sps) { ppos = 0; ++pi; }
       }
     }
     return;
@@ -235,36 +172,25 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
   const int wi = tid >> 5, lane = tid & 31;
   const int slot = lane >> 2, q = lane & 3;
   const long band_stride = (long)D_.nc * D_.wmax;
-  long long xwait = 0;
+  long long xwait = 0, t_sep = 0, t_pre = 0;
   const long long t_start = clock64();
   auto cbar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(ncons) : "memory"); };
+  const long exs = 2L * P * D_.wmax;   // parity stride of yb / xb
+  const long xss = (long)P * D_.wmax;  // parity stride of xs
 
+  // register prefetch cursor (runs D steps ahead of the consumer)
   cplx pre[D][KPL];
-  // schedule of one solve in shared memory
-  StepEnt* sched = reinterpret_cast<StepEnt*>(xsg + A.vec_elems);
-  const int sps = reducer ? 3 * K - 2 : (P > 1 ? 2 : 1) * (2 * m - 1);
-  for (int e = tid; e < sps; e += ncons) {
-    Step st = reducer ? red_decode(e, K) : seg_decode(e, lo, hi, P);
-    StepEnt en;
-    en.row = st.row;
-    en.kind = st.kind;
-    en.blk = st.kind <= 1 ? st.row : st.row * 3 + (st.kind - 2);
-    en.flags = (st.high ? 1 : 0) | (st.ph ? 16 : 0) | (st.js << 8);
-    sched[e] = en;
-  }
-  cbar();
-  // cursor of the next block to load into registers (runs D steps ahead of the consumer)
   int pi = 0, ppos = 0, jp_next = 0;
   int pw = tab[0].w;
-  const cplx* pbase = reducer ? tab[0].red : tab[0].fac;
+  const cplx* pbase = tab[0].fac;
   auto issue = [&](cplx (&dst)[KPL]) {
     if (jp_next < total) {
       const StepEnt en = sched[ppos];
-      load_block(dst, pbase + (long)en.blk * pw * pw, pw, slot_row(wi, slot, en.flags & 1), q);
+      load_block(dst, pbase + (long)en.row * pw * pw, pw, slot_row(wi, slot, en.flags & 1), q);
       ++jp_next;
       if (++ppos == sps) {
         ppos = 0;
-        if (++pi < nsolve) { pw = tab[pi].w; pbase = reducer ? tab[pi].red : tab[pi].fac; }
+        if (++pi < nsolve) { pw = tab[pi].w; pbase = tab[pi].fac; }
       }
     }
   };
@@ -273,26 +199,28 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
   int ci_solve = 0, cpos = 0;
   int cur = 0;
 
-  // ------------------------------------------------------------ segment helpers
-  cplx* bseg = vec0;
-  cplx* yseg = vec1;
-  // epilogue of solve i: gather into Z, publish boundary rows, next correction
+  // ------------------------------------------------------------ per-solve actions
+  // epilogue of solve i: gather into Z, publish boundary rows / separator, next correction
   auto seg_epilogue = [&](int i) {
     const int st = step_of(D_, i);
     const bool bwd = is_bwd(D_, i);
     const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
+    const int par = i & 1;
     if (writes_Z(D_, i)) {
       const int olo = D_.own_lo[s], ohi = D_.own_hi[s], ow = ohi - olo + 1;
       for (int e = tid; e < m * ow; e += ncons) {
         int cl = e / ow, qq = olo + e % ow;
         D_.Z[node_of(D_, a, lo + cl, qq)] = xsg[cl * w + qq];
       }
+      if (p < P - 1)
+        for (int e = tid; e < ow; e += ncons) D_.Z[node_of(D_, a, hi + 1, olo + e)] = xhi[olo + e];
     }
     if (P > 1) {
-      cplx* xb = D_.xb + (long)p * 2 * D_.wmax;
+      cplx* xb = D_.xb + par * exs + (long)p * 2 * D_.wmax;
       for (int e = tid; e < w; e += ncons) {
         xb[e] = xsg[e];
         xb[D_.wmax + e] = xsg[(m - 1) * w + e];
+        if (p < P - 1) D_.xs[par * xss + (long)p * D_.wmax + e] = xhi[e];
       }
     }
     int tdst = -1, side = 0;
@@ -312,6 +240,7 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
       for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction(D_, tdst, side, c, a, X);
     }
   };
+  // RHS of solve i (rows lo..hi) and the couplings of rows lo-1..hi
   auto seg_rhs = [&](int i) {
     const int st = step_of(D_, i);
     const bool bwd = is_bwd(D_, i);
@@ -333,158 +262,170 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
       bne[e] = c >= 0 ? __ldg(nband + (long)c * D_.wmax + qq) : cmk(0, 0);
     }
   };
-
-  // ------------------------------------------------------------ reducer helpers
-  cplx* g = vec0;   // K x WM reduced RHS
-  cplx* z = vec1;   // K x WM: h_k, then z_k, then x_k (in place)
-  auto red_start = [&](int i) {
+  // separator stage of solve i (after phase 1): all-gather, g, x_sep = R^{-1} g rows
+  auto seg_separators = [&](int i) {
     const int st = step_of(D_, i);
     const bool bwd = is_bwd(D_, i);
     const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
+    const int par = i & 1, ppar = par ^ 1;
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     const cplx* cband = D_.cr + s * band_stride;
     const cplx* nband = D_.ne + s * band_stride;
+    cplx* yb = D_.yb + par * exs + (long)p * 2 * D_.wmax;
+    for (int e = tid; e < w; e += ncons) {
+      yb[e] = xsg[e];
+      yb[D_.wmax + e] = xsg[(m - 1) * w + e];
+    }
+    cbar();
     const long long cw0 = clock64();
     if (tid == 0) {
+      __threadfence();
+      red_release_add(&D_.cnt[0], 1u);
       while (ld_relaxed(&D_.cnt[0]) < (unsigned)(P * (i + 1))) __nanosleep(20);
       (void)ld_acquire(&D_.cnt[0]);
     }
     cbar();
     xwait += clock64() - cw0;
-    if (i >= 1) {
-      const int aprev = tab[i - 1].a;
-      const int side = bwd ? next_side(D_) : prev_side(D_);
+    // separator-row transmission corrections (from solve i-1) for every separator
+    if (st > 0 || bwd) {
+      const int aprev = i > 0 ? tab[i - 1].a : 0;
       for (int k = tid; k < K; k += ncons) {
         const int sk = D_.seg_hi[k] + 1;
         auto X = [&](int cc, int qq) -> cplx {
-          if (cc == sk) return z[k * WM + qq];
-          if (cc == sk - 1) return ldcg(D_.xb + (long)k * 2 * D_.wmax + D_.wmax + qq);
-          return ldcg(D_.xb + (long)(k + 1) * 2 * D_.wmax + qq);
+          if (cc == sk) return ldcg(D_.xs + ppar * xss + (long)k * D_.wmax + qq);
+          if (cc == sk - 1) return ldcg(D_.xb + ppar * exs + (long)k * 2 * D_.wmax + D_.wmax + qq);
+          return ldcg(D_.xb + ppar * exs + (long)(k + 1) * 2 * D_.wmax + qq);
         };
-        cplx cv = correction(D_, s, side, sk, aprev, X);
-        if (!bwd) D_.corr_prev[(long)st * D_.nc + sk] = cv;
-        else cnx[k] = cv;
+        cplx cp = cmk(0, 0), cn = cmk(0, 0);
+        if (st > 0) {
+          if (!bwd) {
+            cp = correction(D_, s, prev_side(D_), sk, aprev, X);
+            if (k == p) D_.corr_prev[(long)st * D_.nc + sk] = cp;   // kept for the backward pass
+          } else {
+            cp = ldcg(D_.corr_prev + (long)st * D_.nc + sk);
+          }
+        }
+        if (bwd) cn = correction(D_, s, next_side(D_), sk, aprev, X);
+        cpv[k] = cp;
+        cnv[k] = cn;
       }
       cbar();
     }
+    // g_k = b_{s_k} - U_{h_k}^T y_k[hi] - U_{s_k} y_{k+1}[lo]  (all K separators)
+    const cplx* ybp = D_.yb + par * exs;
     for (int e = tid; e < K * w; e += ncons) {
       const int k = e / w, qq = e % w;
       const int hk = D_.seg_hi[k], sk = hk + 1;
       cplx v = __ldg(D_.R + node_of(D_, a, sk, qq));
-      if (st > 0 && qq == qp) v = cadd(v, D_.corr_prev[(long)st * D_.nc + sk]);
-      if (bwd && qq == qn) v = cadd(v, cnx[k]);
-      const cplx* yh = D_.yb + (long)k * 2 * D_.wmax + D_.wmax;
-      const cplx* yl = D_.yb + (long)(k + 1) * 2 * D_.wmax;
-      cplx t = cmul(__ldg(cband + (long)hk * D_.wmax + qq), ldcg(yh + qq));
-      if (qq >= 1) cfma(t, __ldg(nband + (long)hk * D_.wmax + qq - 1), ldcg(yh + qq - 1));
-      cfma(t, __ldg(cband + (long)sk * D_.wmax + qq), ldcg(yl + qq));
-      if (qq + 1 < w) cfma(t, __ldg(nband + (long)sk * D_.wmax + qq), ldcg(yl + qq + 1));
-      g[k * WM + qq] = csub(v, t);
+      if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
+      if (bwd && qq == qn) v = cadd(v, cnv[k]);
+      const cplx* yh = ybp + (long)k * 2 * D_.wmax + D_.wmax;
+      const cplx* yl = ybp + (long)(k + 1) * 2 * D_.wmax;
+      cplx tt = cmul(__ldg(cband + (long)hk * D_.wmax + qq), ldcg(yh + qq));
+      if (qq >= 1) cfma(tt, __ldg(nband + (long)hk * D_.wmax + qq - 1), ldcg(yh + qq - 1));
+      cfma(tt, __ldg(cband + (long)sk * D_.wmax + qq), ldcg(yl + qq));
+      if (qq + 1 < w) cfma(tt, __ldg(nband + (long)sk * D_.wmax + qq), ldcg(yl + qq + 1));
+      gsm[k * w + qq] = csub(v, tt);
     }
     cbar();
-  };
-  auto red_finish = [&](int i) {
-    const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
-    for (int e = tid; e < K * w; e += ncons) {
-      const int k = e / w, qq = e % w;
-      D_.xs[(long)k * D_.wmax + qq] = z[k * WM + qq];
+    // x_sep[p-1] (rows of separator p-1) and x_sep[p]: rows of R^{-1} times g.
+    // Each warp takes 4 rows at a time; every lane keeps 8 independent loads in
+    // flight (4 rows x 2 columns) so the ~1 MB read is bandwidth-, not latency-bound.
+    const long Kw = (long)K * w;
+    const int r0 = p > 0 ? 0 : w, r1 = p < P - 1 ? 2 * w : w;
+    for (int rb = r0 + 4 * wi; rb < r1; rb += 4 * A.nw) {
+      const cplx* Xr[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = rb + u;
+        ok[u] = rr < r1;
+        const int sk = rr < w ? p - 1 : p, r = rr < w ? rr : rr - w;
+        Xr[u] = ok[u] ? tab[i].xinv + ((long)sk * w + r) * Kw : tab[i].xinv;
+      }
+      cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+      for (long jj = lane; jj < Kw; jj += 64) {
+        const bool two = jj + 32 < Kw;
+        cplx xv[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          xv[u][0] = ok[u] ? __ldcg(Xr[u] + jj) : cmk(0, 0);
+          xv[u][1] = (ok[u] && two) ? __ldcg(Xr[u] + jj + 32) : cmk(0, 0);
+        }
+        const cplx g0 = gsm[jj], g1 = two ? gsm[jj + 32] : cmk(0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cfma(acc[u], xv[u][0], g0);
+          cfma(acc[u], xv[u][1], g1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
+          acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+        }
+        const int rr = rb + u;
+        if (lane == 0 && ok[u]) (rr < w ? xlo : xhi)[rr < w ? rr : rr - w] = acc[u];
+      }
+    }
+    for (int e = tid; e < WM; e += ncons) {
+      if (p == 0) xlo[e] = cmk(0, 0);
+      if (p == P - 1) xhi[e] = cmk(0, 0);
     }
     cbar();
-    if (tid == 0) {
-      __threadfence();
-      st_release(&D_.cnt[1], (unsigned)(i + 1));
-    }
-    if (writes_Z(D_, i)) {
-      const int olo = D_.own_lo[s], ohi = D_.own_hi[s], ow = ohi - olo + 1;
-      for (int e = tid; e < K * ow; e += ncons) {
-        const int k = e / ow, qq = olo + e % ow;
-        D_.Z[node_of(D_, a, D_.seg_hi[k] + 1, qq)] = z[k * WM + qq];
+    // phase-3 RHS: b_lo -= U_{lo-1}^T x_sep[p-1]; b_hi -= U_hi x_sep[p]
+    for (int qq = tid; qq < w; qq += ncons) {
+      if (p > 0) {
+        cplx tt = cmul(bcr[qq], xlo[qq]);
+        if (qq >= 1) cfma(tt, bne[qq - 1], xlo[qq - 1]);
+        bseg[qq] = csub(bseg[qq], tt);
+      }
+      if (p < P - 1) {
+        const cplx* crr = bcr + (long)m * w;      // row hi
+        const cplx* ner = bne + (long)m * w;
+        cplx tt = cmul(crr[qq], xhi[qq]);
+        if (qq + 1 < w) cfma(tt, ner[qq], xhi[qq + 1]);
+        bseg[(m - 1) * w + qq] = csub(bseg[(m - 1) * w + qq], tt);
       }
     }
   };
 
   // ------------------------------------------------------------ one block step
   auto do_step = [&](int j, cplx (&S)[KPL]) {
-    Step s;
-    {
-      const StepEnt en = sched[cpos];
-      s.i = ci_solve; s.kind = en.kind; s.row = en.row; s.high = en.flags & 1;
-      s.js = en.flags >> 8; s.ph = reducer ? 0 : ((P > 1) ? ((en.flags >> 4) & 1) : 1);
-    }
-    const int w = tab[s.i].w;
+    const StepEnt en = sched[cpos];
+    const int i = ci_solve;
+    const int kind = en.kind, row_c = en.row, high = en.flags & 1;
+    const int js = en.flags >> 8, ph3 = (en.flags >> 4) & 1;
+    const int w = tab[i].w;
     // ---- pre-actions (uniform over the CTA)
-    if (!reducer) {
-      if (s.js == 0 && (s.ph == 0 || P == 1)) {
-        if (s.i > 0) {
-          seg_epilogue(s.i - 1);
+    if (js == 0) {
+      const long long cp0 = clock64();
+      if (!ph3 || P == 1) {
+        if (i > 0) {
+          seg_epilogue(i - 1);
           cbar();
         }
-        seg_rhs(s.i);
-        cbar();
-        for (int e = tid; e < w; e += ncons) vbuf[cur * WM + e] = bseg[e];
-        cbar();
-      } else if (s.js == 0 && s.ph == 1) {
-        // end of phase 1: publish y[lo], y[hi]; wait for the separators; phase-3 RHS
-        cplx* yb = D_.yb + (long)p * 2 * D_.wmax;
-        for (int e = tid; e < w; e += ncons) {
-          yb[e] = xsg[e];
-          yb[D_.wmax + e] = xsg[(m - 1) * w + e];
-        }
-        cbar();
-        const long long cw0 = clock64();
-        if (tid == 0) {
-          __threadfence();
-          red_release_add(&D_.cnt[0], 1u);
-          while (ld_relaxed(&D_.cnt[1]) < (unsigned)(s.i + 1)) __nanosleep(20);
-          (void)ld_acquire(&D_.cnt[1]);
-        }
-        cbar();
-        xwait += clock64() - cw0;
-        for (int e = tid; e < w; e += ncons) {
-          xlo[e] = p > 0 ? ldcg(D_.xs + (long)(p - 1) * D_.wmax + e) : cmk(0, 0);
-          xhi[e] = p < P - 1 ? ldcg(D_.xs + (long)p * D_.wmax + e) : cmk(0, 0);
-        }
-        cbar();
-        for (int qq = tid; qq < w; qq += ncons) {
-          if (p > 0) {
-            const cplx* crr = bcr;                    // row lo-1
-            const cplx* ner = bne;
-            cplx t = cmul(crr[qq], xlo[qq]);
-            if (qq >= 1) cfma(t, ner[qq - 1], xlo[qq - 1]);
-            bseg[qq] = csub(bseg[qq], t);
-          }
-          if (p < P - 1) {
-            const cplx* crr = bcr + (long)m * w;      // row hi
-            const cplx* ner = bne + (long)m * w;
-            cplx t = cmul(crr[qq], xhi[qq]);
-            if (qq + 1 < w) cfma(t, ner[qq], xhi[qq + 1]);
-            bseg[(m - 1) * w + qq] = csub(bseg[(m - 1) * w + qq], t);
-          }
-        }
-        cbar();
-        for (int e = tid; e < w; e += ncons) vbuf[cur * WM + e] = bseg[e];
-        cbar();
+        seg_rhs(i);
+      } else {
+        seg_separators(i);
       }
-    } else {
-      if (s.js == 0) red_start(s.i);
+      cbar();
+      for (int e = tid; e < w; e += ncons) vbuf[cur * WM + e] = bseg[e];
+      cbar();
+      if (!ph3 || P == 1) t_pre += clock64() - cp0;
+      else t_sep += clock64() - cp0;
     }
     if (tid == 0) *prog = j;
     // ---- mat-vec on the block held in registers
-    const int row = slot_row(wi, slot, s.high);
+    const int row = slot_row(wi, slot, high);
     const bool act = row >= 0 && row < w;
-    const cplx* vin;
-    if (s.kind <= 1) vin = vbuf + cur * WM;
-    else if (s.kind == 2) vin = g + s.row * WM;
-    else if (s.kind == 3) vin = z + (s.row - 1) * WM;
-    else vin = z + (s.row + 1) * WM;
-    // base for "x = base - acc" steps
+    const cplx* vin = vbuf + cur * WM;
+    const int ci = row_c - lo;   // local block row
     cplx base = cmk(0, 0);
-    const int ci = s.row - lo;   // segment local row
-    if (act) {
-      if (s.kind == 1) base = yseg[ci * w + row];
-      else if (s.kind >= 3) base = z[s.row * WM + row];
-    }
+    if (act && kind == 1) base = yseg[ci * w + row];
     cplx a0 = cmk(0, 0), a1 = cmk(0, 0);
 #pragma unroll
     for (int c = 0; c < KPL; ++c) {
@@ -499,54 +440,46 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
-    cplx o = (s.kind == 1 || s.kind >= 3) ? csub(base, acc) : acc;
+    cplx o = kind == 1 ? csub(base, acc) : acc;
     if (!act) o = cmk(0, 0);
     // neighbour row value (r-1 for the low-halo mapping, r+1 for the high-halo one)
     cplx nb;
-    if (s.high) {
+    if (high) {
       nb.x = __shfl_down_sync(0xffffffffu, o.x, 4);
       nb.y = __shfl_down_sync(0xffffffffu, o.y, 4);
     } else {
       nb.x = __shfl_up_sync(0xffffffffu, o.x, 4);
       nb.y = __shfl_up_sync(0xffffffffu, o.y, 4);
     }
-    // issue the register loads for step j + D (independent of this step's data)
+    // register loads for step j + D (independent of this step's data)
     issue(S);
-    if (q == 0 && act && slot_owned(slot, s.high)) {
-      if (s.kind <= 1) {
-        // forward rows go to yseg (read-only during the backward pass, so a halo
-        // slot can never observe an owner's update); final rows go to xsg
-        if (s.kind == 0) {
-          yseg[ci * w + row] = o;
-          if (s.js == m - 1) xsg[ci * w + row] = o;    // x_hi = y_hi
-        } else {
-          xsg[ci * w + row] = o;
-        }
-        cplx* vn = vbuf + (cur ^ 1) * WM;
-        if (s.kind == 0 && s.js < m - 1) {
-          // forward-style input of row c+1: b_{c+1} - cr_c o - ne_c[r-1] o[r-1]
-          const cplx* cr = bcr + (long)(ci + 1) * w;
-          const cplx* ne = bne + (long)(ci + 1) * w;
-          cplx v = csub(bseg[(ci + 1) * w + row], cmul(cr[row], o));
-          if (row >= 1) v = csub(v, cmul(ne[row - 1], nb));
-          vn[row] = v;
-        } else if (s.kind == 0 ? (m > 1) : (s.row > lo)) {
-          // backward-style input of row c' = (fwd: hi-1, bwd: c-1): cr_c' o + ne_c' o[r+1]
-          const int cp = s.kind == 0 ? hi - 1 : s.row - 1;
-          const cplx* cr = bcr + (long)(cp - lo + 1) * w;
-          const cplx* ne = bne + (long)(cp - lo + 1) * w;
-          cplx v = cmul(cr[row], o);
-          if (row + 1 < w) cfma(v, ne[row], nb);
-          vn[row] = v;
-        }
+    if (q == 0 && act && slot_owned(slot, high)) {
+      cplx* vn = vbuf + (cur ^ 1) * WM;
+      if (kind == 0) {
+        yseg[ci * w + row] = o;
+        if (js == m - 1) xsg[ci * w + row] = o;    // x_hi = y_hi
       } else {
-        z[s.row * WM + row] = o;
+        xsg[ci * w + row] = o;
+      }
+      if (kind == 0 && js < m - 1) {
+        // forward-style input of row c+1: b_{c+1} - cr_c o - ne_c[r-1] o[r-1]
+        const cplx* cr = bcr + (long)(ci + 1) * w;
+        const cplx* ne = bne + (long)(ci + 1) * w;
+        cplx v = csub(bseg[(ci + 1) * w + row], cmul(cr[row], o));
+        if (row >= 1) v = csub(v, cmul(ne[row - 1], nb));
+        vn[row] = v;
+      } else if (kind == 0 ? (m > 1) : (row_c > lo)) {
+        // backward-style input of row c' (fwd: hi-1, bwd: c-1): cr_c' o + ne_c' o[r+1]
+        const int cp = kind == 0 ? hi - 1 : row_c - 1;
+        const cplx* cr = bcr + (long)(cp - lo + 1) * w;
+        const cplx* ne = bne + (long)(cp - lo + 1) * w;
+        cplx v = cmul(cr[row], o);
+        if (row + 1 < w) cfma(v, ne[row], nb);
+        vn[row] = v;
       }
     }
-    const bool need_bar = !(s.kind == 2 && s.js < K - 1);
-    if (need_bar) cbar();
-    if (s.kind <= 1) cur ^= 1;
-    if (reducer && s.js == 3 * K - 3) red_finish(s.i);
+    cbar();
+    cur ^= 1;
     if (++cpos == sps) { cpos = 0; ++ci_solve; }
   };
 
@@ -557,14 +490,11 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
       if (j < total) do_step(j, pre[dd]);
     }
   }
-  if (!reducer) {
-    seg_epilogue(nsolve - 1);
-    cbar();
-  }
+  seg_epilogue(nsolve - 1);
   if (A.prof && tid == 0) {
     long long* o = A.prof + (long)blockIdx.x * 8;
-    o[0] = 0; o[1] = 0; o[2] = 0; o[3] = total; o[4] = xwait;
-    o[5] = clock64() - t_start; o[6] = reducer ? 1 : 0; o[7] = d;
+    o[0] = t_pre; o[1] = t_sep; o[2] = 0; o[3] = total; o[4] = xwait;
+    o[5] = clock64() - t_start; o[6] = 0; o[7] = d;
   }
 }
 
@@ -572,8 +502,9 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
 static constexpr int kFastSmemMax = 227 * 1024;
 extern long long* helm_sweep_prof_buffer();
 
-// Returns HELM_OK and launches if every direction fits the fast kernel
-// (w <= 36); returns -1 (not applicable) otherwise.
+// Launches the register-streaming kernel if every direction fits it (w <= 36
+// and, for P > 1, the explicit separator inverse was built at setup); returns
+// -1 (not applicable) otherwise.
 int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                      cudaStream_t st) {
   using namespace fastk;
@@ -582,35 +513,29 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     wmax = std::max(wmax, dirs[d]->wmax);
     pmax = std::max(pmax, dirs[d]->P);
     nsolve_max = std::max(nsolve_max, dirs[d]->is_double ? 2 * dirs[d]->N - 1 : dirs[d]->N);
+    if (dirs[d]->P > 1 && !dirs[d]->d_xinv) return -1;
   }
   if (wmax > LPR * KPL || wmax > WM) return -1;
   nsolve_max = (nsolve_max + 1) & ~1;
   const int nw = (wmax + OWN - 1) / OWN;
   const int threads = nw * 32 + 32;
   long vec_elems = 0;
-  int ctas = 0;
+  int ctas = 0, sps_max = 1;
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     int mmax = 0;
     for (int p = 0; p < h->P; ++p) mmax = std::max(mmax, h->seg_hi[p] - h->seg_lo[p] + 1);
     vec_elems = std::max(vec_elems, (long)(mmax + 1) * h->wmax);
-    vec_elems = std::max(vec_elems, (long)std::max(h->P - 1, 1) * WM);
-    ctas += h->P + (h->P > 1 ? 1 : 0);
+    vec_elems = std::max(vec_elems, (long)std::max(h->P - 1, 1) * h->wmax);
+    sps_max = std::max(sps_max, (h->P > 1 ? 2 : 1) * (2 * mmax - 1));
+    ctas += h->P;
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
-  size_t head = sizeof(cplx) * (4 * WM + pmax) + sizeof(FastTab) * nsolve_max + 16;
+  size_t head = sizeof(cplx) * (4 * WM + 2 * pmax) + sizeof(FastTab) * nsolve_max + 16;
   head = (head + 127) / 128 * 128;
-  int sps_max = 1;
-  for (int d = 0; d < t; ++d) {
-    const helm_sweep_s* h = dirs[d];
-    int mmax = 0;
-    for (int p = 0; p < h->P; ++p) mmax = std::max(mmax, h->seg_hi[p] - h->seg_lo[p] + 1);
-    sps_max = std::max(sps_max, (h->P > 1 ? 2 : 1) * (2 * mmax - 1));
-    sps_max = std::max(sps_max, 3 * h->P);
-  }
-  size_t smem = head + sizeof(cplx) * 5 * vec_elems + sizeof(StepEnt) * sps_max;
+  size_t smem = head + sizeof(cplx) * 6 * vec_elems + sizeof(StepEnt) * sps_max;
   if (smem > (size_t)kFastSmemMax) return -1;
-  // per-direction scratch (same layout as the general kernel)
+  // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
   std::vector<size_t> off(t);
   size_t total = 0;
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -618,8 +543,8 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     const helm_sweep_s* h = dirs[d];
     off[d] = total;
     total += al(sizeof(unsigned) * 2);
-    total += al(sizeof(cplx) * 2L * h->P * h->wmax) * 2;
-    total += al(sizeof(cplx) * (long)std::max(h->P - 1, 1) * h->wmax);
+    total += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax) * 2;   // yb, xb
+    total += al(sizeof(cplx) * 2L * h->P * h->wmax);           // xs
     total += al(sizeof(cplx) * (long)h->N * h->nc);
     total += al(sizeof(cplx) * (long)h->nc);
   }
@@ -648,18 +573,19 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.seg_lo = h->d_seg_lo; D.seg_hi = h->d_seg_hi;
     D.cr = h->d_cr; D.ne = h->d_ne; D.tc = h->d_tc;
     D.fac = h->d_fac; D.fac_off = h->d_fac_off; D.red = h->d_red; D.red_off = h->d_red_off;
+    D.xinv = h->d_xinv; D.xinv_off = h->d_xinv_off;
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];
     D.cnt = (unsigned*)q; q += al(sizeof(unsigned) * 2);
-    D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
-    D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
-    D.xs = (cplx*)q; q += al(sizeof(cplx) * (long)std::max(h->P - 1, 1) * h->wmax);
+    D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
+    D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
+    D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
     D.corr_prev = (cplx*)q; q += al(sizeof(cplx) * (long)h->N * h->nc);
     D.corr_next = (cplx*)q;
     D.wmax = h->wmax;
     D.cta_base = base;
-    base += h->P + (h->P > 1 ? 1 : 0);
+    base += h->P;
     if (e == cudaSuccess) e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * 2, st);
   }
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_sweep_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

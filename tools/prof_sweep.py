@@ -44,7 +44,7 @@ print(f"config C{a.config} t={a.t} P={info[0].n_segments} w={info[0].wmax}: {ms:
 if os.environ.get("HELM_CYCLES"):
     import ctypes
     L = hs.load()
-    ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)
+    ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)  # upper bound
     buf = torch.zeros(ctas * 8, dtype=torch.int64, device=dev)
     L.helm_sweep_profile.argtypes = [ctypes.c_void_p]
     L.helm_sweep_profile(ctypes.c_void_p(buf.data_ptr()))
@@ -56,7 +56,10 @@ if os.environ.get("HELM_CYCLES"):
         sel = b[b[:, 6] == role]
         if len(sel) == 0:
             continue
+        sel = sel[sel[:, 3] > 0]
         st = sel[:, 3].mean()
+        print(f"  totals per CTA: pre(epilogue+rhs) {sel[:,0].mean():.3e}  sep-stage {sel[:,1].mean():.3e}  "
+              f"steps {(sel[:,5]-sel[:,0]-sel[:,1]).mean():.3e} -> {(sel[:,5]-sel[:,0]-sel[:,1]).mean()/st:.0f} cyc/step")
         print(f"{'reducer' if role else 'segment'} CTAs={len(sel)} steps={st:.0f} total={sel[:,5].mean():.3e} cyc | "
               f"per step: pre|peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
               f"xwait total {sel[:,4].mean():.3e} ({sel[:,4].mean()/sel[:,5].mean()*100:.1f}%)")
