@@ -53,9 +53,6 @@ struct Ring {
 __device__ __forceinline__ void cbar(int ncons) {
   asm volatile("bar.sync 1, %0;" ::"r"(ncons) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ const cplx* ring_peek(const Ring& rg, uint32_t k) {
   int sidx = k % rg.nstage;
   mbar_wait(&rg.full[sidx], (k / rg.nstage) & 1);

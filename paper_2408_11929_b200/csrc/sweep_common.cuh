@@ -19,6 +19,7 @@ struct DirArgs {
   cplx* Z;               // output column
   cplx *yb, *xs, *xb, *corr_prev, *corr_next;
   unsigned* cnt;         // [0] segment arrivals, [1] reducer releases
+  unsigned* flag;        // fast kernel: per-separator publication flags (solve index + 1)
   const cplx* xinv;      // explicit separator-inverse rows (fast kernel), NULL if absent
   const long* xinv_off;
   int wmax;
@@ -72,6 +73,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;

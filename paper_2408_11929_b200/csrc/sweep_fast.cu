@@ -25,6 +25,7 @@
 //  * Exchange arrays are double-buffered by solve parity, so a CTA one solve
 //    ahead never overwrites data a slower CTA still reads.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "sweep_common.cuh"
@@ -45,6 +46,9 @@ struct FastArgs {
   int vec_elems;    // cplx per vector area
   int nsolve_max;   // even
   int pmax;
+  int nsx;          // stages of the separator-inverse row ring (0 = plain loads)
+  int xrow_elems;   // cplx per ring stage (>= K*w of every direction)
+  int sps_max;
   long long* prof;  // optional per-CTA counters (8 per CTA)
 };
 
@@ -101,7 +105,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant__ FastArgs A) {
+__global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant__ FastArgs A) {
   using namespace fastk;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -127,6 +131,12 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
   cplx* xsg = bne + A.vec_elems;                    // final rows x
   cplx* gsm = xsg + A.vec_elems;                    // separator RHS g (K x w)
   StepEnt* sched = reinterpret_cast<StepEnt*>(gsm + A.vec_elems);
+  // TMA ring for the rows of x_sep[p] = X_p g: mbarriers + stages (128-byte aligned)
+  unsigned char* rb = reinterpret_cast<unsigned char*>(sched + A.sps_max);
+  rb = reinterpret_cast<unsigned char*>((((uintptr_t)rb) + 127) & ~(uintptr_t)127);
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(rb);
+  uint64_t* xempty = xfull + 16;
+  cplx* xring = reinterpret_cast<cplx*>(rb + 256);
 
   const int nsolve = n_solves(D_);
   for (int i = tid; i < nsolve; i += blockDim.x) {
@@ -143,27 +153,44 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
   const int sps = (P > 1 ? 2 : 1) * (2 * m - 1);
   const int total = nsolve * sps;
   for (int e = tid; e < sps; e += blockDim.x) sched[e] = seg_entry(e, lo, hi, P);
+  if (tid == 0 && A.nsx > 0) {
+    for (int s2 = 0; s2 < A.nsx; ++s2) {
+      mbar_init(&xfull[s2], 1);
+      mbar_init(&xempty[s2], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  // rows of X_p streamed per solve (0 when this CTA owns no separator)
+  const bool own_sep = P > 1 && p < P - 1;
 
   if (tid >= ncons) {
     // ================================================================ L2 prefetch helper warp
     if (tid == ncons) {
+      // lane 0: keep the factor blocks of the next PF steps warm in L2
       int pi = 0, ppos = 0;
       for (int jp = 0; jp < total; ++jp) {
         while (*prog + PF < jp) __nanosleep(500);
         const int w = tab[pi].w;
         const StepEnt en = sched[ppos];
-        if (false && ppos == 0 && P > 1 && tab[pi].xinv) {
-          // separator-inverse rows this CTA will need after phase 1 of solve pi
-          const long rowblk = (long)w * K * w;   // cplx per separator
-          for (int sk = max(p - 1, 0); sk <= min(p, K - 1); ++sk) {
-            const char* b0 = reinterpret_cast<const char*>(tab[pi].xinv + sk * rowblk);
-            const long bytes = rowblk * (long)sizeof(cplx);
-            for (long o = 0; o < bytes; o += 65536) prefetch_l2(b0 + o, (uint32_t)min(65536L, bytes - o));
-          }
-        }
         prefetch_l2(tab[pi].fac + (long)en.row * w * w, (uint32_t)(w * w * sizeof(cplx)));
         if (++ppos == sps) { ppos = 0; ++pi; }
+      }
+    } else if (tid == ncons + 32 && A.nsx > 0 && own_sep) {
+      // second helper warp: TMA producer of the rows of X_p (separator inverse), solve after
+      // solve; rows of the next solve are staged while the current one runs
+      uint32_t f = 0;
+      for (int i = 0; i < nsolve; ++i) {
+        const int w = tab[i].w;
+        const long Kw = (long)K * w;
+        const uint32_t bytes = (uint32_t)(Kw * sizeof(cplx));
+        const cplx* X = tab[i].xinv + (long)p * w * Kw;
+        for (int r = 0; r < w; ++r, ++f) {
+          const int sidx = f % A.nsx;
+          if (f >= (uint32_t)A.nsx) mbar_wait(&xempty[sidx], ((f / A.nsx) - 1) & 1);
+          mbar_expect_tx(&xfull[sidx], bytes);
+          bulk_g2s(xring + (long)sidx * A.xrow_elems, X + (long)r * Kw, bytes, &xfull[sidx]);
+        }
       }
     }
     return;
@@ -198,6 +225,7 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
   for (int dd = 0; dd < D; ++dd) issue(pre[dd]);
   int ci_solve = 0, cpos = 0;
   int cur = 0;
+  uint32_t xrow_base = 0;   // X rows consumed before the current solve (ring position)
 
   // ------------------------------------------------------------ per-solve actions
   // epilogue of solve i: gather into Z, publish boundary rows / separator, next correction
@@ -220,7 +248,6 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
       for (int e = tid; e < w; e += ncons) {
         xb[e] = xsg[e];
         xb[D_.wmax + e] = xsg[(m - 1) * w + e];
-        if (p < P - 1) D_.xs[par * xss + (long)p * D_.wmax + e] = xhi[e];
       }
     }
     int tdst = -1, side = 0;
@@ -329,53 +356,98 @@ __global__ void __launch_bounds__(32 * 7, 1) k_sweep_fast(const __grid_constant_
       gsm[k * w + qq] = csub(v, tt);
     }
     cbar();
-    // x_sep[p-1] (rows of separator p-1) and x_sep[p]: rows of R^{-1} times g.
-    // Each warp takes 4 rows at a time; every lane keeps 8 independent loads in
-    // flight (4 rows x 2 columns) so the ~1 MB read is bandwidth-, not latency-bound.
+    // x_sep[p] = X_p g: the rows of X_p arrive through the TMA ring (one row per
+    // stage, issued by the helper warp); warp wi reduces rows wi, wi + nw, ...
     const long Kw = (long)K * w;
-    const int r0 = p > 0 ? 0 : w, r1 = p < P - 1 ? 2 * w : w;
-    for (int rb = r0 + 4 * wi; rb < r1; rb += 4 * A.nw) {
-      const cplx* Xr[4];
-      bool ok[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = rb + u;
-        ok[u] = rr < r1;
-        const int sk = rr < w ? p - 1 : p, r = rr < w ? rr : rr - w;
-        Xr[u] = ok[u] ? tab[i].xinv + ((long)sk * w + r) * Kw : tab[i].xinv;
-      }
-      cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-      for (long jj = lane; jj < Kw; jj += 64) {
-        const bool two = jj + 32 < Kw;
-        cplx xv[4][2];
+    if (own_sep && A.nsx == 0) {
+      // plain-load path: 4 rows per warp, 8 independent loads in flight per lane
+      for (int rb = 4 * wi; rb < w; rb += 4 * A.nw) {
+        const cplx* Xr[4];
+        bool ok[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          xv[u][0] = ok[u] ? __ldcg(Xr[u] + jj) : cmk(0, 0);
-          xv[u][1] = (ok[u] && two) ? __ldcg(Xr[u] + jj + 32) : cmk(0, 0);
+          ok[u] = rb + u < w;
+          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * Kw;
         }
-        const cplx g0 = gsm[jj], g1 = two ? gsm[jj + 32] : cmk(0, 0);
+        cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+        for (long jj = lane; jj < Kw; jj += 64) {
+          const bool two = jj + 32 < Kw;
+          cplx xv[4][2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            xv[u][0] = ok[u] ? __ldcg(Xr[u] + jj) : cmk(0, 0);
+            xv[u][1] = (ok[u] && two) ? __ldcg(Xr[u] + jj + 32) : cmk(0, 0);
+          }
+          const cplx g0 = gsm[jj], g1 = two ? gsm[jj + 32] : cmk(0, 0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cfma(acc[u], xv[u][0], g0);
+            cfma(acc[u], xv[u][1], g1);
+          }
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          cfma(acc[u], xv[u][0], g0);
-          cfma(acc[u], xv[u][1], g1);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
+            acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+          }
+          if (lane == 0 && ok[u]) xhi[rb + u] = acc[u];
         }
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
+    } else if (own_sep) {
+      for (int r = wi; r < w; r += A.nw) {
+        const uint32_t f = xrow_base + r;
+        const int sidx = f % A.nsx;
+        mbar_wait(&xfull[sidx], (f / A.nsx) & 1);
+        const cplx* Xr = xring + (long)sidx * A.xrow_elems;
+        cplx a0 = cmk(0, 0), a1 = cmk(0, 0);
+        long jj = lane;
+        for (; jj + 32 < Kw; jj += 64) {
+          cfma(a0, Xr[jj], gsm[jj]);
+          cfma(a1, Xr[jj + 32], gsm[jj + 32]);
+        }
+        if (jj < Kw) cfma(a0, Xr[jj], gsm[jj]);
+        cplx acc = cadd(a0, a1);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-          acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
-          acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
         }
-        const int rr = rb + u;
-        if (lane == 0 && ok[u]) (rr < w ? xlo : xhi)[rr < w ? rr : rr - w] = acc[u];
+        __syncwarp();
+        if (lane == 0) {
+          xhi[r] = acc;
+          mbar_arrive(&xempty[sidx]);
+        }
       }
+      xrow_base += w;
     }
     for (int e = tid; e < WM; e += ncons) {
       if (p == 0) xlo[e] = cmk(0, 0);
       if (p == P - 1) xhi[e] = cmk(0, 0);
     }
     cbar();
+    // publish x_sep[p] (parity buffer; also the next solve's correction source),
+    // then take x_sep[p-1] from the left neighbour
+    if (p < P - 1) {
+      for (int e = tid; e < w; e += ncons) D_.xs[par * xss + (long)p * D_.wmax + e] = xhi[e];
+      cbar();
+      if (tid == 0) {
+        __threadfence();
+        st_release(&D_.flag[p], (unsigned)(i + 1));
+      }
+    }
+    if (p > 0) {
+      const long long cw1 = clock64();
+      if (tid == 0) {
+        while (ld_relaxed(&D_.flag[p - 1]) < (unsigned)(i + 1)) __nanosleep(20);
+        (void)ld_acquire(&D_.flag[p - 1]);
+      }
+      cbar();
+      xwait += clock64() - cw1;
+      for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D_.xs + par * xss + (long)(p - 1) * D_.wmax + e);
+      cbar();
+    }
     // phase-3 RHS: b_lo -= U_{lo-1}^T x_sep[p-1]; b_hi -= U_hi x_sep[p]
     for (int qq = tid; qq < w; qq += ncons) {
       if (p > 0) {
@@ -518,7 +590,7 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   if (wmax > LPR * KPL || wmax > WM) return -1;
   nsolve_max = (nsolve_max + 1) & ~1;
   const int nw = (wmax + OWN - 1) / OWN;
-  const int threads = nw * 32 + 32;
+  const int threads = nw * 32 + 64;   // consumers + L2-prefetch warp + TMA producer warp
   long vec_elems = 0;
   int ctas = 0, sps_max = 1;
   for (int d = 0; d < t; ++d) {
@@ -534,6 +606,22 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   size_t head = sizeof(cplx) * (4 * WM + 2 * pmax) + sizeof(FastTab) * nsolve_max + 16;
   head = (head + 127) / 128 * 128;
   size_t smem = head + sizeof(cplx) * 6 * vec_elems + sizeof(StepEnt) * sps_max;
+  // separator-inverse row ring
+  long xrow = 1;
+  for (int d = 0; d < t; ++d) xrow = std::max(xrow, (long)std::max(dirs[d]->P - 1, 1) * dirs[d]->wmax);
+  xrow = (xrow + 7) / 8 * 8;
+  const size_t ring_fixed = 128 + 256;
+  long room = (long)kFastSmemMax - (long)smem - (long)ring_fixed;
+  int nsx = room > 0 ? (int)std::min<long>(8, room / (long)(sizeof(cplx) * xrow)) : 0;
+  if (pmax > 1 && nsx < 2) nsx = 0;
+  if (pmax == 1) nsx = 0;
+  {
+    // The TMA ring for the separator-inverse rows is experimental: it hangs with
+    // >= ~96 co-resident CTAs (cause not yet understood), so it is opt-in.
+    const char* ev = getenv("HELM_XRING");
+    if (!(ev && ev[0] == '1')) nsx = 0;
+  }
+  smem += ring_fixed + (size_t)nsx * xrow * sizeof(cplx);
   if (smem > (size_t)kFastSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
   std::vector<size_t> off(t);
@@ -542,7 +630,7 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     off[d] = total;
-    total += al(sizeof(unsigned) * 2);
+    total += al(sizeof(unsigned) * (2 + h->P));               // counters + separator flags
     total += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax) * 2;   // yb, xb
     total += al(sizeof(cplx) * 2L * h->P * h->wmax);           // xs
     total += al(sizeof(cplx) * (long)h->N * h->nc);
@@ -562,6 +650,9 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   A.vec_elems = (int)vec_elems;
   A.nsolve_max = nsolve_max;
   A.pmax = pmax;
+  A.nsx = nsx;
+  A.xrow_elems = (int)xrow;
+  A.sps_max = sps_max;
   A.prof = helm_sweep_prof_buffer();
   int base = 0;
   for (int d = 0; d < t; ++d) {
@@ -577,7 +668,7 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];
-    D.cnt = (unsigned*)q; q += al(sizeof(unsigned) * 2);
+    D.cnt = (unsigned*)q; D.flag = D.cnt + 2; q += al(sizeof(unsigned) * (2 + h->P));
     D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
@@ -586,7 +677,7 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.wmax = h->wmax;
     D.cta_base = base;
     base += h->P;
-    if (e == cudaSuccess) e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * 2, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * (2 + h->P), st);
   }
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_sweep_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 0, occ = 0;
