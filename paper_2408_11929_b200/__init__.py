@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhelmsweep.so")
+LIB_PATH = os.environ.get("HELM_LIB") or os.path.join(_HERE, "libhelmsweep.so")
 
 HELM_OK = 0
 STATUS = {0: "HELM_OK", 1: "HELM_EINVAL", 2: "HELM_EDIM", 3: "HELM_ESINGULAR", 4: "HELM_ECUDA",

@@ -35,6 +35,28 @@ extern "C" const char* helm_strerror(int code) {
   }
 }
 
+// ------------------------------------------------------------------ device memory
+cudaError_t helm_dev_alloc(void** p, size_t bytes) {
+  static bool pool_ready = false;
+  if (!pool_ready) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_ready = true;
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 16, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  return e;
+}
+
+void helm_dev_free(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+
 // ------------------------------------------------------------------ staging
 bool helm_is_device_ptr(const void* p) {
   if (!p) return false;
@@ -183,16 +205,19 @@ extern "C" int helm_assemble(const helm_grid_desc* gd, void* stream, helm_proble
     return HELM_ECUDA;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  static long next_uid = 1;
   helm_problem_s* p = new helm_problem_s();
+  p->uid = next_uid++;
   p->nx = gd->nx; p->ny = gd->ny; p->h = gd->h; p->omega = gd->omega;
   p->n = (long)(gd->nx + 1) * (gd->ny + 1);
   size_t vb = sizeof(cplx) * p->n;
   cudaError_t e = cudaSuccess;
-  e = cudaMalloc(&p->c, sizeof(double) * p->n);
-  if (e == cudaSuccess) e = cudaMalloc(&p->dC, vb);
-  if (e == cudaSuccess) e = cudaMalloc(&p->dE, vb);
-  if (e == cudaSuccess) e = cudaMalloc(&p->dN, vb);
-  if (e == cudaSuccess) e = cudaMalloc(&p->dNE, vb);
+  p->c = nullptr; p->dC = p->dE = p->dN = p->dNE = nullptr;
+  e = helm_dev_alloc((void**)&p->c, sizeof(double) * p->n);
+  if (e == cudaSuccess) e = helm_dev_alloc((void**)&p->dC, vb);
+  if (e == cudaSuccess) e = helm_dev_alloc((void**)&p->dE, vb);
+  if (e == cudaSuccess) e = helm_dev_alloc((void**)&p->dN, vb);
+  if (e == cudaSuccess) e = helm_dev_alloc((void**)&p->dNE, vb);
   if (e != cudaSuccess) {
     helm_set_error("helm_assemble: cudaMalloc: %s", cudaGetErrorString(e));
     helm_problem_destroy(p);
@@ -280,10 +305,10 @@ extern "C" int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols
 extern "C" void helm_problem_destroy(helm_problem_t p) {
   if (!p) return;
   helm_problem_free_ws(p);
-  cudaFree(p->c);
-  cudaFree(p->dC);
-  cudaFree(p->dE);
-  cudaFree(p->dN);
-  cudaFree(p->dNE);
+  helm_dev_free(p->c);
+  helm_dev_free(p->dC);
+  helm_dev_free(p->dE);
+  helm_dev_free(p->dN);
+  helm_dev_free(p->dNE);
   delete p;
 }

@@ -68,6 +68,14 @@ extern long g_helm_launches;
     if (_rc != HELM_OK) return _rc; \
   } while (0)
 
+// ------------------------------------------------------------------ device memory
+// Handle and workspace memory comes from the device's default stream-ordered
+// pool with an unlimited release threshold: freed blocks stay in the pool, so
+// the per-problem / per-sweep buffers of repeated solves are reused instead of
+// being mapped and unmapped by cudaMalloc / cudaFree every time.
+cudaError_t helm_dev_alloc(void** p, size_t bytes);
+void helm_dev_free(void* p);
+
 // ------------------------------------------------------------------ handles
 struct helm_problem_s {
   int nx, ny;
@@ -79,6 +87,7 @@ struct helm_problem_s {
   cplx* dN;
   cplx* dNE;
   void* ws = nullptr;  // cached MPGMRES workspace (krylov.cu), grown on demand
+  long uid = 0;        // unique id (factor-set sharing key; addresses can be reused)
 };
 void helm_problem_free_ws(helm_problem_s* p);
 
@@ -110,6 +119,9 @@ struct helm_sweep_s {
   // explicit rows of the separator inverse (w <= 36 only): per strip, separator k:
   // w x (K w) row-major at xinv_off[s] + k * w * K * w
   cplx* d_xinv = nullptr; std::vector<long> xinv_off; long* d_xinv_off = nullptr;
+  // the band/factor arrays above are shared by every handle with the same
+  // (problem, axis, N, overlap, P) -- e.g. LRL and RLR -- through this record
+  struct SharedFactors* shared = nullptr;
   long factor_bytes;
 };
 

@@ -6,11 +6,17 @@
 // Tall-skinny reductions are deterministic two-stage sums (per-block partials
 // in a fixed row order, then a fixed-order sum over blocks): no fp64 atomics,
 // so reruns are bitwise reproducible.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <complex>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 int helm_spmm_dev(const helm_problem_s* p, const cplx* X, cplx* Y, int ncols, long ld, cudaStream_t st);
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
@@ -115,6 +121,236 @@ __global__ void k_gemv(long n, const cplx* __restrict__ Z, long ldz, int ncols, 
 __global__ void k_axpy_sub(long n, const cplx* __restrict__ b, const cplx* __restrict__ ax, cplx* __restrict__ r) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     r[i] = csub(b[i], ax[i]);
+}
+
+
+// ------------------------------------------------------------------ fused orthogonalisation
+// One cooperative launch per iteration runs row a6 (D10 steps 4-5):
+//   gram_i = ||A z_i||^2                               (deflation reference)
+//   C1 = V^H W; W -= V C1; C2 = V^H W; W -= V C2         (BCGS2 against V_1..k)
+//   for i = 0..t-1: two CGS passes of w_i against the new slots V[:, m..m+i),
+//     nrm_i = ||w_i||, keep iff nrm_i > 1e-10 ||A z_i||, V[:, m+i] = w_i/nrm_i (else 0)
+// Block b owns a contiguous row range and walks it in tiles of kOrthTile rows:
+// a tile of W is updated (thread per row) and staged in shared memory, then the
+// warps form the projections (warp per V column, lanes over rows) into per-block
+// partials.  Reductions are two-stage in a fixed order (partials, grid sync, a
+// fixed-order sum over blocks), so results are bitwise reproducible; norms are
+// summed redundantly by every block, which saves the grid sync that would
+// broadcast the keep/drop decision.  ~5 grid syncs per column instead of ~10
+// launches and a host round trip per column.
+static constexpr int kOrthTile = 1024;
+static constexpr int kOrthThreads = 256;
+
+struct OrthArgs {
+  long n;
+  cplx* V;          // n x (m + t), ld n; the new slots start at column m
+  int m, t;
+  cplx* W;          // n x t (A Z_k on entry, orthogonalised on exit)
+  cplx* part;       // nblk x S partial sums, S = (m + 1) * t
+  cplx* out;        // [C1 m*t][C2 m*t][gram t*t][cv 2*t*t][nn t]  (host copy, one D2H)
+  long rows;        // rows per block
+};
+
+// One pass over this block's rows.  Optional update W[:, wc0+i] -= sum_j Vb[:, j] Cs[j*tc+i]
+// (i < tc); then optional projections outsm[j*tc+i] = sum conj(Vb[:, j]) W[:, wc0+i] (j < mcols)
+// and squared norms outsm[mcols*tc + q] = ||W[:, nc0+q]||^2 (q < nn).
+__device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* outsm, const cplx* Vb, int mcols,
+                          int wc0, int tc, bool upd, bool dots, int nc0, int nn, long r0, long r1) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int nout = (dots ? mcols * tc : 0) + nn;
+  for (int e = threadIdx.x; e < nout; e += blockDim.x) outsm[e] = cmk(0, 0);
+  __syncthreads();
+  for (long t0 = r0; t0 < r1; t0 += kOrthTile) {
+    const int rows = (int)min((long)kOrthTile, r1 - t0);
+    for (int rr = threadIdx.x; rr < rows; rr += blockDim.x) {
+      const long r = t0 + rr;
+      cplx w[kMaxT];
+#pragma unroll
+      for (int i = 0; i < kMaxT; ++i)
+        if (i < tc) w[i] = a.W[(long)(wc0 + i) * a.n + r];
+      if (upd) {
+        cplx acc[kMaxT];
+#pragma unroll
+        for (int i = 0; i < kMaxT; ++i) acc[i] = cmk(0, 0);
+        int j = 0;
+        for (; j + 8 <= mcols; j += 8) {   // eight independent loads in flight per thread
+          cplx v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(Vb + (long)(j + u) * a.n + r);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int i = 0; i < kMaxT; ++i)
+              if (i < tc) cfma(acc[i], v[u], Cs[(j + u) * tc + i]);
+        }
+        for (; j < mcols; ++j) {
+          const cplx v = __ldcg(Vb + (long)j * a.n + r);
+#pragma unroll
+          for (int i = 0; i < kMaxT; ++i)
+            if (i < tc) cfma(acc[i], v, Cs[j * tc + i]);
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxT; ++i)
+          if (i < tc) {
+            w[i] = csub(w[i], acc[i]);
+            a.W[(long)(wc0 + i) * a.n + r] = w[i];
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxT; ++i)
+        if (i < tc) Wt[i * kOrthTile + rr] = w[i];
+    }
+    __syncthreads();
+    const int jn = (dots ? mcols : 0) + nn;
+    for (int j = warp; j < jn; j += nw) {
+      const bool isdot = dots && j < mcols;
+      cplx acc[kMaxT];
+#pragma unroll
+      for (int i = 0; i < kMaxT; ++i) acc[i] = cmk(0, 0);
+      if (isdot) {
+        const cplx* v = Vb + (long)j * a.n + t0;
+        int rr = lane;
+        for (; rr + 224 < rows; rr += 256) {   // eight independent loads in flight per lane
+          cplx vv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) vv[u] = __ldcg(v + rr + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int i = 0; i < kMaxT; ++i)
+              if (i < tc) cfmaconj(acc[i], vv[u], Wt[i * kOrthTile + rr + 32 * u]);
+        }
+        for (; rr < rows; rr += 32) {
+          const cplx vv = __ldcg(v + rr);
+#pragma unroll
+          for (int i = 0; i < kMaxT; ++i)
+            if (i < tc) cfmaconj(acc[i], vv, Wt[i * kOrthTile + rr]);
+        }
+      } else {
+        const int c = nc0 + (j - (dots ? mcols : 0)) - wc0;
+        for (int rr = lane; rr < rows; rr += 32) {
+          const cplx ww = Wt[c * kOrthTile + rr];
+          cfmaconj(acc[0], ww, ww);
+        }
+      }
+      const int na = isdot ? tc : 1;
+#pragma unroll
+      for (int i = 0; i < kMaxT; ++i) {
+        if (i >= na) break;
+        for (int off = 16; off > 0; off >>= 1) {
+          acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, off);
+          acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, off);
+        }
+      }
+      if (lane == 0) {
+        if (isdot) {
+#pragma unroll
+          for (int i = 0; i < kMaxT; ++i)
+            if (i < tc) outsm[j * tc + i] = cadd(outsm[j * tc + i], acc[i]);
+        }
+        else
+          outsm[(dots ? mcols * tc : 0) + (j - (dots ? mcols : 0))] =
+              cadd(outsm[(dots ? mcols * tc : 0) + (j - (dots ? mcols : 0))], acc[0]);
+      }
+    }
+    __syncthreads();
+  }
+  const int S = (a.m + 1) * a.t;
+  for (int e = threadIdx.x; e < nout; e += blockDim.x) a.part[(long)blockIdx.x * S + e] = outsm[e];
+}
+
+// dst[e] = sum_b part[b][off + e] for e < count, fixed order over b (grid-strided)
+__device__ __forceinline__ void orth_reduce(const OrthArgs& a, int off, int count, cplx* dst) {
+  const int S = (a.m + 1) * a.t;
+  const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x, gsz = (long)gridDim.x * blockDim.x;
+  for (long e = gtid; e < count; e += gsz) {
+    cplx acc = cmk(0, 0);
+    for (int b = 0; b < (int)gridDim.x; ++b) acc = cadd(acc, __ldcg(a.part + (long)b * S + off + e));
+    dst[e] = acc;
+  }
+}
+
+// every block: the same fixed-order sum of one norm partial (no broadcast sync needed)
+__device__ __forceinline__ double orth_norm2(const OrthArgs& a, int off) {
+  __shared__ double s;
+  const int S = (a.m + 1) * a.t;
+  if (threadIdx.x == 0) {
+    double acc = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) acc += __ldcg(a.part + (long)b * S + off).x;
+    s = acc;
+  }
+  __syncthreads();
+  const double v = s;
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(kOrthThreads) k_orth(OrthArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ cplx osm[];
+  const int m = a.m, t = a.t;
+  cplx* Wt = osm;                                  // kOrthTile * t
+  cplx* Cs = Wt + (long)kOrthTile * t;             // m * t
+  cplx* outsm = Cs + (long)m * t;                  // (m + 1) * t
+  const long r0 = min(a.n, (long)blockIdx.x * a.rows), r1 = min(a.n, r0 + a.rows);
+  cplx* C1 = a.out;
+  cplx* C2 = C1 + (long)m * t;
+  cplx* gram = C2 + (long)m * t;
+  cplx* cv = gram + t * t;
+  cplx* nn = cv + 2 * t * t;
+  cplx* Vn = a.V + (long)m * a.n;
+  auto load_C = [&](const cplx* C, int cnt) {
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) Cs[e] = __ldcg(C + e);
+    __syncthreads();
+  };
+  // C1 = V^H W and ||w_i||^2 (the Gram diagonal)
+  orth_pass(a, Wt, Cs, outsm, a.V, m, 0, t, false, true, 0, t, r0, r1);
+  grid.sync();
+  orth_reduce(a, 0, m * t, C1);
+  {
+    const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gtid < t) {
+      cplx acc = cmk(0, 0);
+      for (int b = 0; b < (int)gridDim.x; ++b) acc = cadd(acc, __ldcg(a.part + (long)b * (m + 1) * t + m * t + gtid));
+      gram[gtid * t + gtid] = acc;
+    }
+  }
+  grid.sync();
+  // W -= V C1; C2 = V^H W
+  load_C(C1, m * t);
+  orth_pass(a, Wt, Cs, outsm, a.V, m, 0, t, true, true, 0, 0, r0, r1);
+  grid.sync();
+  orth_reduce(a, 0, m * t, C2);
+  grid.sync();
+  // W -= V C2 and ||w_0||^2
+  load_C(C2, m * t);
+  orth_pass(a, Wt, Cs, outsm, a.V, m, 0, t, true, false, 0, 1, r0, r1);
+  for (int i = 0; i < t; ++i) {
+    if (i > 0) {
+      // pass 0: c = Vn[:, :i]^H w_i
+      orth_pass(a, Wt, Cs, outsm, Vn, i, i, 1, false, true, 0, 0, r0, r1);
+      grid.sync();
+      orth_reduce(a, 0, i, cv + (long)i * t);
+      grid.sync();
+      // pass 1: w_i -= Vn c; c' = Vn^H w_i
+      load_C(cv + (long)i * t, i);
+      orth_pass(a, Wt, Cs, outsm, Vn, i, i, 1, true, true, 0, 0, r0, r1);
+      grid.sync();
+      orth_reduce(a, 0, i, cv + (long)t * t + (long)i * t);
+      grid.sync();
+      // w_i -= Vn c'; ||w_i||^2
+      load_C(cv + (long)t * t + (long)i * t, i);
+      orth_pass(a, Wt, Cs, outsm, Vn, i, i, 1, true, false, i, 1, r0, r1);
+    }
+    grid.sync();
+    // keep iff ||w_i|| > 1e-10 ||A z_i|| (D10 step 5); gram[i] is visible after the syncs above
+    const double nrm = sqrt(fmax(orth_norm2(a, 0), 0.0));
+    const double naz = sqrt(fmax(__ldcg(gram + i * t + i).x, 0.0));
+    const double sc = nrm > 1e-10 * naz ? 1.0 / nrm : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) nn[i] = cmk(nrm, 0.0);
+    for (long r = r0 + threadIdx.x; r < r1; r += blockDim.x) Vn[(long)i * a.n + r] = cscale(a.W[(long)i * a.n + r], sc);
+    grid.sync();
+  }
 }
 
 namespace {
@@ -285,12 +521,27 @@ struct KrylovWS {
   long partial_cap = 0;
 };
 
+// Pinned host staging for the per-iteration small D2H copy.  One buffer per
+// host thread, grown on demand and never returned: cudaFreeHost synchronises
+// the device and can take hundreds of ms, so it must not run per problem.
+static cplx* pinned_small(size_t count) {
+  static thread_local cplx* buf = nullptr;
+  static thread_local size_t cap = 0;
+  if (count > cap) {
+    cplx* nb = nullptr;
+    if (cudaMallocHost((void**)&nb, sizeof(cplx) * count) != cudaSuccess) return nullptr;
+    if (buf) cudaFreeHost(buf);
+    buf = nb;
+    cap = count;
+  }
+  return buf;
+}
+
 static void ws_free(KrylovWS* w) {
   if (!w) return;
-  cudaFree(w->V); cudaFree(w->Z); cudaFree(w->W); cudaFree(w->Rsrc); cudaFree(w->tmp);
-  cudaFree(w->partial); cudaFree(w->dC1); cudaFree(w->dC2); cudaFree(w->dsm); cudaFree(w->dy);
-  cudaFree(w->dscal);
-  if (w->hsmall) cudaFreeHost(w->hsmall);
+  helm_dev_free(w->V); helm_dev_free(w->Z); helm_dev_free(w->W); helm_dev_free(w->Rsrc); helm_dev_free(w->tmp);
+  helm_dev_free(w->partial); helm_dev_free(w->dC1); helm_dev_free(w->dC2); helm_dev_free(w->dsm); helm_dev_free(w->dy);
+  helm_dev_free(w->dscal);
   delete w;
 }
 
@@ -307,42 +558,44 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
   const long n = p->n;
   cudaError_t e = cudaSuccess;
   if (t > w->tcap) {
-    cudaFree(w->W); cudaFree(w->Rsrc); cudaFree(w->tmp); cudaFree(w->dscal);
+    helm_dev_free(w->W); helm_dev_free(w->Rsrc); helm_dev_free(w->tmp); helm_dev_free(w->dscal);
     w->W = w->Rsrc = w->tmp = nullptr; w->dscal = nullptr;
-    if (e == cudaSuccess) e = cudaMalloc(&w->W, sizeof(cplx) * n * t);
-    if (e == cudaSuccess) e = cudaMalloc(&w->Rsrc, sizeof(cplx) * n * t);
-    if (e == cudaSuccess) e = cudaMalloc(&w->tmp, sizeof(cplx) * n);
-    if (e == cudaSuccess) e = cudaMalloc(&w->dscal, sizeof(double) * 16);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->W, sizeof(cplx) * n * t);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->Rsrc, sizeof(cplx) * n * t);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->tmp, sizeof(cplx) * n);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dscal, sizeof(double) * 16);
     w->tcap = t;
     w->icap = 0;   // column capacities depend on t
   }
   if (e == cudaSuccess && (long)iters * t > (long)w->icap * w->tcap) {
     const long vc = 1 + (long)iters * t, zc = (long)iters * t;
     cplx *V2 = nullptr, *Z2 = nullptr;
-    e = cudaMalloc(&V2, sizeof(cplx) * n * vc);
-    if (e == cudaSuccess) e = cudaMalloc(&Z2, sizeof(cplx) * n * zc);
+    e = helm_dev_alloc((void**)&V2, sizeof(cplx) * n * vc);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&Z2, sizeof(cplx) * n * zc);
     if (e == cudaSuccess && keepV > 0) e = cudaMemcpyAsync(V2, w->V, sizeof(cplx) * n * keepV, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess && keepZ > 0) e = cudaMemcpyAsync(Z2, w->Z, sizeof(cplx) * n * keepZ, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
-      cudaFree(V2); cudaFree(Z2);
+      helm_dev_free(V2); helm_dev_free(Z2);
       helm_set_error("mpgmres_solve: basis of %ld columns: %s", vc, cudaGetErrorString(e));
       return HELM_ENOMEM;
     }
-    cudaFree(w->V); cudaFree(w->Z);
+    helm_dev_free(w->V); helm_dev_free(w->Z);
     w->V = V2; w->Z = Z2;
-    cudaFree(w->dC1); cudaFree(w->dC2); cudaFree(w->dsm); cudaFree(w->dy); cudaFree(w->partial);
+    helm_dev_free(w->dC1); helm_dev_free(w->dC2); helm_dev_free(w->dsm); helm_dev_free(w->dy); helm_dev_free(w->partial);
     w->dC1 = w->dC2 = w->dsm = w->dy = w->partial = nullptr;
-    if (w->hsmall) cudaFreeHost(w->hsmall);
     w->hsmall = nullptr;
-    w->partial_cap = ((n + kDotChunk - 1) / kDotChunk) * kMaxT * vc * t;
+    w->partial_cap = std::max(((n + kDotChunk - 1) / kDotChunk) * kMaxT * vc * t, 148L * 4 * (vc + 1) * t);
     w->small_cap = 4 * vc * t + 64;
-    e = cudaMalloc(&w->dC1, sizeof(cplx) * vc * t);
-    if (e == cudaSuccess) e = cudaMalloc(&w->dC2, sizeof(cplx) * vc * t);
-    if (e == cudaSuccess) e = cudaMalloc(&w->dsm, sizeof(cplx) * w->small_cap);
-    if (e == cudaSuccess) e = cudaMalloc(&w->dy, sizeof(cplx) * zc);
-    if (e == cudaSuccess) e = cudaMalloc(&w->partial, sizeof(cplx) * w->partial_cap);
-    if (e == cudaSuccess) e = cudaMallocHost(&w->hsmall, sizeof(cplx) * w->small_cap);
+    e = helm_dev_alloc((void**)&w->dC1, sizeof(cplx) * vc * t);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dC2, sizeof(cplx) * vc * t);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dsm, sizeof(cplx) * w->small_cap);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dy, sizeof(cplx) * zc);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->partial, sizeof(cplx) * w->partial_cap);
+    if (e == cudaSuccess) {
+      w->hsmall = pinned_small(w->small_cap);
+      if (!w->hsmall) e = cudaErrorMemoryAllocation;
+    }
     w->icap = (int)(zc / t);
   }
   if (e != cudaSuccess) {
@@ -350,6 +603,39 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
     return HELM_ENOMEM;
   }
   return HELM_OK;
+}
+
+// Launch k_orth cooperatively (one launch per iteration).  Returns 1 when it
+// ran, 0 when the shapes exceed its shared-memory plan (the caller then uses
+// the multi-launch sequence), -1 on a CUDA error (message set).
+static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cudaStream_t st) {
+  if (getenv("HELM_ORTH_UNFUSED")) return 0;
+  const size_t smem = sizeof(cplx) * ((size_t)kOrthTile * t + (size_t)m * t + (size_t)(m + 1) * t);
+  if (smem > 200 * 1024) return 0;
+  static int nsm = 0;
+  int dev = 0;
+  if (!nsm) {
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_orth, kOrthThreads, smem);
+  if (e != cudaSuccess || occ < 1) return 0;
+  long nblk = std::min<long>((long)nsm * std::min(occ, 4), (n + kOrthThreads - 1) / kOrthThreads);
+  if ((long)nblk * (m + 1) * t > ws->partial_cap) nblk = ws->partial_cap / ((long)(m + 1) * t);
+  if (nblk < 1) return 0;
+  OrthArgs a;
+  a.n = n; a.V = V; a.m = m; a.t = t; a.W = W; a.part = ws->partial; a.out = ws->dsm;
+  a.rows = (n + nblk - 1) / nblk;
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel((const void*)k_orth, dim3((unsigned)nblk), dim3(kOrthThreads), args, smem, st);
+  if (e != cudaSuccess) {
+    helm_set_error("mpgmres_solve: k_orth: %s", cudaGetErrorString(e));
+    return -1;
+  }
+  g_helm_launches++;
+  return 1;
 }
 
 extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int t, const double* b_in,
@@ -378,7 +664,7 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
   wk.n = n;
   wk.st = st;
   wk.partial = ws->partial;
-  wk.hsmall = ws->hsmall;
+  wk.hsmall = pinned_small(ws->small_cap);   // re-fetched: the buffer is shared per thread
   wk.small_cap = ws->small_cap;
   cudaEvent_t ev[4];
   for (auto& e : ev) cudaEventCreate(&e);
@@ -426,7 +712,7 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
     if (k > ws->icap) {
       rc = ws_reserve(prob, t, std::min(maxit, 2 * ws->icap), mV, nz, st);
       if (rc != HELM_OK) break;
-      wk.partial = ws->partial; wk.hsmall = ws->hsmall; wk.small_cap = ws->small_cap;
+      wk.partial = ws->partial; wk.hsmall = pinned_small(ws->small_cap); wk.small_cap = ws->small_cap;
       d_gram = ws->dsm; d_cv = d_gram + t * t; d_nn = d_cv + 2 * t * t;
     }
     cplx* V = ws->V;
@@ -470,42 +756,54 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
     rc = helm_spmm_dev(prob, Zk, W, t, n, st);
     if (rc != HELM_OK) break;
     cudaEventRecord(ev[2], st);
-    // ---- a6: Gram of A Z_k (for ||A z_i||), BCGS2 against V_1..k
+    // ---- a6: Gram diagonal of A Z_k (for ||A z_i||), BCGS2 against V_1..k, intra-block CGS2
     const int m = (int)mV;
-    rc = dots(wk, W, n, t, W, n, t, d_gram, false);
-    if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, ws->dC1, false);
-    if (rc == HELM_OK) rc = update(wk, V, n, m, ws->dC1, W, n, t);
-    if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, ws->dC2, false);
-    if (rc == HELM_OK) rc = update(wk, V, n, m, ws->dC2, W, n, t);
-    if (rc != HELM_OK) break;
-    inner += 2L * m * t;
-    // intra-block CGS2 on the device: new column i is projected (twice) against
-    // slots V[:, m .. m+i); a dropped column leaves a zero slot, so later
-    // projections onto it vanish exactly as if it were skipped.
-    for (int i = 0; i < t && rc == HELM_OK; ++i) {
-      cplx* wi = W + (long)i * n;
-      for (int pass = 0; pass < 2 && i > 0; ++pass) {
-        cplx* cvi = d_cv + (long)pass * t * t + (long)i * t;
-        rc = dots(wk, V + mV * n, n, i, wi, n, 1, cvi, false);
-        if (rc == HELM_OK) rc = update(wk, V + mV * n, n, i, cvi, wi, n, 1);
+    std::vector<C> h1, h2, small;
+    std::vector<double> nrm(t);
+    int fused = orth_fused(ws, n, V, m, t, W, st);
+    if (fused < 0) { rc = HELM_ECUDA; break; }
+    if (fused) {
+      // one device->host copy: [C1][C2][gram][cv][nn]
+      cudaEventRecord(ev[3], st);
+      std::vector<C> all;
+      if ((rc = to_host(wk, ws->dsm, (size_t)(2 * m * t + 3 * t * t + t), all)) != HELM_OK) break;
+      h1.assign(all.begin(), all.begin() + (size_t)m * t);
+      h2.assign(all.begin() + (size_t)m * t, all.begin() + 2 * (size_t)m * t);
+      small.assign(all.begin() + 2 * (size_t)m * t, all.end());
+      for (int i = 0; i < t; ++i) nrm[i] = small[3 * t * t + i].real();
+    } else {
+      rc = dots(wk, W, n, t, W, n, t, d_gram, false);
+      if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, ws->dC1, false);
+      if (rc == HELM_OK) rc = update(wk, V, n, m, ws->dC1, W, n, t);
+      if (rc == HELM_OK) rc = dots(wk, V, n, m, W, n, t, ws->dC2, false);
+      if (rc == HELM_OK) rc = update(wk, V, n, m, ws->dC2, W, n, t);
+      if (rc != HELM_OK) break;
+      // intra-block CGS2 on the device: new column i is projected (twice) against
+      // slots V[:, m .. m+i); a dropped column leaves a zero slot, so later
+      // projections onto it vanish exactly as if it were skipped.
+      for (int i = 0; i < t && rc == HELM_OK; ++i) {
+        cplx* wi = W + (long)i * n;
+        for (int pass = 0; pass < 2 && i > 0; ++pass) {
+          cplx* cvi = d_cv + (long)pass * t * t + (long)i * t;
+          rc = dots(wk, V + mV * n, n, i, wi, n, 1, cvi, false);
+          if (rc == HELM_OK) rc = update(wk, V + mV * n, n, i, cvi, wi, n, 1);
+          if (rc != HELM_OK) break;
+        }
         if (rc != HELM_OK) break;
+        rc = dots(wk, wi, n, 1, wi, n, 1, d_nn + i, false);
+        if (rc != HELM_OK) break;
+        k_decide<<<1, 32, 0, st>>>(d_nn + i, d_gram, t, i, ws->dscal, d_nrm);
+        k_scale_dev<<<grid_for(n), 256, 0, st>>>(n, wi, ws->dscal, i, V + (mV + i) * n);
+        g_helm_launches += 2;
       }
       if (rc != HELM_OK) break;
-      rc = dots(wk, wi, n, 1, wi, n, 1, d_nn + i, false);
-      if (rc != HELM_OK) break;
-      k_decide<<<1, 32, 0, st>>>(d_nn + i, d_gram, t, i, ws->dscal, d_nrm);
-      k_scale_dev<<<grid_for(n), 256, 0, st>>>(n, wi, ws->dscal, i, V + (mV + i) * n);
-      g_helm_launches += 2;
+      cudaEventRecord(ev[3], st);
+      if ((rc = to_host(wk, ws->dC1, (size_t)m * t, h1)) != HELM_OK) break;
+      if ((rc = to_host(wk, ws->dC2, (size_t)m * t, h2)) != HELM_OK) break;
+      if ((rc = to_host(wk, d_gram, (size_t)(3 * t * t + t), small)) != HELM_OK) break;
+      HELM_CUDA_TRY(cudaMemcpyAsync(nrm.data(), d_nrm, sizeof(double) * t, cudaMemcpyDeviceToHost, st));
     }
-    if (rc != HELM_OK) break;
-    cudaEventRecord(ev[3], st);
-    // ---- one device->host copy per iteration: H block, intra-block coefficients, norms
-    std::vector<C> h1, h2, small;
-    if ((rc = to_host(wk, ws->dC1, (size_t)m * t, h1)) != HELM_OK) break;
-    if ((rc = to_host(wk, ws->dC2, (size_t)m * t, h2)) != HELM_OK) break;
-    if ((rc = to_host(wk, d_gram, (size_t)(3 * t * t + t), small)) != HELM_OK) break;
-    std::vector<double> nrm(t);
-    HELM_CUDA_TRY(cudaMemcpyAsync(nrm.data(), d_nrm, sizeof(double) * t, cudaMemcpyDeviceToHost, st));
+    inner += 2L * m * t;
     HELM_CUDA_TRY(cudaStreamSynchronize(st));
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[0], ev[1]); sweep_ms += ms;

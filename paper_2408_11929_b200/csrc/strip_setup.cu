@@ -17,12 +17,24 @@
 // stored as Rinv_k, G_k = Rinv_k R_{k,k-1}, F_k = Rinv_k R_{k,k+1}.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "dense.cuh"
 #include "p1_entries.cuh"
 
 static constexpr int kXinvMaxW = 36;   // explicit separator inverse for the register-streaming kernel
+
+// Factor sets are shared between handles that describe the same strips (LRL and
+// RLR, BTB and TBT, or different gathers): same problem, axis, N, overlap, P.
+struct SharedFactors {
+  int refs;
+  long prob_uid;
+  int axis, N, overlap, P;
+  cplx *dg, *al, *cr, *ne, *tc, *fac, *red, *xinv;
+  long factor_bytes;
+};
+static std::vector<SharedFactors*> g_shared;
 
 // ------------------------------------------------------------------ bands + corrections
 struct StripGeo {
@@ -154,6 +166,233 @@ __global__ void k_factor_segments(FacArgs fa) {
     cplx* t = cur; cur = nxt; nxt = t;
   }
   blk_copy(XLH, cur, w);
+}
+
+// ------------------------------------------------------------------ register-row factorisation (w <= 36)
+// Same recurrences as k_factor_segments, laid out for throughput: one CTA of
+// 96 threads per (segment, strip, kind).  Row i of the current block lives in
+// the registers of the thread pair (2i, 2i+1), thread half h holding columns
+// j = 2 jj + h.  The in-place Gauss-Jordan inversion uses implicit partial
+// pivoting (rows stay in their threads; the pivot row is broadcast through
+// shared memory, two barriers per pivot step; the permutation is undone when
+// the inverse is written back in natural order).
+//   kind 0: top-down Thomas S_c = D_c - U_{c-1}^T Sinv_{c-1} U_{c-1} (writes fac),
+//           then X[lo,hi] by Y_hi = Sinv_hi, Y_c = -Sinv_c U_c Y_{c+1}
+//   kind 1: bottom-up S'_c = D_c - U_c S'^{-1}_{c+1} U_c^T, X[lo,lo] = S'^{-1}_lo
+// Pivot choice (largest |a_ik| among the rows not yet used, ties to the lower
+// row) and the elementary operations are those of gj_invert.
+static constexpr int kRowW = 36;
+static constexpr int kRowHW = kRowW / 2;
+static constexpr int kRowThreads = 96;
+static constexpr int kRowWarps = kRowThreads / 32;
+
+struct RowSmem {
+  cplx mat[kRowW * kRowW];    // natural-order inverse of the current block / Y
+  cplx tmat[kRowW * kRowW];   // U_c Y (kind 0, X[lo,hi] chain)
+  cplx prow[kRowW];
+  double redv[kRowWarps];
+  int redi[kRowWarps];
+  int pivrow[kRowW];
+};
+
+// Invert the w x w block held as described above; leaves the inverse in
+// sm.mat (natural order, row stride kRowW).  Returns 1 (uniformly) on a zero pivot.
+__device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i = tid >> 1, h = tid & 1;
+  const bool active = i < w;
+  bool used = false;
+  int kstep = 0;
+#pragma unroll
+  for (int k = 0; k < kRowW; ++k) {
+    if (k >= w) break;
+    const int kh = k & 1, kj = k >> 1;
+    double best = (active && !used && h == kh) ? cabs2(a[kj]) : -1.0;
+    int bi = i;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { sm.redv[warp] = best; sm.redi[warp] = bi; }
+    __syncthreads();
+    double b0 = sm.redv[0];
+    int p = sm.redi[0];
+#pragma unroll
+    for (int q = 1; q < kRowWarps; ++q)
+      if (sm.redv[q] > b0) { b0 = sm.redv[q]; p = sm.redi[q]; }
+    if (!(b0 > 0.0)) return 1;
+    // pivot element to both halves of the pivot row; multiplier to both halves of the others
+    const cplx mine = a[kj];
+    cplx akk;
+    akk.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);
+    akk.y = __shfl_xor_sync(0xffffffffu, mine.y, 1);
+    if (h == kh) akk = mine;
+    if (i == p) {
+      const cplx dinv = cinv(akk);
+      if (h == kh) a[kj] = cmk(1.0, 0.0);
+#pragma unroll
+      for (int jj = 0; jj < kRowHW; ++jj) {
+        a[jj] = cmul(a[jj], dinv);
+        sm.prow[2 * jj + h] = a[jj];
+      }
+      used = true;
+      kstep = k;
+      if (h == 0) sm.pivrow[k] = p;
+    }
+    __syncthreads();
+    if (active && i != p) {
+      const cplx f = akk;
+      if (h == kh) a[kj] = cmk(0.0, 0.0);
+#pragma unroll
+      for (int jj = 0; jj < kRowHW; ++jj) {
+        const cplx r = sm.prow[2 * jj + h];
+        a[jj].x -= f.x * r.x - f.y * r.y;
+        a[jj].y -= f.x * r.y + f.y * r.x;
+      }
+    }
+  }
+  __syncthreads();   // pivrow complete; everyone is done reading mat from the previous block
+  if (active) {
+#pragma unroll
+    for (int jj = 0; jj < kRowHW; ++jj) {
+      const int j = 2 * jj + h;
+      if (j < w) sm.mat[kstep * kRowW + sm.pivrow[j]] = a[jj];
+    }
+  }
+  __syncthreads();
+  return 0;
+}
+
+// a = row i of D_c - (L X R) with X = sm.mat:
+//   td (kind 0): L = U_{c-1}^T, R = U_{c-1};  bu (kind 1): L = U_c, R = U_c^T
+__device__ __forceinline__ void row_schur(cplx (&a)[kRowHW], int w, const cplx* dg, const cplx* al, const cplx* cr,
+                                          const cplx* ne, bool has, bool td, const RowSmem& sm) {
+  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  const cplx zero = cmk(0, 0);
+  const cplx dgi = i < w ? __ldg(dg + i) : zero;
+  const cplx ali = i + 1 < w ? __ldg(al + i) : zero;
+  const cplx alm = (i >= 1 && i < w) ? __ldg(al + i - 1) : zero;
+#pragma unroll
+  for (int jj = 0; jj < kRowHW; ++jj) {
+    const int q = 2 * jj + h;
+    a[jj] = q == i ? dgi : (q == i + 1 ? ali : (q + 1 == i ? alm : zero));
+  }
+  if (!has || i >= w) return;
+  const cplx ci = __ldg(cr + i);
+  const cplx* x0 = sm.mat + i * kRowW;
+  if (td) {
+    // (L X)[i] = cr[i] X[i] + ne[i-1] X[i-1];  v_q = cr[q] y_q + ne[q-1] y_{q-1}
+    const cplx nm = i >= 1 ? __ldg(ne + i - 1) : zero;
+    const cplx* x1 = sm.mat + (i >= 1 ? i - 1 : 0) * kRowW;
+#pragma unroll
+    for (int jj = 0; jj < kRowHW; ++jj) {
+      const int q = 2 * jj + h;
+      if (q >= w) break;
+      cplx yq = cmul(ci, x0[q]);
+      if (i >= 1) cfma(yq, nm, x1[q]);
+      cplx v = cmul(__ldg(cr + q), yq);
+      if (q >= 1) {
+        cplx yp = cmul(ci, x0[q - 1]);
+        if (i >= 1) cfma(yp, nm, x1[q - 1]);
+        cfma(v, __ldg(ne + q - 1), yp);
+      }
+      a[jj] = csub(a[jj], v);
+    }
+  } else {
+    // (L X)[i] = cr[i] X[i] + ne[i] X[i+1];  v_q = cr[q] y_q + ne[q] y_{q+1}
+    const cplx ni = i + 1 < w ? __ldg(ne + i) : zero;
+    const cplx* x1 = sm.mat + (i + 1 < w ? i + 1 : i) * kRowW;
+#pragma unroll
+    for (int jj = 0; jj < kRowHW; ++jj) {
+      const int q = 2 * jj + h;
+      if (q >= w) break;
+      cplx yq = cmul(ci, x0[q]);
+      if (i + 1 < w) cfma(yq, ni, x1[q]);
+      cplx v = cmul(__ldg(cr + q), yq);
+      if (q + 1 < w) {
+        cplx yn = cmul(ci, x0[q + 1]);
+        if (i + 1 < w) cfma(yn, ni, x1[q + 1]);
+        cfma(v, __ldg(ne + q), yn);
+      }
+      a[jj] = csub(a[jj], v);
+    }
+  }
+}
+
+__device__ __forceinline__ void row_store(cplx* dst, int w, const RowSmem& sm) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int r = e / w;
+    dst[e] = sm.mat[r * kRowW + (e - r * w)];
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
+  __shared__ RowSmem sm;
+  const int s = blockIdx.y, pseg = blockIdx.x, kind = blockIdx.z;
+  if (kind == 1 && fa.P == 1) return;
+  const int w = fa.w[s];
+  const int lo = fa.seg_lo[pseg], hi = fa.seg_hi[pseg];
+  const long band = (long)s * fa.nc * fa.wmax;
+  cplx* fac = fa.fac + fa.fac_off[s];
+  const long w2 = (long)w * w;
+  cplx* scr = fa.scratch + ((long)s * fa.P + pseg) * fa.scratch_stride;
+  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  cplx a[kRowHW];
+  auto B = [&](const cplx* base, int c) { return base + band + (long)c * fa.wmax; };
+  if (kind == 0) {
+    for (int c = lo; c <= hi; ++c) {
+      row_schur(a, w, B(fa.dg, c), B(fa.al, c), B(fa.cr, c - 1), B(fa.ne, c - 1), c > lo, true, sm);
+      if (row_invert(a, w, sm)) {
+        if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
+        return;
+      }
+      row_store(fac + (long)c * w2, w, sm);
+    }
+    if (fa.P == 1) return;
+    // X[lo,hi]: Y_hi = Sinv_hi (in sm.mat); Y_c = -Sinv_c (U_c Y_{c+1})
+    for (int c = hi - 1; c >= lo; --c) {
+      const cplx* cr = B(fa.cr, c);
+      const cplx* ne = B(fa.ne, c);
+      if (i < w) {
+        const cplx ci = __ldg(cr + i);
+        const cplx ni = i + 1 < w ? __ldg(ne + i) : cmk(0, 0);
+        for (int q = h; q < w; q += 2) {
+          cplx v = cmul(ci, sm.mat[i * kRowW + q]);
+          if (i + 1 < w) cfma(v, ni, sm.mat[(i + 1) * kRowW + q]);
+          sm.tmat[i * kRowW + q] = v;
+        }
+      }
+      __syncthreads();
+      if (i < w) {
+        const cplx* srow = fac + (long)c * w2 + (long)i * w;
+        cplx acc[kRowHW];
+#pragma unroll
+        for (int jj = 0; jj < kRowHW; ++jj) acc[jj] = cmk(0, 0);
+        for (int r = 0; r < w; ++r) {
+          const cplx sv = srow[r];
+#pragma unroll
+          for (int jj = 0; jj < kRowHW; ++jj) cfma(acc[jj], sv, sm.tmat[r * kRowW + 2 * jj + h]);
+        }
+        // mat is not read in this phase: overwrite row i with Y_c directly
+#pragma unroll
+        for (int jj = 0; jj < kRowHW; ++jj)
+          if (2 * jj + h < w) sm.mat[i * kRowW + 2 * jj + h] = cscale(acc[jj], -1.0);
+      }
+      __syncthreads();
+    }
+    row_store(scr + 3 * w2, w, sm);
+  } else {
+    for (int c = hi; c >= lo; --c) {
+      row_schur(a, w, B(fa.dg, c), B(fa.al, c), B(fa.cr, c), B(fa.ne, c), c < hi, false, sm);
+      if (row_invert(a, w, sm)) {
+        if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
+        return;
+      }
+    }
+    row_store(scr + 2 * w2, w, sm);
+  }
 }
 
 // ------------------------------------------------------------------ separator system
@@ -376,8 +615,21 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h->factor_bytes = (fac_total + red_total) * (long)sizeof(cplx);
   cudaError_t e = cudaSuccess;
   auto alloc = [&](void** p, size_t bytes) {
-    if (e == cudaSuccess) e = cudaMalloc(p, bytes > 0 ? bytes : 16);
+    if (e == cudaSuccess) e = helm_dev_alloc(p, bytes);
   };
+  // explicit separator-inverse offsets (register-streaming kernel only)
+  const bool want_xinv = P > 1 && wmax <= kXinvMaxW;
+  long xinv_total = 0;
+  if (want_xinv) {
+    h->xinv_off.resize(n_strips);
+    for (int s2 = 0; s2 < n_strips; ++s2) {
+      h->xinv_off[s2] = xinv_total;
+      xinv_total += (long)(P - 1) * h->w[s2] * (long)(P - 1) * h->w[s2];
+    }
+  }
+  SharedFactors* sf = nullptr;
+  for (SharedFactors* c : g_shared)
+    if (c->prob_uid == prob->uid && c->axis == axis && c->N == n_strips && c->overlap == overlap && c->P == P) sf = c;
   h->d_a = h->d_w = h->d_own_lo = h->d_own_hi = h->d_seg_lo = h->d_seg_hi = nullptr;
   h->d_dg = h->d_al = h->d_cr = h->d_ne = h->d_tc = h->d_fac = h->d_red = nullptr;
   h->d_fac_off = h->d_red_off = nullptr;
@@ -391,13 +643,17 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   alloc((void**)&h->d_seg_hi, sizeof(int) * P);
   alloc((void**)&h->d_fac_off, sizeof(long) * n_strips);
   alloc((void**)&h->d_red_off, sizeof(long) * n_strips);
-  alloc((void**)&h->d_dg, sizeof(cplx) * bandN);
-  alloc((void**)&h->d_al, sizeof(cplx) * bandN);
-  alloc((void**)&h->d_cr, sizeof(cplx) * bandN);
-  alloc((void**)&h->d_ne, sizeof(cplx) * bandN);
-  alloc((void**)&h->d_tc, sizeof(cplx) * n_strips * 2 * nc * 5);
-  alloc((void**)&h->d_fac, sizeof(cplx) * fac_total);
-  alloc((void**)&h->d_red, sizeof(cplx) * std::max(red_total, 1L));
+  if (want_xinv) alloc((void**)&h->d_xinv_off, sizeof(long) * n_strips);
+  if (!sf) {
+    alloc((void**)&h->d_dg, sizeof(cplx) * bandN);
+    alloc((void**)&h->d_al, sizeof(cplx) * bandN);
+    alloc((void**)&h->d_cr, sizeof(cplx) * bandN);
+    alloc((void**)&h->d_ne, sizeof(cplx) * bandN);
+    alloc((void**)&h->d_tc, sizeof(cplx) * n_strips * 2 * nc * 5);
+    alloc((void**)&h->d_fac, sizeof(cplx) * fac_total);
+    alloc((void**)&h->d_red, sizeof(cplx) * std::max(red_total, 1L));
+    if (want_xinv) alloc((void**)&h->d_xinv, sizeof(cplx) * xinv_total);
+  }
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: cudaMalloc (%.2f GB factors): %s", h->factor_bytes / 1e9, cudaGetErrorString(e));
     sweep_destroy(h);
@@ -414,13 +670,36 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h2d(h->d_seg_hi, h->seg_hi.data(), sizeof(int) * P);
   h2d(h->d_fac_off, h->fac_off.data(), sizeof(long) * n_strips);
   h2d(h->d_red_off, h->red_off.data(), sizeof(long) * n_strips);
+  if (want_xinv) h2d(h->d_xinv_off, h->xinv_off.data(), sizeof(long) * n_strips);
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: copy geometry: %s", cudaGetErrorString(e));
     sweep_destroy(h);
     return HELM_ECUDA;
   }
+  if (sf) {
+    // same strips already factored: share the device factor set
+    h->d_dg = sf->dg; h->d_al = sf->al; h->d_cr = sf->cr; h->d_ne = sf->ne; h->d_tc = sf->tc;
+    h->d_fac = sf->fac; h->d_red = sf->red; h->d_xinv = sf->xinv;
+    h->factor_bytes = sf->factor_bytes;
+    h->shared = sf;
+    sf->refs++;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      helm_set_error("sweep_setup: %s", cudaGetErrorString(e));
+      sweep_destroy(h);
+      return HELM_ECUDA;
+    }
+    *out = h;
+    return HELM_OK;
+  }
   GridView g{prob->nx, prob->ny, prob->h, prob->omega, prob->c};
   StripGeo sg{h->d_a, h->d_w, n_strips, nc, wmax, axis};
+  const bool timing = getenv("HELM_SETUP_TIMING") != nullptr;
+  cudaEvent_t tev[6];
+  if (timing) {
+    for (auto& x : tev) cudaEventCreate(&x);
+    cudaEventRecord(tev[0], st);
+  }
   {
     dim3 grid((nc * wmax + 255) / 256, n_strips);
     k_strip_bands<<<grid, 256, 0, st>>>(g, sg, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc);
@@ -431,7 +710,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   cplx* scratch = nullptr;
   cplx* rscratch = nullptr;
   const long sstride = 4L * wmax * wmax;
-  if (e == cudaSuccess) e = cudaMalloc(&d_status, sizeof(int));
+  if (e == cudaSuccess) e = helm_dev_alloc((void**)&d_status, sizeof(int));
   if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, sizeof(int), st);
   if (P > 1) {
     alloc((void**)&scratch, sizeof(cplx) * sstride * n_strips * P);
@@ -439,7 +718,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   }
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: scratch: %s", cudaGetErrorString(e));
-    cudaFree(d_status); cudaFree(scratch); cudaFree(rscratch);
+    helm_dev_free(d_status); helm_dev_free(scratch); helm_dev_free(rscratch);
     sweep_destroy(h);
     return HELM_ENOMEM;
   }
@@ -449,31 +728,29 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   int threads = wmax * wmax >= 1024 ? 512 : 256;
   FacArgs fa{h->d_w, h->d_fac_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr, h->d_ne,
              nc, wmax, P, h->d_fac, scratch, sstride, d_status};
-  k_factor_segments<<<dim3(P, n_strips), threads, smem, st>>>(fa);
+  if (timing) cudaEventRecord(tev[1], st);
+  if (wmax <= kRowW && !getenv("HELM_FACTOR_GENERIC"))
+    k_factor_rows<<<dim3(P, n_strips, 2), kRowThreads, 0, st>>>(fa);
+  else
+    k_factor_segments<<<dim3(P, n_strips), threads, smem, st>>>(fa);
+  if (timing) cudaEventRecord(tev[2], st);
   g_helm_launches++;
   e = cudaGetLastError();
   if (e == cudaSuccess && P > 1) {
     RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
                h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
     k_reduced<<<n_strips, threads, smem, st>>>(ra);
+    if (timing) cudaEventRecord(tev[3], st);
     g_helm_launches++;
     e = cudaGetLastError();
-    if (e == cudaSuccess && wmax <= kXinvMaxW) {
+    if (e == cudaSuccess && want_xinv) {
       // explicit separator inverse rows for the register-streaming kernel
-      h->xinv_off.resize(n_strips);
-      long tot = 0;
-      for (int s2 = 0; s2 < n_strips; ++s2) {
-        h->xinv_off[s2] = tot;
-        tot += (long)(P - 1) * h->w[s2] * (long)(P - 1) * h->w[s2];
-      }
-      e = cudaMalloc(&h->d_xinv, sizeof(cplx) * tot);
-      if (e == cudaSuccess) e = cudaMalloc(&h->d_xinv_off, sizeof(long) * n_strips);
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(h->d_xinv_off, h->xinv_off.data(), sizeof(long) * n_strips, cudaMemcpyHostToDevice, st);
+      const long tot = xinv_total;
       if (e == cudaSuccess) {
         size_t sm3 = sizeof(cplx) * 3 * wmax * wmax;
         cudaFuncSetAttribute(k_reduced_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
         k_reduced_inverse<<<dim3(P - 1, n_strips), 256, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        if (timing) cudaEventRecord(tev[4], st);
         g_helm_launches++;
         e = cudaGetLastError();
         h->factor_bytes += tot * (long)sizeof(cplx);
@@ -483,9 +760,18 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   int status = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFree(d_status);
-  cudaFree(scratch);
-  cudaFree(rscratch);
+  if (timing && e == cudaSuccess) {
+    float t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    cudaEventElapsedTime(&t1, tev[0], tev[1]);
+    cudaEventElapsedTime(&t2, tev[1], tev[2]);
+    if (P > 1) cudaEventElapsedTime(&t3, tev[2], tev[3]);
+    if (P > 1 && want_xinv) cudaEventElapsedTime(&t4, tev[3], tev[4]);
+    fprintf(stderr, "[sweep_setup] bands %.2f ms, segment factors %.2f ms, separator factors %.2f ms, separator inverse %.2f ms\n",
+            t1, t2, t3, t4);
+  }
+  helm_dev_free(d_status);
+  helm_dev_free(scratch);
+  helm_dev_free(rscratch);
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: factorisation kernel: %s", cudaGetErrorString(e));
     sweep_destroy(h);
@@ -497,6 +783,10 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     sweep_destroy(h);
     return HELM_ESINGULAR;
   }
+  sf = new SharedFactors{1, prob->uid, axis, n_strips, overlap, P, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc,
+                         h->d_fac, h->d_red, h->d_xinv, h->factor_bytes};
+  g_shared.push_back(sf);
+  h->shared = sf;
   *out = h;
   return HELM_OK;
 }
@@ -529,10 +819,23 @@ extern "C" int sweep_info(helm_sweep_t h, long* info) {
 
 extern "C" void sweep_destroy(helm_sweep_t h) {
   if (!h) return;
-  cudaFree(h->d_a); cudaFree(h->d_w); cudaFree(h->d_own_lo); cudaFree(h->d_own_hi);
-  cudaFree(h->d_seg_lo); cudaFree(h->d_seg_hi); cudaFree(h->d_fac_off); cudaFree(h->d_red_off);
-  cudaFree(h->d_dg); cudaFree(h->d_al); cudaFree(h->d_cr); cudaFree(h->d_ne); cudaFree(h->d_tc);
-  cudaFree(h->d_fac); cudaFree(h->d_red);
-  cudaFree(h->d_xinv); cudaFree(h->d_xinv_off);
+  helm_dev_free(h->d_a); helm_dev_free(h->d_w); helm_dev_free(h->d_own_lo); helm_dev_free(h->d_own_hi);
+  helm_dev_free(h->d_seg_lo); helm_dev_free(h->d_seg_hi); helm_dev_free(h->d_fac_off);
+  helm_dev_free(h->d_red_off); helm_dev_free(h->d_xinv_off);
+  bool free_factors = true;
+  if (h->shared) {
+    SharedFactors* sf = h->shared;
+    if (--sf->refs > 0) {
+      free_factors = false;
+    } else {
+      for (size_t k = 0; k < g_shared.size(); ++k)
+        if (g_shared[k] == sf) { g_shared.erase(g_shared.begin() + k); break; }
+      delete sf;
+    }
+  }
+  if (free_factors) {
+    helm_dev_free(h->d_dg); helm_dev_free(h->d_al); helm_dev_free(h->d_cr); helm_dev_free(h->d_ne);
+    helm_dev_free(h->d_tc); helm_dev_free(h->d_fac); helm_dev_free(h->d_red); helm_dev_free(h->d_xinv);
+  }
   delete h;
 }

@@ -498,16 +498,24 @@ __global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant_
     const int ci = row_c - lo;   // local block row
     cplx base = cmk(0, 0);
     if (act && kind == 1) base = yseg[ci * w + row];
-    cplx a0 = cmk(0, 0), a1 = cmk(0, 0);
+    // 4 independent accumulator chains (dependent DFMA depth 3 x 2 instead of 5 x 2)
+    cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
+#ifndef HELM_ABL_NOFMA
 #pragma unroll
     for (int c = 0; c < KPL; ++c) {
       const int k = q + LPR * c;
       if (k < w) {
-        if (c & 1) cfma(a1, S[c], vin[k]);
-        else cfma(a0, S[c], vin[k]);
+        const cplx v = vin[k];
+        if ((c & 3) == 0) cfma(a0, S[c], v);
+        else if ((c & 3) == 1) cfma(a1, S[c], v);
+        else if ((c & 3) == 2) cfma(a2, S[c], v);
+        else cfma(a3, S[c], v);
       }
     }
-    cplx acc = cadd(a0, a1);
+#else
+    a0 = cadd(vin[q], S[0]);
+#endif
+    cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
@@ -524,8 +532,14 @@ __global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant_
       nb.y = __shfl_up_sync(0xffffffffu, o.y, 4);
     }
     // register loads for step j + D (independent of this step's data)
+#ifndef HELM_ABL_NOLDG
     issue(S);
+#endif
+#ifdef HELM_ABL_NOWRITER
+    if (false) {
+#else
     if (q == 0 && act && slot_owned(slot, high)) {
+#endif
       cplx* vn = vbuf + (cur ^ 1) * WM;
       if (kind == 0) {
         yseg[ci * w + row] = o;
