@@ -228,7 +228,7 @@ def run_ours(args):
         "spmm_ms_avg": round(spmv_ms / max(n_sweeps, 1), 4),
         "orth_ms_avg": round(orth_ms / max(n_sweeps, 1), 4),
         "true_rel_res": st["true_rel_res"],
-        "roofline": {"kernel": "k_sweep_fast (t=4 batched double sweeps, one cooperative launch per iteration)",
+        "roofline": {"kernel": hs.sweep_kernel_name() + " (t=4 batched double sweeps, one cooperative launch per iteration)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "model_bytes_per_launch": model_bytes,

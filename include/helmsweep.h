@@ -149,6 +149,12 @@ const char* helm_last_error(void);
 /* Number of this library's kernel launches since load (host counter). */
 long helm_kernel_launches(void);
 
+/* Name of the sweep kernel the last sweep_apply / mpgmres_solve iteration of
+ * this process launched ("k_sweep_dual", "k_sweep_warp", "k_sweep_fast",
+ * "k_sweep_apply"; "" before the first apply).  Diagnostics: the choice
+ * depends on the strip width, the segment count and HELM_SWEEP_KERNEL. */
+const char* helm_sweep_kernel_name(void);
+
 #ifdef __cplusplus
 }
 #endif

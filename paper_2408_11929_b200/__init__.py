@@ -29,7 +29,7 @@ DIRECTIONS = {"LRL": (0, 0, 1), "RLR": (0, 1, 1), "BTB": (1, 0, 1), "TBT": (1, 1
 
 EXPORTS = ["helm_assemble", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
            "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve", "helm_problem_destroy",
-           "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches"]
+           "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches", "helm_sweep_kernel_name"]
 
 
 class HelmError(RuntimeError):
@@ -85,6 +85,8 @@ def load():
     L.helm_last_error.restype = ctypes.c_char_p
     L.helm_kernel_launches.argtypes = []
     L.helm_kernel_launches.restype = l
+    L.helm_sweep_kernel_name.argtypes = []
+    L.helm_sweep_kernel_name.restype = ctypes.c_char_p
     for name in ["helm_assemble", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
                  "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve"]:
         getattr(L, name).restype = i
@@ -98,6 +100,11 @@ def last_error() -> str:
 
 def kernel_launches() -> int:
     return int(load().helm_kernel_launches())
+
+
+def sweep_kernel_name() -> str:
+    """Sweep kernel launched by the last apply (diagnostics)."""
+    return load().helm_sweep_kernel_name().decode()
 
 
 def _check(code, where):

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhelmsweep.so")
-SOURCES = ["assemble.cu", "strip_setup.cu", "sweep_apply.cu", "sweep_fast.cu", "krylov.cu"]
+SOURCES = ["assemble.cu", "strip_setup.cu", "sweep_apply.cu", "sweep_fast.cu", "sweep_dual.cu", "sweep_warp.cu", "krylov.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

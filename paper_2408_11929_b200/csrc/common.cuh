@@ -119,6 +119,13 @@ struct helm_sweep_s {
   // explicit rows of the separator inverse (w <= 36 only): per strip, separator k:
   // w x (K w) row-major at xinv_off[s] + k * w * K * w
   cplx* d_xinv = nullptr; std::vector<long> xinv_off; long* d_xinv_off = nullptr;
+  // two-chain kernel (sweep_dual.cu): the top-down inverses Sinv_c (d_facp) and the
+  // bottom-up inverses S'^{-1}_c (d_fac2) of every segment row, complex symmetric,
+  // stored as packed upper triangles (row r holds columns r..w-1), w(w+1)/2 per
+  // row, at pfac_off[s] + c * w(w+1)/2
+  cplx* d_facp = nullptr;
+  cplx* d_fac2 = nullptr;
+  std::vector<long> pfac_off; long* d_pfac_off = nullptr;
   // the band/factor arrays above are shared by every handle with the same
   // (problem, axis, N, overlap, P) -- e.g. LRL and RLR -- through this record
   struct SharedFactors* shared = nullptr;

@@ -31,7 +31,7 @@ struct SharedFactors {
   int refs;
   long prob_uid;
   int axis, N, overlap, P;
-  cplx *dg, *al, *cr, *ne, *tc, *fac, *red, *xinv;
+  cplx *dg, *al, *cr, *ne, *tc, *fac, *red, *xinv, *fac2, *facp;
   long factor_bytes;
 };
 static std::vector<SharedFactors*> g_shared;
@@ -98,6 +98,9 @@ struct FacArgs {
   cplx* scratch;   // per (s,p): 4 w^2: ping, pong, XLL, XLH
   long scratch_stride;
   int* status;     // first failure: (s*nc + c) + 1
+  cplx* fac2;      // packed bottom-up inverses S'^{-1}_c, NULL = not kept
+  cplx* facp;      // packed top-down inverses Sinv_c, NULL = not kept
+  const long* pfac_off;
 };
 
 __device__ inline void build_D(cplx* S, const cplx* dg, const cplx* al, int w) {
@@ -328,6 +331,16 @@ __device__ __forceinline__ void row_store(cplx* dst, int w, const RowSmem& sm) {
   }
 }
 
+// packed upper triangle of the (symmetrised) block in sm.mat: row r holds columns r..w-1
+__device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem& sm) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int r = e / w, q = e - r * w;
+    if (q < r) continue;
+    const cplx a = sm.mat[r * kRowW + q], b = sm.mat[q * kRowW + r];
+    dst[(long)r * w - (long)r * (r - 1) / 2 + (q - r)] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+  }
+}
+
 __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
   __shared__ RowSmem sm;
   const int s = blockIdx.y, pseg = blockIdx.x, kind = blockIdx.z;
@@ -349,6 +362,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
         return;
       }
       row_store(fac + (long)c * w2, w, sm);
+      if (fa.facp) row_store_packed(fa.facp + fa.pfac_off[s] + (long)c * (w2 + w) / 2, w, sm);
     }
     if (fa.P == 1) return;
     // X[lo,hi]: Y_hi = Sinv_hi (in sm.mat); Y_c = -Sinv_c (U_c Y_{c+1})
@@ -390,6 +404,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
         if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
         return;
       }
+      if (fa.fac2) row_store_packed(fa.fac2 + fa.pfac_off[s] + (long)c * (w2 + w) / 2, w, sm);
     }
     row_store(scr + 2 * w2, w, sm);
   }
@@ -619,6 +634,15 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   };
   // explicit separator-inverse offsets (register-streaming kernel only)
   const bool want_xinv = P > 1 && wmax <= kXinvMaxW;
+  // bottom-up inverses for the two-chain kernel (sweep_dual.cu): row factorisation only
+  const bool want_fac2 = want_xinv && wmax <= kRowW && !getenv("HELM_FACTOR_GENERIC");
+  long pfac_total = 0;
+  h->pfac_off.resize(n_strips);
+  for (int s2 = 0; s2 < n_strips; ++s2) {
+    h->pfac_off[s2] = pfac_total;
+    pfac_total += (long)nc * h->w[s2] * (h->w[s2] + 1) / 2;
+  }
+  if (want_fac2) h->factor_bytes += 2 * pfac_total * (long)sizeof(cplx);
   long xinv_total = 0;
   if (want_xinv) {
     h->xinv_off.resize(n_strips);
@@ -635,6 +659,9 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h->d_fac_off = h->d_red_off = nullptr;
   h->d_xinv = nullptr;
   h->d_xinv_off = nullptr;
+  h->d_fac2 = nullptr;
+  h->d_facp = nullptr;
+  h->d_pfac_off = nullptr;
   alloc((void**)&h->d_a, sizeof(int) * n_strips);
   alloc((void**)&h->d_w, sizeof(int) * n_strips);
   alloc((void**)&h->d_own_lo, sizeof(int) * n_strips);
@@ -642,6 +669,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   alloc((void**)&h->d_seg_lo, sizeof(int) * P);
   alloc((void**)&h->d_seg_hi, sizeof(int) * P);
   alloc((void**)&h->d_fac_off, sizeof(long) * n_strips);
+  alloc((void**)&h->d_pfac_off, sizeof(long) * n_strips);
   alloc((void**)&h->d_red_off, sizeof(long) * n_strips);
   if (want_xinv) alloc((void**)&h->d_xinv_off, sizeof(long) * n_strips);
   if (!sf) {
@@ -653,6 +681,8 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     alloc((void**)&h->d_fac, sizeof(cplx) * fac_total);
     alloc((void**)&h->d_red, sizeof(cplx) * std::max(red_total, 1L));
     if (want_xinv) alloc((void**)&h->d_xinv, sizeof(cplx) * xinv_total);
+    if (want_fac2) alloc((void**)&h->d_fac2, sizeof(cplx) * pfac_total);
+    if (want_fac2) alloc((void**)&h->d_facp, sizeof(cplx) * pfac_total);
   }
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: cudaMalloc (%.2f GB factors): %s", h->factor_bytes / 1e9, cudaGetErrorString(e));
@@ -669,6 +699,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h2d(h->d_seg_lo, h->seg_lo.data(), sizeof(int) * P);
   h2d(h->d_seg_hi, h->seg_hi.data(), sizeof(int) * P);
   h2d(h->d_fac_off, h->fac_off.data(), sizeof(long) * n_strips);
+  h2d(h->d_pfac_off, h->pfac_off.data(), sizeof(long) * n_strips);
   h2d(h->d_red_off, h->red_off.data(), sizeof(long) * n_strips);
   if (want_xinv) h2d(h->d_xinv_off, h->xinv_off.data(), sizeof(long) * n_strips);
   if (e != cudaSuccess) {
@@ -679,7 +710,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   if (sf) {
     // same strips already factored: share the device factor set
     h->d_dg = sf->dg; h->d_al = sf->al; h->d_cr = sf->cr; h->d_ne = sf->ne; h->d_tc = sf->tc;
-    h->d_fac = sf->fac; h->d_red = sf->red; h->d_xinv = sf->xinv;
+    h->d_fac = sf->fac; h->d_red = sf->red; h->d_xinv = sf->xinv; h->d_fac2 = sf->fac2; h->d_facp = sf->facp;
     h->factor_bytes = sf->factor_bytes;
     h->shared = sf;
     sf->refs++;
@@ -727,7 +758,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int threads = wmax * wmax >= 1024 ? 512 : 256;
   FacArgs fa{h->d_w, h->d_fac_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr, h->d_ne,
-             nc, wmax, P, h->d_fac, scratch, sstride, d_status};
+             nc, wmax, P, h->d_fac, scratch, sstride, d_status, h->d_fac2, h->d_facp, h->d_pfac_off};
   if (timing) cudaEventRecord(tev[1], st);
   if (wmax <= kRowW && !getenv("HELM_FACTOR_GENERIC"))
     k_factor_rows<<<dim3(P, n_strips, 2), kRowThreads, 0, st>>>(fa);
@@ -784,7 +815,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     return HELM_ESINGULAR;
   }
   sf = new SharedFactors{1, prob->uid, axis, n_strips, overlap, P, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc,
-                         h->d_fac, h->d_red, h->d_xinv, h->factor_bytes};
+                         h->d_fac, h->d_red, h->d_xinv, h->d_fac2, h->d_facp, h->factor_bytes};
   g_shared.push_back(sf);
   h->shared = sf;
   *out = h;
@@ -821,6 +852,7 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
   if (!h) return;
   helm_dev_free(h->d_a); helm_dev_free(h->d_w); helm_dev_free(h->d_own_lo); helm_dev_free(h->d_own_hi);
   helm_dev_free(h->d_seg_lo); helm_dev_free(h->d_seg_hi); helm_dev_free(h->d_fac_off);
+  helm_dev_free(h->d_pfac_off);
   helm_dev_free(h->d_red_off); helm_dev_free(h->d_xinv_off);
   bool free_factors = true;
   if (h->shared) {
@@ -836,6 +868,7 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
   if (free_factors) {
     helm_dev_free(h->d_dg); helm_dev_free(h->d_al); helm_dev_free(h->d_cr); helm_dev_free(h->d_ne);
     helm_dev_free(h->d_tc); helm_dev_free(h->d_fac); helm_dev_free(h->d_red); helm_dev_free(h->d_xinv);
+    helm_dev_free(h->d_fac2); helm_dev_free(h->d_facp);
   }
   delete h;
 }

@@ -612,7 +612,10 @@ long long* helm_sweep_prof_buffer() { return g_sweep_prof; }
 
 int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                      cudaStream_t st);
-static int g_force_general = -1;   // HELM_SWEEP_KERNEL=general forces the TMA-ring kernel (diagnostics)
+int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
+                     cudaStream_t st);
+int sweep_apply_warp(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
+                     cudaStream_t st);
 
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                     cudaStream_t st);
@@ -649,17 +652,40 @@ extern "C" int sweep_apply(const helm_sweep_t* dirs, int t, const double* Rin, l
   return helm_stage_out(sZ, st);
 }
 
+static const char* g_sweep_kernel = "";
+extern "C" const char* helm_sweep_kernel_name(void) { return g_sweep_kernel; }
+
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                     cudaStream_t st) {
   const helm_problem_s* prob = dirs[0]->prob;
-  if (g_force_general < 0) {
-    const char* ev = getenv("HELM_SWEEP_KERNEL");
-    g_force_general = (ev && strcmp(ev, "general") == 0) ? 1 : 0;
+  // kernel choice: the two-chain block kernel (sweep_dual.cu) where it applies
+  // (w <= 36, P > 1), else the single-chain register-streaming kernel
+  // (sweep_fast.cu, w <= 36), else the general TMA-ring kernel.
+  // HELM_SWEEP_KERNEL=fast|general starts lower, =warp selects the experimental
+  // warp-chain kernel (sweep_warp.cu) first (diagnostics, parity tests of every
+  // kernel); read per call.
+  const char* ev = getenv("HELM_SWEEP_KERNEL");
+  const int level = !ev ? 1
+                        : strcmp(ev, "general") == 0 ? 3
+                        : strcmp(ev, "fast") == 0    ? 2
+                        : strcmp(ev, "warp") == 0    ? 0
+                                                     : 1;
+  if (level == 0) {
+    g_sweep_kernel = "k_sweep_warp";
+    int rc = sweep_apply_warp(dirs, t, Rdev, ldr, Zdev, ldz, st);
+    if (rc != -1) return rc;
   }
-  if (!g_force_general) {
+  if (level <= 1) {
+    g_sweep_kernel = "k_sweep_dual";
+    int rc = sweep_apply_dual(dirs, t, Rdev, ldr, Zdev, ldz, st);
+    if (rc != -1) return rc;
+  }
+  if (level <= 2) {
+    g_sweep_kernel = "k_sweep_fast";
     int rc = sweep_apply_fast(dirs, t, Rdev, ldr, Zdev, ldz, st);
     if (rc != -1) return rc;
   }
+  g_sweep_kernel = "k_sweep_apply";
   // launch geometry: 8 consumer lanes per block row (<= 36 rows per tile) + 1 TMA producer warp
   int wmax = 0, pmax = 1;
   for (int d = 0; d < t; ++d) {

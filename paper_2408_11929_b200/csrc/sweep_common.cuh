@@ -12,6 +12,9 @@ struct DirArgs {
   const cplx *cr, *ne;   // bands: U_c couplings, stride wmax per row, nc*wmax per strip
   const cplx* tc;        // transmission stencils [s][side][c][5]
   const cplx* fac;
+  const cplx* facp;      // two-chain kernel: packed top-down inverses, NULL if absent
+  const cplx* fac2;      // two-chain kernel: packed bottom-up inverses, NULL if absent
+  const long* pfac_off;  // per-strip offsets of the packed arrays
   const long* fac_off;
   const cplx* red;
   const long* red_off;

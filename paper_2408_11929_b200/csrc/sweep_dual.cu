@@ -1,0 +1,707 @@
+// sweep_dual.cu -- hot-path row a4 for block rows of <= 36 nodes and P > 1
+// segments: the batched, partitioned double sweep with TWO independent
+// recurrence chains per segment, so that the dependent path of one local solve
+// is ~2m block steps instead of the 4m - 2 of sweep_fast.cu.
+//
+// Segment [lo, hi] (m rows) of strip s, separators x_{p-1} (row lo-1) and
+// x_p (row hi+1).  With top-down inverses Sinv_c (fac) and bottom-up inverses
+// S'^{-1}_c (fac2, strip_setup.cu k_factor_rows kind 1):
+//   phase 1 (independent, concurrent):
+//     chain A  y_c  = Sinv_c (b_c - U_{c-1}^T y_{c-1}),      c = lo..hi   (y_hi = x0_hi)
+//     chain B  z_c  = S'^{-1}_c (b_c - U_c z_{c+1}),          c = hi..lo   (z_lo = x0_lo)
+//   separator stage (as sweep_fast.cu): g from x0_lo / x0_hi of all segments,
+//     x_p = X_p g (explicit separator-inverse rows), neighbour exchange for x_{p-1}
+//   phase 3 (independent, concurrent):
+//     chain A  xa_c = y_c - Sinv_c U_c xa_{c+1},  xa_{hi+1} = x_p   c = hi..lo
+//     chain B  f_c  = -S'^{-1}_c U_{c-1}^T f_{c-1}, f_{lo-1} = x_{p-1}  c = lo..hi
+//   x_c = xa_c + f_c.
+// Chain A phase 3 is the back substitution of the top-down Thomas factorisation
+// with b_hi replaced by b_hi - U_hi x_p; chain B phase 3 adds the response
+// T^{-1}[:, lo] (-U_{lo-1}^T x_{p-1}) through the first block column of the
+// segment inverse, X[c][lo] = -S'^{-1}_c U_{c-1}^T X[c-1][lo].
+// Both phases read Sinv and S'^{-1} once per row: 4 w^2 per row per solve, the
+// same factor bytes as sweep_fast.cu, with half the dependent steps.
+//
+// Warps [0, nw) run chain A, [nw, 2 nw) chain B (named barriers 1 and 2);
+// whole-consumer stages use barrier 3; one helper warp keeps the factor blocks
+// of the next PF steps warm in L2.  The block-step data path (4 lanes per
+// block row, 7 owned + 1 halo row per warp, factor blocks streamed
+// L2 -> registers D steps ahead) is that of sweep_fast.cu.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "sweep_common.cuh"
+
+namespace dualk {
+constexpr int LPR = 4;    // lanes per block row
+constexpr int OWN = 7;    // owned rows per warp (8 slots, 1 halo)
+constexpr int KPL = 9;    // complex entries per lane per block row (w <= 36)
+constexpr int D = 2;      // register prefetch depth (block steps)
+constexpr int WM = 40;    // vector stride
+constexpr int PF = 12;    // L2 prefetch distance (block steps)
+constexpr int MAXT = 5 * 64;   // 2 groups of <= 5 warps (w <= 35)
+}  // namespace dualk
+
+struct DualArgs {
+  DirArgs d[HELM_MAXDIR];
+  int t;
+  int nw;           // consumer warps per chain group
+  int vec_elems;    // cplx per vector area
+  int nsolve_max;
+  int pmax;
+  long long* prof;  // optional per-CTA counters (8 per CTA)
+};
+
+struct DualTab {
+  const cplx* fac;
+  const cplx* fac2;
+  const cplx* xinv;
+  int w, a, s, pad;
+};
+
+__device__ __forceinline__ int dslot_row(int wi, int slot, int high) {
+  return high ? dualk::OWN * wi + slot : dualk::OWN * wi + slot - 1;
+}
+__device__ __forceinline__ bool dslot_owned(int slot, int high) { return high ? slot < 7 : slot >= 1; }
+
+// L2 residency: factor blocks read in phase 1 are re-read in phase 3 of the
+// same solve after ~2m block steps and the separator stage (~300 MB of other
+// traffic for C5 t = 4, more than L2), so phase-1 loads carry evict_last and
+// phase-3 / separator-inverse loads evict_first.
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ cplx ld_nc_hint(const cplx* a, uint64_t pol) {
+  cplx v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ cplx ld_cg_hint(const cplx* a, uint64_t pol) {
+  cplx v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(a), "l"(pol));
+  return v;
+}
+
+// entries S[row][q + 4c] of a complex-symmetric block stored as a packed upper
+// triangle (row i at i w - i (i-1) / 2): k >= row from row `row`, k < row from
+// row k (column `row`); the 8 row slots of a warp read consecutive addresses in
+// the lower part, so both halves stay coalesced per 4-lane group / per column
+__device__ __forceinline__ void dload_block(cplx (&dst)[dualk::KPL], const cplx* B, int w, int row, int q,
+                                            uint64_t pol) {
+  const bool ok = row >= 0 && row < w;
+  const int rs = row * w - (row * (row - 1)) / 2;
+#pragma unroll
+  for (int c = 0; c < dualk::KPL; ++c) {
+    const int k = q + dualk::LPR * c;
+    int idx;
+    if (k >= row) idx = rs + (k - row);
+    else idx = k * w - (k * (k - 1)) / 2 + (row - k);
+    dst[c] = (ok && k < w) ? ld_nc_hint(B + idx, pol) : cmk(0, 0);
+  }
+}
+
+__device__ __forceinline__ void dprefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+// block row and halo mapping of step e (0 <= e < 2m) of chain g
+__device__ __forceinline__ void chain_row(int g, int e, int m, int lo, int hi, int& row, int& high, int& js,
+                                          int& ph) {
+  ph = e >= m ? 1 : 0;
+  js = e - ph * m;
+  const bool up = (g == 0) == (ph == 0);   // A1, B3 walk lo -> hi
+  row = up ? lo + js : hi - js;
+  high = up ? 0 : 1;                       // lo -> hi steps need o[r-1]: low mapping
+}
+
+__global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_constant__ DualArgs A) {
+  using namespace dualk;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int gsz = A.nw * 32;
+  const int ncons = 2 * gsz;
+  int d = 0;
+  while (d + 1 < A.t && (int)blockIdx.x >= A.d[d + 1].cta_base) ++d;
+  const DirArgs& D_ = A.d[d];
+  const int p = blockIdx.x - D_.cta_base;
+  const int P = D_.P, K = P - 1;
+
+  cplx* vbuf = reinterpret_cast<cplx*>(smem_raw);   // [group][2][WM]
+  cplx* xlo = vbuf + 4 * WM;                        // x_{p-1}
+  cplx* xhi = xlo + WM;                             // x_p
+  cplx* zlo = xhi + WM;                             // x0_lo (chain B phase 1)
+  cplx* cpv = zlo + WM;                             // [pmax] prev-side separator corrections
+  cplx* cnv = cpv + A.pmax;                         // [pmax] next-side separator corrections
+  DualTab* tab = reinterpret_cast<DualTab*>(cnv + A.pmax);
+  volatile int* prog = reinterpret_cast<volatile int*>(tab + A.nsolve_max);
+  cplx* vec0 = reinterpret_cast<cplx*>(smem_raw + ((((char*)(prog + 4) - (char*)smem_raw) + 127) / 128) * 128);
+  cplx* bseg = vec0;                                // RHS rows lo..hi
+  cplx* yseg = bseg + A.vec_elems;                  // chain A phase 1 (y)
+  cplx* xa = yseg + A.vec_elems;                    // chain A phase 3
+  cplx* fb = xa + A.vec_elems;                      // chain B phase 3
+  cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi
+  cplx* bne = bcr + A.vec_elems;
+  cplx* xsg = bne + A.vec_elems;                    // final rows x = xa + fb
+  cplx* gsm = xsg + A.vec_elems;                    // separator RHS g (K x w)
+
+  const int nsolve = n_solves(D_);
+  for (int i = tid; i < nsolve; i += blockDim.x) {
+    const int s = sigma(D_, step_of(D_, i));
+    tab[i].fac = D_.facp + D_.pfac_off[s];
+    tab[i].fac2 = D_.fac2 + D_.pfac_off[s];
+    tab[i].xinv = D_.xinv + D_.xinv_off[s];
+    tab[i].w = D_.w[s];
+    tab[i].a = D_.a[s];
+    tab[i].s = s;
+  }
+  if (tid == 0) *prog = 0;
+  const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
+  const int m = hi - lo + 1;
+  const int sps = 2 * m;                 // steps per solve per chain
+  const int total = nsolve * sps;
+  __syncthreads();
+
+
+  const int g = tid >= gsz ? 1 : 0;       // chain group
+  const int gtid = tid - g * gsz;
+  const int wi = gtid >> 5, lane = tid & 31;
+  const int slot = lane >> 2, q = lane & 3;
+  const long band_stride = (long)D_.nc * D_.wmax;
+  long long xwait = 0, t_sep = 0, t_pre = 0;
+  const long long t_start = clock64();
+  auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
+  auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory"); };
+  const long exs = 2L * P * D_.wmax;   // parity stride of yb / xb
+  const long xss = (long)P * D_.wmax;  // parity stride of xs
+  cplx* myv = vbuf + g * 2 * WM;
+  const uint64_t pol_last = l2_policy_last(), pol_first = l2_policy_first();
+
+  int cur = 0;
+
+  // ------------------------------------------------------------ per-solve actions (all consumers)
+  // epilogue of solve i: x = xa + fb, gather into Z, publish boundary rows, next correction
+  auto seg_epilogue = [&](int i) {
+    const int st = step_of(D_, i);
+    const bool bwd = is_bwd(D_, i);
+    const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
+    const int par = i & 1;
+    for (int e = tid; e < m * w; e += ncons) xsg[e] = cadd(xa[e], fb[e]);
+    cbar();
+    if (writes_Z(D_, i)) {
+      const int olo = D_.own_lo[s], ohi = D_.own_hi[s], ow = ohi - olo + 1;
+      for (int e = tid; e < m * ow; e += ncons) {
+        int cl = e / ow, qq = olo + e % ow;
+        D_.Z[node_of(D_, a, lo + cl, qq)] = xsg[cl * w + qq];
+      }
+      if (p < P - 1)
+        for (int e = tid; e < ow; e += ncons) D_.Z[node_of(D_, a, hi + 1, olo + e)] = xhi[olo + e];
+    }
+    cplx* xb = D_.xb + par * exs + (long)p * 2 * D_.wmax;
+    for (int e = tid; e < w; e += ncons) {
+      xb[e] = xsg[e];
+      xb[D_.wmax + e] = xsg[(m - 1) * w + e];
+    }
+    int tdst = -1, side = 0;
+    cplx* target = nullptr;
+    if (!bwd) {
+      if (st < D_.N - 1) { tdst = sigma(D_, st + 1); side = prev_side(D_); target = D_.corr_prev + (long)(st + 1) * D_.nc; }
+      else if (D_.is_double && D_.N > 1) { tdst = sigma(D_, D_.N - 2); side = next_side(D_); target = D_.corr_next; }
+    } else if (st >= 1) {
+      tdst = sigma(D_, st - 1); side = next_side(D_); target = D_.corr_next;
+    }
+    if (tdst >= 0) {
+      auto X = [&](int cc, int qq) -> cplx {
+        if (cc < lo) return xlo[qq];
+        if (cc > hi) return xhi[qq];
+        return xsg[(cc - lo) * w + qq];
+      };
+      for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction(D_, tdst, side, c, a, X);
+    }
+  };
+  // RHS of solve i (rows lo..hi) and the couplings of rows lo-1..hi
+  auto seg_rhs = [&](int i) {
+    const int st = step_of(D_, i);
+    const bool bwd = is_bwd(D_, i);
+    const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
+    const int qp = prev_side(D_) == 0 ? 0 : w - 1;
+    const int qn = next_side(D_) == 0 ? 0 : w - 1;
+    const cplx* cband = D_.cr + s * band_stride;
+    const cplx* nband = D_.ne + s * band_stride;
+    for (int e = tid; e < m * w; e += ncons) {
+      int cl = e / w, qq = e % w, c = lo + cl;
+      cplx v = __ldg(D_.R + node_of(D_, a, c, qq));
+      if (st > 0 && qq == qp) v = cadd(v, D_.corr_prev[(long)st * D_.nc + c]);
+      if (bwd && qq == qn) v = cadd(v, D_.corr_next[c]);
+      bseg[cl * w + qq] = v;
+    }
+    for (int e = tid; e < (m + 1) * w; e += ncons) {
+      int cl = e / w, qq = e % w, c = lo - 1 + cl;
+      bcr[e] = c >= 0 ? __ldg(cband + (long)c * D_.wmax + qq) : cmk(0, 0);
+      bne[e] = c >= 0 ? __ldg(nband + (long)c * D_.wmax + qq) : cmk(0, 0);
+    }
+  };
+  // separator stage of solve i (after phase 1): all-gather of x0_lo / x0_hi, g,
+  // x_p = X_p g, neighbour exchange, phase-3 chain inputs
+  auto seg_separators = [&](int i) {
+    const int st = step_of(D_, i);
+    const bool bwd = is_bwd(D_, i);
+    const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
+    const int par = i & 1, ppar = par ^ 1;
+    const int qp = prev_side(D_) == 0 ? 0 : w - 1;
+    const int qn = next_side(D_) == 0 ? 0 : w - 1;
+    const cplx* cband = D_.cr + s * band_stride;
+    const cplx* nband = D_.ne + s * band_stride;
+    const long Kw = (long)K * w;
+    if (p < P - 1 && tid < 32) {
+      // stream this CTA's rows of the separator inverse (w x Kw, contiguous) into L2
+      // while the all-gather completes; the mat-vec below then reads L2
+      const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * Kw);
+      const long bytes = (long)w * Kw * (long)sizeof(cplx);
+      for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
+        dprefetch_l2(xp + o, (uint32_t)(bytes - o < 32768L ? bytes - o : 32768L), pol_first);
+    }
+    cplx* yb = D_.yb + par * exs + (long)p * 2 * D_.wmax;
+    for (int e = tid; e < w; e += ncons) {
+      yb[e] = zlo[e];
+      yb[D_.wmax + e] = yseg[(m - 1) * w + e];
+    }
+    cbar();
+    const long long cw0 = clock64();
+    if (tid == 0) {
+      __threadfence();
+      red_release_add(&D_.cnt[0], 1u);
+      while (ld_relaxed(&D_.cnt[0]) < (unsigned)(P * (i + 1))) __nanosleep(20);
+      (void)ld_acquire(&D_.cnt[0]);
+    }
+    cbar();
+    xwait += clock64() - cw0;
+    // separator-row transmission corrections (from solve i-1) for every separator
+    if (st > 0 || bwd) {
+      const int aprev = i > 0 ? tab[i - 1].a : 0;
+      for (int k = tid; k < K; k += ncons) {
+        const int sk = D_.seg_hi[k] + 1;
+        auto X = [&](int cc, int qq) -> cplx {
+          if (cc == sk) return ldcg(D_.xs + ppar * xss + (long)k * D_.wmax + qq);
+          if (cc == sk - 1) return ldcg(D_.xb + ppar * exs + (long)k * 2 * D_.wmax + D_.wmax + qq);
+          return ldcg(D_.xb + ppar * exs + (long)(k + 1) * 2 * D_.wmax + qq);
+        };
+        cplx cp = cmk(0, 0), cn = cmk(0, 0);
+        if (st > 0) {
+          if (!bwd) {
+            cp = correction(D_, s, prev_side(D_), sk, aprev, X);
+            if (k == p) D_.corr_prev[(long)st * D_.nc + sk] = cp;   // kept for the backward pass
+          } else {
+            cp = ldcg(D_.corr_prev + (long)st * D_.nc + sk);
+          }
+        }
+        if (bwd) cn = correction(D_, s, next_side(D_), sk, aprev, X);
+        cpv[k] = cp;
+        cnv[k] = cn;
+      }
+      cbar();
+    }
+    // g_k = b_{s_k} - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]  (all K separators)
+    const cplx* ybp = D_.yb + par * exs;
+    for (int e = tid; e < K * w; e += ncons) {
+      const int k = e / w, qq = e % w;
+      const int hk = D_.seg_hi[k], sk = hk + 1;
+      cplx v = __ldg(D_.R + node_of(D_, a, sk, qq));
+      if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
+      if (bwd && qq == qn) v = cadd(v, cnv[k]);
+      const cplx* yh = ybp + (long)k * 2 * D_.wmax + D_.wmax;
+      const cplx* yl = ybp + (long)(k + 1) * 2 * D_.wmax;
+      cplx tt = cmul(__ldg(cband + (long)hk * D_.wmax + qq), ldcg(yh + qq));
+      if (qq >= 1) cfma(tt, __ldg(nband + (long)hk * D_.wmax + qq - 1), ldcg(yh + qq - 1));
+      cfma(tt, __ldg(cband + (long)sk * D_.wmax + qq), ldcg(yl + qq));
+      if (qq + 1 < w) cfma(tt, __ldg(nband + (long)sk * D_.wmax + qq), ldcg(yl + qq + 1));
+      gsm[k * w + qq] = csub(v, tt);
+    }
+    cbar();
+    // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
+    const int cw = tid >> 5, ncw = ncons >> 5;
+    if (p < P - 1) {
+      for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
+        const cplx* Xr[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ok[u] = rb + u < w;
+          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * Kw;
+        }
+        cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+        for (long jj = lane; jj < Kw; jj += 128) {
+          cplx xv[4][4], gv[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const bool in = jj + 32 * v < Kw;
+            gv[v] = in ? gsm[jj + 32 * v] : cmk(0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ld_cg_hint(Xr[u] + jj + 32 * v, pol_first) : cmk(0, 0);
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
+            acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+          }
+          if (lane == 0 && ok[u]) xhi[rb + u] = acc[u];
+        }
+      }
+    }
+    for (int e = tid; e < WM; e += ncons) {
+      if (p == 0) xlo[e] = cmk(0, 0);
+      if (p == P - 1) xhi[e] = cmk(0, 0);
+    }
+    cbar();
+    // publish x_p (parity buffer; also the next solve's correction source),
+    // then take x_{p-1} from the left neighbour
+    if (p < P - 1) {
+      for (int e = tid; e < w; e += ncons) D_.xs[par * xss + (long)p * D_.wmax + e] = xhi[e];
+      cbar();
+      if (tid == 0) {
+        __threadfence();
+        st_release(&D_.flag[p], (unsigned)(i + 1));
+      }
+    }
+    if (p > 0) {
+      const long long cw1 = clock64();
+      if (tid == 0) {
+        while (ld_relaxed(&D_.flag[p - 1]) < (unsigned)(i + 1)) __nanosleep(20);
+        (void)ld_acquire(&D_.flag[p - 1]);
+      }
+      cbar();
+      xwait += clock64() - cw1;
+      for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D_.xs + par * xss + (long)(p - 1) * D_.wmax + e);
+      cbar();
+    }
+    // phase-3 inputs: chain A  U_hi x_p;  chain B  -U_{lo-1}^T x_{p-1}
+    cplx* vA = vbuf + 0 * 2 * WM + cur * WM;
+    cplx* vB = vbuf + 1 * 2 * WM + cur * WM;
+    for (int qq = tid; qq < w; qq += ncons) {
+      const cplx* crr = bcr + (long)m * w;      // row hi
+      const cplx* ner = bne + (long)m * w;
+      cplx ta = cmul(crr[qq], xhi[qq]);
+      if (qq + 1 < w) cfma(ta, ner[qq], xhi[qq + 1]);
+      vA[qq] = ta;
+      cplx tb = cmul(bcr[qq], xlo[qq]);          // row lo-1
+      if (qq >= 1) cfma(tb, bne[qq - 1], xlo[qq - 1]);
+      vB[qq] = cscale(tb, -1.0);
+    }
+  };
+
+  // ------------------------------------------------------------ one phase of this group's chain
+  // Chain G, phase PH (0: forward elimination / bottom-up elimination, 1: the
+  // phase-3 chain), m block steps on solve i.  Factor blocks are loaded into
+  // registers two steps ahead (per-lane packed offsets precomputed per phase),
+  // the mode-specific writer is resolved at compile time.
+  auto run_phase = [&](int i, auto G_, auto PH_) {
+    constexpr int G = decltype(G_)::value;
+    constexpr int PH = decltype(PH_)::value;
+    constexpr bool up = (G == 0) == (PH == 0);   // A1, B3 walk lo -> hi
+    constexpr int high = up ? 0 : 1;             // lo -> hi steps need o[r-1]: low-halo mapping
+    constexpr bool sub = G == 0 && PH == 1;      // chain A back substitution: o = y_c - Sinv v
+    const int w = tab[i].w;
+    const int pwb = w * (w + 1) / 2;
+    const int row = dslot_row(wi, slot, high);
+    const bool act = row >= 0 && row < w;
+    const bool owned = q == 0 && act && dslot_owned(slot, high);
+    // packed-triangle offsets of this lane's entries: k = q + 4c >= row read row `row`
+    // (affine in c), k < row read column `row` of row k; nlow = #c with k < row
+    const int rs = row * w - (row * (row - 1)) / 2;
+    const int nlow = act ? (row - q + LPR - 1) / LPR : 0;     // c < nlow  <=>  q + 4c < row
+    const int nval = act ? (w - q + LPR - 1) / LPR : 0;       // c < nval  <=>  q + 4c < w
+    const cplx* fb0 = G == 0 ? tab[i].fac : tab[i].fac2;
+    const uint64_t pol = PH == 0 ? pol_last : pol_first;
+    auto load = [&](cplx (&S)[KPL], int js) {
+#ifdef HELM_DUAL_ABL_FIXEDBLK
+      const cplx* B = fb0 + (long)lo * pwb;   // ablation: always the same block (cache-resident)
+#else
+      const cplx* B = fb0 + (long)(up ? lo + js : hi - js) * pwb;
+#endif
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        const int k = q + LPR * c;
+        const int idx = c < nlow ? k * w - (k * (k - 1)) / 2 + (row - k) : rs + (k - row);
+        S[c] = c < nval ? ld_nc_hint(B + idx, pol) : cmk(0, 0);
+      }
+    };
+    auto step = [&](int js, cplx (&S)[KPL]) {
+#ifndef HELM_DUAL_PF
+#define HELM_DUAL_PF PF
+#endif
+      if (gtid == 0 && HELM_DUAL_PF > 0) {
+        // keep the factor block PF steps ahead warm in L2 (this phase, then the
+        // other phase / the next solve's first phase)
+        int e = PH * m + js + HELM_DUAL_PF, ii = i;
+        if (e >= 2 * m) { e -= 2 * m; ++ii; }
+        if (ii < nsolve && e < 2 * m) {
+          const int ph2 = e >= m ? 1 : 0, js2 = e - ph2 * m;
+          const bool up2 = (G == 0) == (ph2 == 0);
+          const int w2 = tab[ii].w, pw2 = w2 * (w2 + 1) / 2;
+          const cplx* fbp = (G == 0 ? tab[ii].fac : tab[ii].fac2) + (long)(up2 ? lo + js2 : hi - js2) * pw2;
+          dprefetch_l2(fbp, (uint32_t)(pw2 * sizeof(cplx)), ph2 == 0 ? pol_last : pol_first);
+        }
+      }
+      const int ci = up ? js : m - 1 - js;   // local block row
+      const cplx* vin = myv + cur * WM;
+      cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        const int k = q + LPR * c;
+        if (k < w) {
+          const cplx v = vin[k];
+          if ((c & 3) == 0) cfma(a0, S[c], v);
+          else if ((c & 3) == 1) cfma(a1, S[c], v);
+          else if ((c & 3) == 2) cfma(a2, S[c], v);
+          else cfma(a3, S[c], v);
+        }
+      }
+      // refill S with the block of step js + 2 right after its last use, so the
+      // load overlaps the rest of this step and all of the next one
+      if (js + 2 < m) load(S, js + 2);
+      cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      cplx o = acc;
+      if (sub) o = act ? csub(yseg[ci * w + row], acc) : cmk(0, 0);
+      cplx nb;
+      if (high) {
+        nb.x = __shfl_down_sync(0xffffffffu, o.x, 4);
+        nb.y = __shfl_down_sync(0xffffffffu, o.y, 4);
+      } else {
+        nb.x = __shfl_up_sync(0xffffffffu, o.x, 4);
+        nb.y = __shfl_up_sync(0xffffffffu, o.y, 4);
+      }
+      if (owned) {
+        cplx* vn = myv + (cur ^ 1) * WM;
+        const bool last = js == m - 1;
+        if (G == 0 && PH == 0) {
+          // A1: y_c; next input b_{c+1} - U_c^T y_c
+          yseg[ci * w + row] = o;
+          if (!last) {
+            const cplx* cr = bcr + (long)(ci + 1) * w;
+            const cplx* ne = bne + (long)(ci + 1) * w;
+            cplx v = csub(bseg[(ci + 1) * w + row], cmul(cr[row], o));
+            if (row >= 1) v = csub(v, cmul(ne[row - 1], nb));
+            vn[row] = v;
+          }
+        } else if (G == 0) {
+          // A3: xa_c; next input U_{c-1} xa_c
+          xa[ci * w + row] = o;
+          if (!last) {
+            const cplx* cr = bcr + (long)ci * w;
+            const cplx* ne = bne + (long)ci * w;
+            cplx v = cmul(cr[row], o);
+            if (row + 1 < w) cfma(v, ne[row], nb);
+            vn[row] = v;
+          }
+        } else if (PH == 0) {
+          // B1: z_c; next input b_{c-1} - U_{c-1} z_c; z_lo = x0_lo
+          if (last) {
+            zlo[row] = o;
+          } else {
+            const cplx* cr = bcr + (long)ci * w;
+            const cplx* ne = bne + (long)ci * w;
+            cplx v = cmul(cr[row], o);
+            if (row + 1 < w) cfma(v, ne[row], nb);
+            vn[row] = csub(bseg[(ci - 1) * w + row], v);
+          }
+        } else {
+          // B3: f_c; next input -U_c^T f_c
+          fb[ci * w + row] = o;
+          if (!last) {
+            const cplx* cr = bcr + (long)(ci + 1) * w;
+            const cplx* ne = bne + (long)(ci + 1) * w;
+            cplx v = cmul(cr[row], o);
+            if (row >= 1) cfma(v, ne[row - 1], nb);
+            vn[row] = cscale(v, -1.0);
+          }
+        }
+      }
+      gbar();
+      cur ^= 1;
+    };
+    cplx S0[KPL], S1[KPL];
+    load(S0, 0);
+    if (m > 1) load(S1, 1);
+    for (int js = 0; js < m; js += 2) {
+      step(js, S0);
+      if (js + 1 < m) step(js + 1, S1);
+    }
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+
+  // the solve loop, instantiated per chain group (each group only carries the
+  // registers of its own two phases)
+  auto solve_loop = [&](auto G_) {
+    for (int i = 0; i < nsolve; ++i) {
+      const int w = tab[i].w;
+      // ---- pre-actions: epilogue of the previous solve, RHS, phase-1 inputs
+      long long c0 = clock64();
+      cbar();
+      if (i > 0) {
+        seg_epilogue(i - 1);
+        cbar();
+      }
+      seg_rhs(i);
+      cbar();
+      for (int e = tid; e < w; e += ncons) {
+        vbuf[0 * 2 * WM + cur * WM + e] = bseg[e];                // chain A: b_lo
+        vbuf[1 * 2 * WM + cur * WM + e] = bseg[(m - 1) * w + e];  // chain B: b_hi
+      }
+      cbar();
+      t_pre += clock64() - c0;
+      run_phase(i, G_, I0{});
+      // ---- separator stage, phase-3 inputs
+      c0 = clock64();
+      cbar();
+      seg_separators(i);
+      cbar();
+      t_sep += clock64() - c0;
+      run_phase(i, G_, I1{});
+    }
+  };
+  if (g == 0) solve_loop(I0{});
+  else solve_loop(I1{});
+  cbar();
+  seg_epilogue(nsolve - 1);
+  if (A.prof && tid == 0) {
+    long long* o = A.prof + (long)blockIdx.x * 8;
+    o[0] = t_pre; o[1] = t_sep; o[2] = 0; o[3] = total; o[4] = xwait;
+    o[5] = clock64() - t_start; o[6] = 1; o[7] = d;
+  }
+}
+
+// ------------------------------------------------------------------ host
+static constexpr int kDualSmemMax = 227 * 1024;
+extern long long* helm_sweep_prof_buffer();
+
+// Launches the two-chain kernel if every direction fits it (w <= 36, P > 1,
+// explicit separator inverse and bottom-up inverses built at setup); returns
+// -1 (not applicable) otherwise.
+int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
+                     cudaStream_t st) {
+  using namespace dualk;
+  int wmax = 0, pmax = 1, nsolve_max = 1;
+  for (int d = 0; d < t; ++d) {
+    wmax = std::max(wmax, dirs[d]->wmax);
+    pmax = std::max(pmax, dirs[d]->P);
+    nsolve_max = std::max(nsolve_max, dirs[d]->is_double ? 2 * dirs[d]->N - 1 : dirs[d]->N);
+    if (dirs[d]->P < 2 || !dirs[d]->d_xinv || !dirs[d]->d_fac2 || !dirs[d]->d_facp) return -1;
+  }
+  if (wmax > LPR * KPL || wmax > WM) return -1;
+  const int nw = (wmax + OWN - 1) / OWN;
+  const int threads = 2 * nw * 32;
+  if (threads > MAXT) return -1;
+  long vec_elems = 0;
+  int ctas = 0;
+  for (int d = 0; d < t; ++d) {
+    const helm_sweep_s* h = dirs[d];
+    int mmax = 0;
+    for (int p = 0; p < h->P; ++p) mmax = std::max(mmax, h->seg_hi[p] - h->seg_lo[p] + 1);
+    vec_elems = std::max(vec_elems, (long)(mmax + 1) * h->wmax);
+    vec_elems = std::max(vec_elems, (long)(h->P - 1) * h->wmax);
+    ctas += h->P;
+  }
+  vec_elems = (vec_elems + 7) / 8 * 8;
+  size_t head = sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + 16;
+  head = (head + 127) / 128 * 128;
+  const size_t smem = head + sizeof(cplx) * 8 * vec_elems;
+  if (smem > (size_t)kDualSmemMax) return -1;
+  // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
+  std::vector<size_t> off(t);
+  size_t total = 0;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  for (int d = 0; d < t; ++d) {
+    const helm_sweep_s* h = dirs[d];
+    off[d] = total;
+    total += al(sizeof(unsigned) * (2 + h->P));
+    total += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax) * 2;
+    total += al(sizeof(cplx) * 2L * h->P * h->wmax);
+    total += al(sizeof(cplx) * (long)h->N * h->nc);
+    total += al(sizeof(cplx) * (long)h->nc);
+  }
+  unsigned char* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&scratch, total, st);
+  if (e != cudaSuccess) {
+    helm_set_error("sweep_apply: scratch alloc: %s", cudaGetErrorString(e));
+    return HELM_ENOMEM;
+  }
+  const helm_problem_s* prob = dirs[0]->prob;
+  DualArgs A;
+  memset(&A, 0, sizeof(A));
+  A.t = t;
+  A.nw = nw;
+  A.vec_elems = (int)vec_elems;
+  A.nsolve_max = nsolve_max;
+  A.pmax = pmax;
+  A.prof = helm_sweep_prof_buffer();
+  int base = 0;
+  for (int d = 0; d < t; ++d) {
+    const helm_sweep_s* h = dirs[d];
+    DirArgs& D = A.d[d];
+    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc;
+    D.nxp1 = prob->nx + 1; D.is_double = h->is_double; D.ntile_max = 1;
+    D.a = h->d_a; D.w = h->d_w; D.own_lo = h->d_own_lo; D.own_hi = h->d_own_hi;
+    D.seg_lo = h->d_seg_lo; D.seg_hi = h->d_seg_hi;
+    D.cr = h->d_cr; D.ne = h->d_ne; D.tc = h->d_tc;
+    D.fac = h->d_fac; D.fac2 = h->d_fac2; D.facp = h->d_facp; D.pfac_off = h->d_pfac_off; D.fac_off = h->d_fac_off; D.red = h->d_red; D.red_off = h->d_red_off;
+    D.xinv = h->d_xinv; D.xinv_off = h->d_xinv_off;
+    D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
+    D.Z = Zdev + (long)d * ldz;
+    unsigned char* q = scratch + off[d];
+    D.cnt = (unsigned*)q; D.flag = D.cnt + 2; q += al(sizeof(unsigned) * (2 + h->P));
+    D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
+    D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
+    D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
+    D.corr_prev = (cplx*)q; q += al(sizeof(cplx) * (long)h->N * h->nc);
+    D.corr_next = (cplx*)q;
+    D.wmax = h->wmax;
+    D.cta_base = base;
+    base += h->P;
+    if (e == cudaSuccess) e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * (2 + h->P), st);
+  }
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_sweep_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, nsm = 0, occ = 0;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_dual, threads, smem);
+  if (e == cudaSuccess && occ * nsm < ctas) {
+    cudaFreeAsync(scratch, st);
+    return -1;   // not co-resident: the caller falls back to the single-chain kernel
+  }
+  if (e == cudaSuccess) {
+    void* args[] = {(void*)&A};
+    e = cudaLaunchCooperativeKernel((void*)k_sweep_dual, dim3(ctas), dim3(threads), args, smem, st);
+    g_helm_launches++;
+  }
+  cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) {
+    helm_set_error("sweep_apply (dual): %s", cudaGetErrorString(e));
+    return HELM_ECUDA;
+  }
+  return HELM_OK;
+}

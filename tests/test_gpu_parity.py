@@ -106,6 +106,27 @@ def test_sweep_apply_parity(name, nseg):
         assert rel(Zh[k], z_ref) <= 1e-10, (name, names[k], rel(Zh[k], z_ref))
 
 
+@pytest.mark.parametrize("kernel", ["dual", "warp", "fast", "general"])
+@pytest.mark.parametrize("name", ["var", "C2", "C5s"])
+def test_sweep_kernels_parity(kernel, name, monkeypatch):
+    """Every sweep kernel (HELM_SWEEP_KERNEL, read per call) against the oracle:
+    two-chain block kernel (default), warp-chain kernel, single-chain
+    register-streaming kernel, general TMA-ring kernel."""
+    monkeypatch.setenv("HELM_SWEEP_KERNEL", kernel)
+    cfg = CFGS[name]()
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+    R = random_vector(cfg.n, 12, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    Zh = Z.cpu().numpy()
+    for k, P in enumerate(_oracle_precs(cfg, A, names)):
+        z_ref = P.apply(R[k])
+        assert rel(Zh[k], z_ref) <= 1e-10, (kernel, name, names[k], rel(Zh[k], z_ref))
+
+
 @pytest.mark.parametrize("names", [["LR", "RL", "BT", "TB"]])
 def test_single_sweeps_and_broadcast(names):
     cfg = CFGS["var"]()

@@ -29,7 +29,7 @@ def run(ds):
     return Z.cpu().numpy()
 
 
-kern = os.environ.get("HELM_SWEEP_KERNEL", "fast")
+kern = os.environ.get("HELM_SWEEP_KERNEL", "default")
 Zb = run(dirs)
 for k, nm in enumerate(cfg.dirs):
     Zs = run([dirs[k]])[0]

@@ -59,6 +59,7 @@ if os.environ.get("HELM_CYCLES"):
         sel = sel[sel[:, 3] > 0]
         st = sel[:, 3].mean()
         print(f"  totals per CTA: pre(epilogue+rhs) {sel[:,0].mean():.3e}  sep-stage {sel[:,1].mean():.3e}  "
+              f"ring-wait {sel[:,2].mean():.3e}  "
               f"steps {(sel[:,5]-sel[:,0]-sel[:,1]).mean():.3e} -> {(sel[:,5]-sel[:,0]-sel[:,1]).mean()/st:.0f} cyc/step")
         print(f"{'reducer' if role else 'segment'} CTAs={len(sel)} steps={st:.0f} total={sel[:,5].mean():.3e} cyc | "
               f"per step: pre|peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
