@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     tab[i].s = s;
   }
   if (tid == 0) *prog = 0;
+  for (int e = tid; e < 4 * WM; e += blockDim.x) vbuf[e] = cmk(0, 0);   // padding entries stay finite
   const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
   const int m = hi - lo + 1;
   const int sps = 2 * m;                 // steps per solve per chain
@@ -181,7 +182,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   const int wi = gtid >> 5, lane = tid & 31;
   const int slot = lane >> 2, q = lane & 3;
   const long band_stride = (long)D_.nc * D_.wmax;
-  long long xwait = 0, t_sep = 0, t_pre = 0;
+  long long xwait = 0, t_sep = 0, t_pre = 0, t_xmv = 0;
+  long long tprof[4] = {0, 0, 0, 0};   // step sub-phases (thread 0): mat-vec, loads+reduce, writer, barrier
   const long long t_start = clock64();
   auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
   auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory"); };
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     cbar();
     // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
+    const long long cx0 = clock64();
     const int cw = tid >> 5, ncw = ncons >> 5;
     if (p < P - 1) {
       for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
@@ -373,6 +376,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (p == P - 1) xhi[e] = cmk(0, 0);
     }
     cbar();
+    t_xmv += clock64() - cx0;
     // publish x_p (parity buffer; also the next solve's correction source),
     // then take x_{p-1} from the left neighbour
     if (p < P - 1) {
@@ -446,6 +450,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       }
     };
     auto step = [&](int js, cplx (&S)[KPL]) {
+      long long q0 = 0;
+      if (A.prof && tid == 0) q0 = clock64();
 #ifndef HELM_DUAL_PF
 #define HELM_DUAL_PF PF
 #endif
@@ -465,6 +471,20 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       const int ci = up ? js : m - 1 - js;   // local block row
       const cplx* vin = myv + cur * WM;
       cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
+#ifndef HELM_DUAL_ABL_NOFMA
+#ifdef HELM_DUAL_VHOIST
+      // all nine input entries first (entries k >= w of the input are zero-padded)
+      cplx vv[KPL];
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) vv[c] = vin[q + LPR * c];
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        if ((c & 3) == 0) cfma(a0, S[c], vv[c]);
+        else if ((c & 3) == 1) cfma(a1, S[c], vv[c]);
+        else if ((c & 3) == 2) cfma(a2, S[c], vv[c]);
+        else cfma(a3, S[c], vv[c]);
+      }
+#else
 #pragma unroll
       for (int c = 0; c < KPL; ++c) {
         const int k = q + LPR * c;
@@ -476,9 +496,17 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           else cfma(a3, S[c], v);
         }
       }
+#endif
+#else
+      a0 = cadd(vin[q], S[0]);
+#endif
+      long long q1 = 0;
+      if (A.prof && tid == 0) { q1 = clock64(); tprof[0] += q1 - q0; }
       // refill S with the block of step js + 2 right after its last use, so the
       // load overlaps the rest of this step and all of the next one
+#ifndef HELM_DUAL_ABL_NOLDG
       if (js + 2 < m) load(S, js + 2);
+#endif
       cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
@@ -494,6 +522,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         nb.x = __shfl_up_sync(0xffffffffu, o.x, 4);
         nb.y = __shfl_up_sync(0xffffffffu, o.y, 4);
       }
+      long long q2 = 0;
+      if (A.prof && tid == 0) { q2 = clock64(); tprof[1] += q2 - q1; }
       if (owned) {
         cplx* vn = myv + (cur ^ 1) * WM;
         const bool last = js == m - 1;
@@ -540,7 +570,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           }
         }
       }
+      long long q3 = 0;
+      if (A.prof && tid == 0) { q3 = clock64(); tprof[2] += q3 - q2; }
       gbar();
+      if (A.prof && tid == 0) tprof[3] += clock64() - q3;
       cur ^= 1;
     };
     cplx S0[KPL], S1[KPL];
@@ -589,9 +622,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cbar();
   seg_epilogue(nsolve - 1);
   if (A.prof && tid == 0) {
-    long long* o = A.prof + (long)blockIdx.x * 8;
-    o[0] = t_pre; o[1] = t_sep; o[2] = 0; o[3] = total; o[4] = xwait;
+    long long* o = A.prof + (long)blockIdx.x * 16;
+    o[0] = t_pre; o[1] = t_sep; o[2] = t_xmv; o[3] = total; o[4] = xwait;
     o[5] = clock64() - t_start; o[6] = 1; o[7] = d;
+    for (int k = 0; k < 4; ++k) o[8 + k] = tprof[k];
   }
 }
 

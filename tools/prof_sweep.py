@@ -45,13 +45,19 @@ if os.environ.get("HELM_CYCLES"):
     import ctypes
     L = hs.load()
     ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)  # upper bound
-    buf = torch.zeros(ctas * 8, dtype=torch.int64, device=dev)
+    stride = 16 if hs.sweep_kernel_name() == "k_sweep_dual" else 8
+    buf = torch.zeros(ctas * stride, dtype=torch.int64, device=dev)
     L.helm_sweep_profile.argtypes = [ctypes.c_void_p]
     L.helm_sweep_profile(ctypes.c_void_p(buf.data_ptr()))
     hs.sweep_apply(dirs, r, Z, ldr=0)
     torch.cuda.synchronize()
     L.helm_sweep_profile(ctypes.c_void_p(0))
-    b = buf.view(ctas, 8).cpu().numpy()
+    b = buf.view(ctas, stride).cpu().numpy()
+    if stride == 16:
+        sel = b[b[:, 3] > 0]
+        tp = sel[:, 8:12].mean(axis=0) / sel[:, 3].mean()
+        print(f"  dual step sub-phases (cycles/step, thread 0): mat-vec {tp[0]:.0f}  loads+reduce+nb {tp[1]:.0f}  "
+              f"writer {tp[2]:.0f}  barrier {tp[3]:.0f}")
     for role in (0, 1):
         sel = b[b[:, 6] == role]
         if len(sel) == 0:
@@ -59,7 +65,7 @@ if os.environ.get("HELM_CYCLES"):
         sel = sel[sel[:, 3] > 0]
         st = sel[:, 3].mean()
         print(f"  totals per CTA: pre(epilogue+rhs) {sel[:,0].mean():.3e}  sep-stage {sel[:,1].mean():.3e}  "
-              f"ring-wait {sel[:,2].mean():.3e}  "
+              f"slot2 (warp: ring wait, dual: X mat-vec) {sel[:,2].mean():.3e}  xwait {sel[:,4].mean():.3e}  "
               f"steps {(sel[:,5]-sel[:,0]-sel[:,1]).mean():.3e} -> {(sel[:,5]-sel[:,0]-sel[:,1]).mean()/st:.0f} cyc/step")
         print(f"{'reducer' if role else 'segment'} CTAs={len(sel)} steps={st:.0f} total={sel[:,5].mean():.3e} cyc | "
               f"per step: pre|peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
