@@ -98,6 +98,22 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ cplx ldcg(const cplx* p) { return __ldcg(p); }
+// TMA bulk copy global -> shared with an L2 cache-policy hint
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// 16-byte shared-memory load by byte address
+__device__ __forceinline__ cplx lds128(uint32_t addr) {
+  cplx v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 
 // ------------------------------------------------------------------ geometry helpers
 __device__ __forceinline__ int sigma(const DirArgs& D, int m) { return D.order == 0 ? m : D.N - 1 - m; }

@@ -23,10 +23,15 @@
 // same factor bytes as sweep_fast.cu, with half the dependent steps.
 //
 // Warps [0, nw) run chain A, [nw, 2 nw) chain B (named barriers 1 and 2);
-// whole-consumer stages use barrier 3; one helper warp keeps the factor blocks
-// of the next PF steps warm in L2.  The block-step data path (4 lanes per
-// block row, 7 owned + 1 halo row per warp, factor blocks streamed
-// L2 -> registers D steps ahead) is that of sweep_fast.cu.
+// whole-consumer stages use barrier 3.  A block step: 4 lanes per block row,
+// 7 owned + 1 halo row per warp (the halo gives the writer lanes the
+// neighbour value of the bidiagonal coupling with one shuffle).  The packed
+// factor blocks are streamed HBM/L2 -> shared memory by one cp.async.bulk per
+// block into a per-chain NST-stage ring (mbarrier complete_tx) issued NST-1
+// blocks ahead across phase and solve boundaries by lane 0 of the group; each
+// lane reads its nine entries with precomputed byte offsets (the 16-byte
+// register loads of an earlier revision cost ~1200 cycles per step in L1
+// wavefronts and exposed latency, tools/bench_dualstep.cu).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -38,9 +43,8 @@ namespace dualk {
 constexpr int LPR = 4;    // lanes per block row
 constexpr int OWN = 7;    // owned rows per warp (8 slots, 1 halo)
 constexpr int KPL = 9;    // complex entries per lane per block row (w <= 36)
-constexpr int D = 2;      // register prefetch depth (block steps)
 constexpr int WM = 40;    // vector stride
-constexpr int PF = 12;    // L2 prefetch distance (block steps)
+constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
 constexpr int MAXT = 5 * 64;   // 2 groups of <= 5 warps (w <= 35)
 }  // namespace dualk
 
@@ -51,7 +55,8 @@ struct DualArgs {
   int vec_elems;    // cplx per vector area
   int nsolve_max;
   int pmax;
-  long long* prof;  // optional per-CTA counters (8 per CTA)
+  int stage_elems;  // cplx per ring stage (>= largest packed block + 1 zero entry)
+  long long* prof;  // optional per-CTA counters (16 per CTA)
 };
 
 struct DualTab {
@@ -80,37 +85,12 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ cplx ld_nc_hint(const cplx* a, uint64_t pol) {
-  cplx v;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(a), "l"(pol));
-  return v;
-}
 __device__ __forceinline__ cplx ld_cg_hint(const cplx* a, uint64_t pol) {
   cplx v;
   asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(v.x), "=d"(v.y)
                : "l"(a), "l"(pol));
   return v;
-}
-
-// entries S[row][q + 4c] of a complex-symmetric block stored as a packed upper
-// triangle (row i at i w - i (i-1) / 2): k >= row from row `row`, k < row from
-// row k (column `row`); the 8 row slots of a warp read consecutive addresses in
-// the lower part, so both halves stay coalesced per 4-lane group / per column
-__device__ __forceinline__ void dload_block(cplx (&dst)[dualk::KPL], const cplx* B, int w, int row, int q,
-                                            uint64_t pol) {
-  const bool ok = row >= 0 && row < w;
-  const int rs = row * w - (row * (row - 1)) / 2;
-#pragma unroll
-  for (int c = 0; c < dualk::KPL; ++c) {
-    const int k = q + dualk::LPR * c;
-    int idx;
-    if (k >= row) idx = rs + (k - row);
-    else idx = k * w - (k * (k - 1)) / 2 + (row - k);
-    dst[c] = (ok && k < w) ? ld_nc_hint(B + idx, pol) : cmk(0, 0);
-  }
 }
 
 __device__ __forceinline__ void dprefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
@@ -140,23 +120,25 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   const int p = blockIdx.x - D_.cta_base;
   const int P = D_.P, K = P - 1;
 
-  cplx* vbuf = reinterpret_cast<cplx*>(smem_raw);   // [group][2][WM]
+  // ring stages first (TMA destinations, 128-byte aligned), then barriers, vectors
+  cplx* ring = reinterpret_cast<cplx*>(smem_raw);                          // [2][NST][stage_elems]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 2L * NST * A.stage_elems);   // [2][NST]
+  cplx* vbuf = reinterpret_cast<cplx*>(full + 2 * NST);                    // [group][2][WM]
   cplx* xlo = vbuf + 4 * WM;                        // x_{p-1}
   cplx* xhi = xlo + WM;                             // x_p
   cplx* zlo = xhi + WM;                             // x0_lo (chain B phase 1)
   cplx* cpv = zlo + WM;                             // [pmax] prev-side separator corrections
   cplx* cnv = cpv + A.pmax;                         // [pmax] next-side separator corrections
   DualTab* tab = reinterpret_cast<DualTab*>(cnv + A.pmax);
-  volatile int* prog = reinterpret_cast<volatile int*>(tab + A.nsolve_max);
-  cplx* vec0 = reinterpret_cast<cplx*>(smem_raw + ((((char*)(prog + 4) - (char*)smem_raw) + 127) / 128) * 128);
+  cplx* vec0 = reinterpret_cast<cplx*>(
+      smem_raw + ((((char*)(tab + A.nsolve_max) - (char*)smem_raw) + 127) / 128) * 128);
   cplx* bseg = vec0;                                // RHS rows lo..hi
   cplx* yseg = bseg + A.vec_elems;                  // chain A phase 1 (y)
-  cplx* xa = yseg + A.vec_elems;                    // chain A phase 3
+  cplx* xa = yseg + A.vec_elems;                    // chain A phase 3 (aliased by g in the separator stage)
   cplx* fb = xa + A.vec_elems;                      // chain B phase 3
   cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi
   cplx* bne = bcr + A.vec_elems;
-  cplx* xsg = bne + A.vec_elems;                    // final rows x = xa + fb
-  cplx* gsm = xsg + A.vec_elems;                    // separator RHS g (K x w)
+  cplx* gsm = xa;                                   // separator RHS g (K x w), dead before phase 3
 
   const int nsolve = n_solves(D_);
   for (int i = tid; i < nsolve; i += blockDim.x) {
@@ -168,12 +150,16 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     tab[i].a = D_.a[s];
     tab[i].s = s;
   }
-  if (tid == 0) *prog = 0;
   for (int e = tid; e < 4 * WM; e += blockDim.x) vbuf[e] = cmk(0, 0);   // padding entries stay finite
+  // the zero entry after each ring stage (target of out-of-range lanes)
+  for (int e = tid; e < 2 * NST; e += blockDim.x) ring[(long)e * A.stage_elems + A.stage_elems - 1] = cmk(0, 0);
+  if (tid == 0) {
+    for (int e = 0; e < 2 * NST; ++e) mbar_init(&full[e], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
   const int m = hi - lo + 1;
-  const int sps = 2 * m;                 // steps per solve per chain
-  const int total = nsolve * sps;
+  const int total = nsolve * 2 * m;      // block steps per chain
   __syncthreads();
 
 
@@ -195,27 +181,25 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   int cur = 0;
 
   // ------------------------------------------------------------ per-solve actions (all consumers)
-  // epilogue of solve i: x = xa + fb, gather into Z, publish boundary rows, next correction
+  // epilogue of solve i: x = xa + fb gathered into Z, boundary rows published, next correction
   auto seg_epilogue = [&](int i) {
     const int st = step_of(D_, i);
     const bool bwd = is_bwd(D_, i);
     const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
     const int par = i & 1;
-    for (int e = tid; e < m * w; e += ncons) xsg[e] = cadd(xa[e], fb[e]);
-    cbar();
     if (writes_Z(D_, i)) {
       const int olo = D_.own_lo[s], ohi = D_.own_hi[s], ow = ohi - olo + 1;
       for (int e = tid; e < m * ow; e += ncons) {
         int cl = e / ow, qq = olo + e % ow;
-        D_.Z[node_of(D_, a, lo + cl, qq)] = xsg[cl * w + qq];
+        D_.Z[node_of(D_, a, lo + cl, qq)] = cadd(xa[cl * w + qq], fb[cl * w + qq]);
       }
       if (p < P - 1)
         for (int e = tid; e < ow; e += ncons) D_.Z[node_of(D_, a, hi + 1, olo + e)] = xhi[olo + e];
     }
     cplx* xb = D_.xb + par * exs + (long)p * 2 * D_.wmax;
     for (int e = tid; e < w; e += ncons) {
-      xb[e] = xsg[e];
-      xb[D_.wmax + e] = xsg[(m - 1) * w + e];
+      xb[e] = cadd(xa[e], fb[e]);
+      xb[D_.wmax + e] = cadd(xa[(m - 1) * w + e], fb[(m - 1) * w + e]);
     }
     int tdst = -1, side = 0;
     cplx* target = nullptr;
@@ -229,7 +213,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       auto X = [&](int cc, int qq) -> cplx {
         if (cc < lo) return xlo[qq];
         if (cc > hi) return xhi[qq];
-        return xsg[(cc - lo) * w + qq];
+        return cadd(xa[(cc - lo) * w + qq], fb[(cc - lo) * w + qq]);
       };
       for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction(D_, tdst, side, c, a, X);
     }
@@ -418,6 +402,34 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // phase-3 chain), m block steps on solve i.  Factor blocks are loaded into
   // registers two steps ahead (per-lane packed offsets precomputed per phase),
   // the mode-specific writer is resolved at compile time.
+  // ---- TMA producer of this group's ring (thread gtid == 0): the block sequence
+  // of chain g is, per solve, phase 0 then phase 1, m blocks each
+  uint32_t fseq = 0, cseq = 0;          // blocks issued (producer) / consumed
+  int pr_i = 0, pr_e = 0;
+  auto produce_one = [&]() {
+    if (pr_i >= nsolve) return;
+    const int w = tab[pr_i].w, pw = w * (w + 1) / 2;
+    const int ph = pr_e >= m ? 1 : 0, js = pr_e - ph * m;
+    const bool up = (g == 0) == (ph == 0);
+    const cplx* src = (g == 0 ? tab[pr_i].fac : tab[pr_i].fac2) + (long)(up ? lo + js : hi - js) * pw;
+    const int st = fseq % NST;
+    uint64_t* bar = &full[g * NST + st];
+    const uint32_t bytes = (uint32_t)(pw * sizeof(cplx));
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s_hint(ring + ((long)g * NST + st) * A.stage_elems, src, bytes, bar, ph == 0 ? pol_last : pol_first);
+    ++fseq;
+    if (++pr_e == 2 * m) { pr_e = 0; ++pr_i; }
+  };
+  if (gtid == 0)
+    for (int k = 0; k < NST - 1; ++k) produce_one();
+  const uint32_t ring_base = smem_u32(ring + (long)g * NST * A.stage_elems);
+  const uint32_t stage_bytes = (uint32_t)A.stage_elems * (uint32_t)sizeof(cplx);
+
+  // ------------------------------------------------------------ one phase of this group's chain
+  // Chain G, phase PH (0: top-down / bottom-up elimination, 1: the phase-3
+  // chain), m block steps on solve i.  Each step waits for its packed block in
+  // the ring, reads this lane's nine entries with precomputed byte offsets, and
+  // the group's producer refills the stage freed by the previous step.
   auto run_phase = [&](int i, auto G_, auto PH_) {
     constexpr int G = decltype(G_)::value;
     constexpr int PH = decltype(PH_)::value;
@@ -425,88 +437,50 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     constexpr int high = up ? 0 : 1;             // lo -> hi steps need o[r-1]: low-halo mapping
     constexpr bool sub = G == 0 && PH == 1;      // chain A back substitution: o = y_c - Sinv v
     const int w = tab[i].w;
-    const int pwb = w * (w + 1) / 2;
     const int row = dslot_row(wi, slot, high);
     const bool act = row >= 0 && row < w;
     const bool owned = q == 0 && act && dslot_owned(slot, high);
-    // packed-triangle offsets of this lane's entries: k = q + 4c >= row read row `row`
-    // (affine in c), k < row read column `row` of row k; nlow = #c with k < row
-    const int rs = row * w - (row * (row - 1)) / 2;
-    const int nlow = act ? (row - q + LPR - 1) / LPR : 0;     // c < nlow  <=>  q + 4c < row
-    const int nval = act ? (w - q + LPR - 1) / LPR : 0;       // c < nval  <=>  q + 4c < w
-    const cplx* fb0 = G == 0 ? tab[i].fac : tab[i].fac2;
-    const uint64_t pol = PH == 0 ? pol_last : pol_first;
-    auto load = [&](cplx (&S)[KPL], int js) {
-#ifdef HELM_DUAL_ABL_FIXEDBLK
-      const cplx* B = fb0 + (long)lo * pwb;   // ablation: always the same block (cache-resident)
-#else
-      const cplx* B = fb0 + (long)(up ? lo + js : hi - js) * pwb;
-#endif
+    // packed-triangle byte offsets of this lane's entries k = q + 4c: k >= row from
+    // row `row`, k < row from row k (column `row`); others -> the zero entry
+    uint32_t off[KPL];
+    {
+      const int rs = row * w - (row * (row - 1)) / 2;
 #pragma unroll
       for (int c = 0; c < KPL; ++c) {
         const int k = q + LPR * c;
-        const int idx = c < nlow ? k * w - (k * (k - 1)) / 2 + (row - k) : rs + (k - row);
-        S[c] = c < nval ? ld_nc_hint(B + idx, pol) : cmk(0, 0);
+        int idx = A.stage_elems - 1;
+        if (act && k < w) idx = k >= row ? rs + (k - row) : k * w - (k * (k - 1)) / 2 + (row - k);
+        off[c] = (uint32_t)idx * (uint32_t)sizeof(cplx);
       }
-    };
-    auto step = [&](int js, cplx (&S)[KPL]) {
+    }
+    for (int js = 0; js < m; ++js) {
       long long q0 = 0;
       if (A.prof && tid == 0) q0 = clock64();
-#ifndef HELM_DUAL_PF
-#define HELM_DUAL_PF PF
-#endif
-      if (gtid == 0 && HELM_DUAL_PF > 0) {
-        // keep the factor block PF steps ahead warm in L2 (this phase, then the
-        // other phase / the next solve's first phase)
-        int e = PH * m + js + HELM_DUAL_PF, ii = i;
-        if (e >= 2 * m) { e -= 2 * m; ++ii; }
-        if (ii < nsolve && e < 2 * m) {
-          const int ph2 = e >= m ? 1 : 0, js2 = e - ph2 * m;
-          const bool up2 = (G == 0) == (ph2 == 0);
-          const int w2 = tab[ii].w, pw2 = w2 * (w2 + 1) / 2;
-          const cplx* fbp = (G == 0 ? tab[ii].fac : tab[ii].fac2) + (long)(up2 ? lo + js2 : hi - js2) * pw2;
-          dprefetch_l2(fbp, (uint32_t)(pw2 * sizeof(cplx)), ph2 == 0 ? pol_last : pol_first);
-        }
-      }
+      if (gtid == 0) produce_one();   // refill the stage consumed by the previous step
+      const int st = cseq % NST;
+      mbar_wait(&full[G * NST + st], (cseq / NST) & 1);
+      ++cseq;
+      const uint32_t sb = ring_base + st * stage_bytes;
       const int ci = up ? js : m - 1 - js;   // local block row
       const cplx* vin = myv + cur * WM;
-      cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
-#ifndef HELM_DUAL_ABL_NOFMA
-#ifdef HELM_DUAL_VHOIST
-      // all nine input entries first (entries k >= w of the input are zero-padded)
-      cplx vv[KPL];
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) vv[c] = vin[q + LPR * c];
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) {
-        if ((c & 3) == 0) cfma(a0, S[c], vv[c]);
-        else if ((c & 3) == 1) cfma(a1, S[c], vv[c]);
-        else if ((c & 3) == 2) cfma(a2, S[c], vv[c]);
-        else cfma(a3, S[c], vv[c]);
-      }
-#else
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) {
-        const int k = q + LPR * c;
-        if (k < w) {
-          const cplx v = vin[k];
-          if ((c & 3) == 0) cfma(a0, S[c], v);
-          else if ((c & 3) == 1) cfma(a1, S[c], v);
-          else if ((c & 3) == 2) cfma(a2, S[c], v);
-          else cfma(a3, S[c], v);
-        }
-      }
-#endif
-#else
-      a0 = cadd(vin[q], S[0]);
-#endif
       long long q1 = 0;
       if (A.prof && tid == 0) { q1 = clock64(); tprof[0] += q1 - q0; }
-      // refill S with the block of step js + 2 right after its last use, so the
-      // load overlaps the rest of this step and all of the next one
-#ifndef HELM_DUAL_ABL_NOLDG
-      if (js + 2 < m) load(S, js + 2);
-#endif
+      cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
+      {
+        cplx vv[KPL], S[KPL];
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) {
+          vv[c] = vin[q + LPR * c];       // entries k >= w of the input are zero-padded
+          S[c] = lds128(sb + off[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) {
+          if ((c & 3) == 0) cfma(a0, S[c], vv[c]);
+          else if ((c & 3) == 1) cfma(a1, S[c], vv[c]);
+          else if ((c & 3) == 2) cfma(a2, S[c], vv[c]);
+          else cfma(a3, S[c], vv[c]);
+        }
+      }
       cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
@@ -575,13 +549,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       gbar();
       if (A.prof && tid == 0) tprof[3] += clock64() - q3;
       cur ^= 1;
-    };
-    cplx S0[KPL], S1[KPL];
-    load(S0, 0);
-    if (m > 1) load(S1, 1);
-    for (int js = 0; js < m; js += 2) {
-      step(js, S0);
-      if (js + 1 < m) step(js + 1, S1);
     }
   };
   using I0 = std::integral_constant<int, 0>;
@@ -661,9 +628,11 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     ctas += h->P;
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
-  size_t head = sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + 16;
-  head = (head + 127) / 128 * 128;
-  const size_t smem = head + sizeof(cplx) * 8 * vec_elems;
+  const long pwmax = (long)wmax * (wmax + 1) / 2;
+  const long stage_elems = (pwmax + 1 + 7) / 8 * 8;   // packed block + zero entry, 128-byte multiple
+  size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * 2 * NST +
+                sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + 256;
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * 6 * vec_elems;
   if (smem > (size_t)kDualSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
   std::vector<size_t> off(t);
@@ -692,6 +661,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   A.vec_elems = (int)vec_elems;
   A.nsolve_max = nsolve_max;
   A.pmax = pmax;
+  A.stage_elems = (int)stage_elems;
   A.prof = helm_sweep_prof_buffer();
   int base = 0;
   for (int d = 0; d < t; ++d) {

@@ -71,20 +71,6 @@ __device__ __forceinline__ void wprefetch_l2(const void* p, uint32_t bytes, uint
   asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
                : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ cplx lds128(uint32_t addr) {
-  cplx v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
-}
-
 __global__ void __launch_bounds__(warpk::NTH, 1) k_sweep_warp(const __grid_constant__ WarpArgs A) {
   using namespace warpk;
   extern __shared__ __align__(128) unsigned char smem_raw[];

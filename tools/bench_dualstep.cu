@@ -13,14 +13,14 @@ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
-template <int VAR>
-__global__ void __launch_bounds__(320, 1) k(int steps, double2* out, long long* cyc, const double2* __restrict__ F) {
-  __shared__ double2 vb[2][2][40];
-  const int tid = threadIdx.x, g = tid >= 160, gt = tid - g * 160, lane = tid & 31, q = lane & 3;
-  for (int e = tid; e < 160; e += blockDim.x) (&vb[0][0][0])[e] = make_double2(1e-3 * e, 2e-3);
+template <int VAR, int GG>
+__device__ __forceinline__ void body(int steps, double2* out, long long* cyc, const double2* __restrict__ F,
+                                     double2 (*vb)[2][40]) {
+  const int tid = threadIdx.x, g = GG, gt = tid - g * 160, lane = tid & 31, q = lane & 3;
+  for (int e = tid - g * 160; e < 80; e += 160) (&vb[g][0][0])[e] = make_double2(1e-3 * e, 2e-3);
   double2 S[9];
   for (int c = 0; c < 9; ++c) S[c] = make_double2(1e-2 * (c + tid % 7), 1e-3 * c);
-  __syncthreads();
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(160) : "memory");
   const int w = 35;
   int cur = 0;
   long long t0 = clock64();
@@ -71,6 +71,19 @@ __global__ void __launch_bounds__(320, 1) k(int steps, double2* out, long long* 
   if (tid == 0) out[blockIdx.x] = vb[0][cur][0];
 }
 
+template <int VAR>
+__global__ void __launch_bounds__(320, 1) k(int steps, double2* out, long long* cyc, const double2* __restrict__ F) {
+  __shared__ double2 vb[2][2][40];
+  if (VAR == 6) {
+    // the two groups execute two different copies of the loop (as in k_sweep_dual)
+    if (threadIdx.x < 160) body<4, 0>(steps, out, cyc, F, vb);
+    else body<4, 1>(steps, out, cyc, F, vb);
+  } else {
+    if (threadIdx.x < 160) body<VAR, 0>(steps, out, cyc, F, vb);
+    else body<VAR, 1>(steps, out, cyc, F, vb);
+  }
+}
+
 __global__ void k_tput(double* out, int iters, int nchains) {
   double a[8];
   for (int i = 0; i < 8; ++i) a[i] = threadIdx.x + i;
@@ -95,13 +108,13 @@ int main() {
   cudaMalloc(&d, 1 << 26);
   long long h[256];
   const int steps = 4000;
-  const char* names[] = {"full step", "no barrier (syncwarp)", "no shuffles", "no FMAs", "+LDG refill (streaming)", "+LDG refill (same block)"};
+  const char* names[] = {"full step", "no barrier (syncwarp)", "no shuffles", "no FMAs", "+LDG refill (streaming)", "+LDG refill (same block)", "+LDG, distinct code per group"};
   double2* F;
   const long fbytes = (long)nsm * 2 * 4096L * 1225 * 16;
   if (cudaMalloc(&F, fbytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
   cudaMemset(F, 0, fbytes);
   for (int ctas : {1, nsm}) {
-    for (int v = 0; v < 6; ++v) {
+    for (int v = 0; v < 7; ++v) {
       for (int rep = 0; rep < 2; ++rep) {
         if (v == 0) k<0><<<ctas, 320>>>(steps, o, cyc, F);
         if (v == 1) k<1><<<ctas, 320>>>(steps, o, cyc, F);
@@ -109,6 +122,7 @@ int main() {
         if (v == 3) k<3><<<ctas, 320>>>(steps, o, cyc, F);
         if (v == 4) k<4><<<ctas, 320>>>(steps, o, cyc, F);
         if (v == 5) k<5><<<ctas, 320>>>(steps, o, cyc, F);
+        if (v == 6) k<6><<<ctas, 320>>>(steps, o, cyc, F);
       }
       cudaDeviceSynchronize();
       cudaMemcpy(h, cyc, sizeof(long long) * 1, cudaMemcpyDeviceToHost);
