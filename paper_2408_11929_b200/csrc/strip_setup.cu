@@ -193,7 +193,7 @@ struct RowSmem {
   cplx mat[kRowW * kRowW];    // natural-order inverse of the current block / Y
   cplx tmat[kRowW * kRowW];   // U_c Y (kind 0, X[lo,hi] chain)
   cplx prow[kRowW];
-  double redv[kRowWarps];
+  unsigned redk[kRowWarps];
   int redi[kRowWarps];
   int pivrow[kRowW];
 };
@@ -206,38 +206,42 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
   const bool active = i < w;
   bool used = false;
   int kstep = 0;
-#pragma unroll
-  for (int k = 0; k < kRowW; ++k) {
-    if (k >= w) break;
+  // the pivot loop is NOT unrolled (a fully unrolled loop thrashed the instruction
+  // cache, ncu no_inst ~27%); the pivot-column entry a[k >> 1] is extracted and
+  // written back with unrolled selects
+#pragma unroll 1
+  for (int k = 0; k < w; ++k) {
     const int kh = k & 1, kj = k >> 1;
-    double best = (active && !used && h == kh) ? cabs2(a[kj]) : -1.0;
-    int bi = i;
+    cplx mine = a[0];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    if (lane == 0) { sm.redv[warp] = best; sm.redi[warp] = bi; }
+    for (int jj = 1; jj < kRowHW; ++jj)
+      if (jj == kj) mine = a[jj];
+    // pivot search: the largest |a_ik|^2 among unused rows, compared on the high
+    // 32 bits of the (non-negative) double -- monotonic; candidates equal to ~1e-6
+    // relative go to the lowest row -- with one warp max-reduction and a ballot
+    const double mag = (active && !used && h == kh) ? cabs2(mine) : 0.0;
+    const unsigned key = (active && !used && h == kh) ? (unsigned)__double2hiint(mag) + 1u : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    const unsigned who = __ballot_sync(0xffffffffu, key == kmax);
+    if (lane == 0) { sm.redk[warp] = kmax; sm.redi[warp] = warp * 16 + ((__ffs(who) - 1) >> 1); }
     __syncthreads();
-    double b0 = sm.redv[0];
+    unsigned k0 = sm.redk[0];
     int p = sm.redi[0];
 #pragma unroll
     for (int q = 1; q < kRowWarps; ++q)
-      if (sm.redv[q] > b0) { b0 = sm.redv[q]; p = sm.redi[q]; }
-    if (!(b0 > 0.0)) return 1;
+      if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
+    if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
     // pivot element to both halves of the pivot row; multiplier to both halves of the others
-    const cplx mine = a[kj];
     cplx akk;
     akk.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);
     akk.y = __shfl_xor_sync(0xffffffffu, mine.y, 1);
     if (h == kh) akk = mine;
     if (i == p) {
       const cplx dinv = cinv(akk);
-      if (h == kh) a[kj] = cmk(1.0, 0.0);
 #pragma unroll
       for (int jj = 0; jj < kRowHW; ++jj) {
-        a[jj] = cmul(a[jj], dinv);
+        const cplx v = (h == kh && jj == kj) ? cmk(1.0, 0.0) : a[jj];
+        a[jj] = cmul(v, dinv);
         sm.prow[2 * jj + h] = a[jj];
       }
       used = true;
@@ -247,12 +251,13 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
     __syncthreads();
     if (active && i != p) {
       const cplx f = akk;
-      if (h == kh) a[kj] = cmk(0.0, 0.0);
 #pragma unroll
       for (int jj = 0; jj < kRowHW; ++jj) {
         const cplx r = sm.prow[2 * jj + h];
-        a[jj].x -= f.x * r.x - f.y * r.y;
-        a[jj].y -= f.x * r.y + f.y * r.x;
+        cplx v = (h == kh && jj == kj) ? cmk(0.0, 0.0) : a[jj];
+        v.x -= f.x * r.x - f.y * r.y;
+        v.y -= f.x * r.y + f.y * r.x;
+        a[jj] = v;
       }
     }
   }
@@ -380,14 +385,23 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
       }
       __syncthreads();
       if (i < w) {
+        // row i of Sinv_c: all loads issued before the products (one latency, not w)
         const cplx* srow = fac + (long)c * w2 + (long)i * w;
         cplx acc[kRowHW];
 #pragma unroll
         for (int jj = 0; jj < kRowHW; ++jj) acc[jj] = cmk(0, 0);
-        for (int r = 0; r < w; ++r) {
-          const cplx sv = srow[r];
 #pragma unroll
-          for (int jj = 0; jj < kRowHW; ++jj) cfma(acc[jj], sv, sm.tmat[r * kRowW + 2 * jj + h]);
+        for (int r0 = 0; r0 < kRowW; r0 += 12) {
+          cplx sr[12];
+#pragma unroll
+          for (int u = 0; u < 12; ++u) sr[u] = r0 + u < w ? __ldcg(srow + r0 + u) : cmk(0, 0);
+#pragma unroll
+          for (int u = 0; u < 12; ++u) {
+            if (r0 + u < w) {
+#pragma unroll
+              for (int jj = 0; jj < kRowHW; ++jj) cfma(acc[jj], sr[u], sm.tmat[(r0 + u) * kRowW + 2 * jj + h]);
+            }
+          }
         }
         // mat is not read in this phase: overwrite row i with Y_c directly
 #pragma unroll
