@@ -231,6 +231,43 @@ class Sweep:
             pass
 
 
+_AXIS = {name: ax for name, (ax, _o, _d) in DIRECTIONS.items()}
+
+
+def make_sweeps(problem, names, n_strips=4, overlap=1, streams=None, **kw):
+    """sweep_setup for several directions, the two axes concurrently: the
+    directions of one axis share a factor set and are set up in order on one
+    stream, each axis on its own stream and host thread (the library call
+    releases the GIL; sweep_setup synchronises its own stream before
+    returning).  `streams` maps axis -> CUDA stream handle (default: two
+    torch streams).  Returns the Sweep handles in the order of `names`."""
+    import threading
+    groups = {}
+    for k, nm in enumerate(names):
+        groups.setdefault(_AXIS[nm], []).append((k, nm))
+    if streams is None:
+        import torch
+        streams = {ax: torch.cuda.Stream().cuda_stream for ax in groups}
+    out = [None] * len(names)
+    errors = []
+
+    def run(ax):
+        try:
+            for k, nm in groups[ax]:
+                out[k] = Sweep(problem, nm, n_strips=n_strips, overlap=overlap, stream=streams[ax], **kw)
+        except Exception as e:  # re-raised in the caller's thread
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(ax,)) for ax in groups]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    return out
+
+
 def _dir_array(dirs):
     arr = (ctypes.c_void_p * len(dirs))()
     for k, d in enumerate(dirs):

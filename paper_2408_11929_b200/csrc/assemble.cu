@@ -9,7 +9,7 @@
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
-long g_helm_launches = 0;
+std::atomic<long> g_helm_launches{0};
 
 void helm_set_error(const char* fmt, ...) {
   va_list ap;
@@ -19,7 +19,7 @@ void helm_set_error(const char* fmt, ...) {
 }
 
 extern "C" const char* helm_last_error(void) { return g_err; }
-extern "C" long helm_kernel_launches(void) { return g_helm_launches; }
+extern "C" long helm_kernel_launches(void) { return g_helm_launches.load(); }
 
 extern "C" const char* helm_strerror(int code) {
   switch (code) {
@@ -37,8 +37,8 @@ extern "C" const char* helm_strerror(int code) {
 
 // ------------------------------------------------------------------ device memory
 cudaError_t helm_dev_alloc(void** p, size_t bytes) {
-  static bool pool_ready = false;
-  if (!pool_ready) {
+  static std::once_flag pool_ready;
+  std::call_once(pool_ready, []() {
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -46,10 +46,16 @@ cudaError_t helm_dev_alloc(void** p, size_t bytes) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
-    pool_ready = true;
-  }
-  cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 16, 0);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  });
+  // allocations are ordered on a private non-blocking stream that carries no
+  // other work: the synchronisation returns at once and never waits for (or
+  // serialises with) kernels the caller runs on other streams -- e.g. the two
+  // axes' sweep_setup calls running concurrently
+  static cudaStream_t alloc_stream = nullptr;
+  static std::once_flag stream_ready;
+  std::call_once(stream_ready, []() { cudaStreamCreateWithFlags(&alloc_stream, cudaStreamNonBlocking); });
+  cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 16, alloc_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(alloc_stream);
   return e;
 }
 

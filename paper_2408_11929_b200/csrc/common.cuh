@@ -1,5 +1,6 @@
 // common.cuh -- shared device/host helpers of the helmsweep library (sm_100a).
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -41,7 +42,7 @@ __host__ __device__ __forceinline__ cplx cinv(cplx a) {
 
 // ------------------------------------------------------------------ errors
 void helm_set_error(const char* fmt, ...);
-extern long g_helm_launches;
+extern std::atomic<long> g_helm_launches;   // host counter of this library's launches (thread-safe)
 
 #define HELM_CUDA_TRY(expr)                                                       \
   do {                                                                            \

@@ -68,6 +68,47 @@ __device__ inline void blk_matmul(cplx* C, const cplx* A, bool transA, const cpl
   __syncthreads();
 }
 
+// Register-tiled C (+)= alpha * op(A) B for w x w blocks with explicit leading
+// dimensions (4 x 4 output tile per thread: 8 operand loads per 16 products).
+// C must not alias A or B.  Whole CTA; ends with __syncthreads().
+__device__ inline void blk_mm_tiled(cplx* C, int ldc, const cplx* A, int lda, bool transA, const cplx* B, int ldb,
+                                    int w, double alpha, bool accumulate) {
+  const int nt = (w + 3) / 4;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+    cplx acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = cmk(0, 0);
+    for (int r = 0; r < w; ++r) {
+      cplx av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        av[u] = i < w ? (transA ? A[(long)r * lda + i] : A[(long)i * lda + r]) : cmk(0, 0);
+        const int j = j0 + u;
+        bv[u] = j < w ? B[(long)r * ldb + j] : cmk(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cfma(acc[u][v], av[u], bv[v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = i0 + u, j = j0 + v;
+        if (i < w && j < w) {
+          const cplx val = cscale(acc[u][v], alpha);
+          C[(long)i * ldc + j] = accumulate ? cadd(C[(long)i * ldc + j], val) : val;
+        }
+      }
+  }
+  __syncthreads();
+}
+
 __device__ inline void blk_copy(cplx* dst, const cplx* src, int w) {
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) dst[e] = src[e];
   __syncthreads();

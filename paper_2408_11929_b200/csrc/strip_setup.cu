@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "dense.cuh"
@@ -35,6 +36,7 @@ struct SharedFactors {
   long factor_bytes;
 };
 static std::vector<SharedFactors*> g_shared;
+static std::mutex g_shared_mu;   // setups of different axes may run on concurrent host threads
 
 // ------------------------------------------------------------------ bands + corrections
 struct StripGeo {
@@ -441,7 +443,94 @@ struct RedArgs {
   int* status;
 };
 
-__global__ void k_reduced(RedArgs ra) {
+// One CTA (96 threads) per strip walks the K = P-1 separators in order (the
+// separator block-Thomas is a chain).  Block inverses use the register-row
+// Gauss-Jordan of k_factor_rows; products use register-tiled smem matmuls.
+// Shared memory: RowSmem (static) + S, T1 (R_{k,k+1}), T2 (F_k) (dynamic).
+__global__ void __launch_bounds__(kRowThreads) k_reduced(RedArgs ra) {
+  __shared__ RowSmem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.x;
+  const int w = ra.w[s];
+  const long w2 = (long)w * w;
+  cplx* S = reinterpret_cast<cplx*>(smem_raw);
+  cplx* T1 = S + w2;   // R_{k-1,k} of the previous separator, then R_{k,k+1}
+  cplx* T2 = T1 + w2;  // F_{k-1}, then F_k
+  cplx* Bh = T2 + w2;  // staged Sinv_{h_k}
+  cplx* Bl = Bh + w2;  // staged X_{k+1}[lo,lo]
+  cplx* Bx = Bl + w2;  // staged X_{k+1}[lo,hi]
+  cplx* bands = Bx + w2;   // cr, ne of rows h_k, s_k, h_{k+1}: [6][w]
+  const long band = (long)s * ra.nc * ra.wmax;
+  const cplx* fac = ra.fac + ra.fac_off[s];
+  cplx* red = ra.red + ra.red_off[s];
+  auto scr = [&](int p) { return ra.scratch + ((long)s * ra.P + p) * ra.scratch_stride; };
+  const int P = ra.P;
+  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  for (int k = 0; k <= P - 2; ++k) {
+    const int hk = ra.seg_hi[k];          // last row of segment k
+    const int sk = hk + 1;                // separator row
+    const int hk1 = ra.seg_hi[k + 1];     // last row of segment k+1
+    cplx* Rinv = red + (long)k * 3 * w2;
+    cplx* G = Rinv + w2;
+    cplx* F = Rinv + 2 * w2;
+    // stage this separator's operands in shared memory (independent loads, one latency)
+    {
+      const cplx* g0 = fac + (long)hk * w2;
+      const cplx* g1 = scr(k + 1) + 2 * w2;
+      const cplx* g2 = scr(k + 1) + 3 * w2;
+      for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+        Bh[e] = __ldcg(g0 + e);
+        Bl[e] = __ldcg(g1 + e);
+        Bx[e] = __ldcg(g2 + e);
+      }
+      const int rows[3] = {hk, sk, hk1};
+      for (int e = threadIdx.x; e < 3 * w; e += blockDim.x) {
+        const int rr = e / w, q2 = e - rr * w;
+        bands[(2 * rr) * w + q2] = ra.cr[band + (long)rows[rr] * ra.wmax + q2];
+        bands[(2 * rr + 1) * w + q2] = ra.ne[band + (long)rows[rr] * ra.wmax + q2];
+      }
+      __syncthreads();
+    }
+    auto Ub = [&](int rr, int mode) { return Bidi{mode, bands + (2 * rr) * w, bands + (2 * rr + 1) * w}; };
+    // R_kk = D_sk - U_hk^T X_k[hi,hi] U_hk - U_sk X_{k+1}[lo,lo] U_sk^T
+    build_D(S, ra.dg + band + (long)sk * ra.wmax, ra.al + band + (long)sk * ra.wmax, w);
+    blk_lxr(S, Bh, Ub(0, BD_UT), Ub(0, BD_U), w, -1.0, true);
+    blk_lxr(S, Bl, Ub(1, BD_U), Ub(1, BD_UT), w, -1.0, true);
+    // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
+    if (k >= 1) blk_mm_tiled(S, w, T1, w, true, T2, w, w, -1.0, true);
+    // Rinv_k (register-row Gauss-Jordan; result in sm.mat, row stride kRowW)
+    cplx a[kRowHW];
+#pragma unroll
+    for (int jj = 0; jj < kRowHW; ++jj) {
+      const int col = 2 * jj + h;
+      a[jj] = (i < w && col < w) ? S[i * w + col] : cmk(0, 0);
+    }
+    if (row_invert(a, w, sm)) {
+      if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
+      return;
+    }
+    row_store(Rinv, w, sm);
+    if (k >= 1) {
+      // G_k = Rinv_k R_{k,k-1} = Rinv_k R_{k-1,k}^T   (S <- T1^T; S is free now)
+      for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+        const int p2 = e / w, q2 = e - p2 * w;
+        S[e] = T1[q2 * w + p2];
+      }
+      __syncthreads();
+      blk_mm_tiled(G, w, sm.mat, kRowW, false, S, w, w, 1.0, false);
+    }
+    if (k <= P - 3) {
+      // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1};  F_k = Rinv_k R_{k,k+1}
+      blk_lxr(T1, Bx, Ub(1, BD_U), Ub(2, BD_U), w, -1.0, false);
+      blk_mm_tiled(T2, w, sm.mat, kRowW, false, T1, w, w, 1.0, false);
+      for (int e = threadIdx.x; e < w * w; e += blockDim.x) F[e] = T2[e];
+    }
+    __syncthreads();
+  }
+}
+
+// general block width (w > 36): generic smem Gauss-Jordan and matmuls
+__global__ void k_reduced_generic(RedArgs ra) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = blockIdx.x;
   const int w = ra.w[s];
@@ -506,7 +595,7 @@ __global__ void k_reduced(RedArgs ra) {
 // (strip, column block j):  Z_j = Rinv_j E_j, Z_k = -G_k Z_{k-1} (k > j),
 // X_{K-1} = Z_{K-1}, X_k = Z_k - F_k X_{k+1}.  Storage per strip:
 // X[k] is w x (K w) row-major (the rows of separator k), contiguous.
-__global__ void k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
+__global__ void __launch_bounds__(128) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = blockIdx.y, j = blockIdx.x;
   const int K = ra.P - 1;
@@ -531,35 +620,22 @@ __global__ void k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) 
     const cplx* G = red + ((long)k * 3 + 1) * w2;
     for (int e = threadIdx.x; e < w2; e += blockDim.x) M[e] = G[e];
     __syncthreads();
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-      const int r = e / w, c = e % w;
-      cplx acc = cmk(0, 0);
-      for (int t = 0; t < w; ++t) cfma(acc, M[r * w + t], cur[t * w + c]);
-      nxt[e] = cscale(acc, -1.0);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-      cur[e] = nxt[e];
-      blkX(k, e / w, e % w) = nxt[e];
-    }
+    blk_mm_tiled(nxt, w, M, w, false, cur, w, w, -1.0, false);
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) blkX(k, e / w, e % w) = nxt[e];
+    cplx* t = cur; cur = nxt; nxt = t;
     __syncthreads();
   }
-  // backward: cur holds X_{K-1}[:, j] = Z_{K-1}[:, j]
+  // backward: cur holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}
   for (int k = K - 2; k >= 0; --k) {
     const cplx* F = red + ((long)k * 3 + 2) * w2;
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) M[e] = F[e];
-    __syncthreads();
     for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-      const int r = e / w, c = e % w;
-      cplx acc = cmk(0, 0);
-      for (int t = 0; t < w; ++t) cfma(acc, M[r * w + t], cur[t * w + c]);
-      nxt[e] = csub(blkX(k, r, c), acc);
+      M[e] = F[e];
+      nxt[e] = blkX(k, e / w, e % w);
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-      cur[e] = nxt[e];
-      blkX(k, e / w, e % w) = nxt[e];
-    }
+    blk_mm_tiled(nxt, w, M, w, false, cur, w, w, -1.0, true);
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) blkX(k, e / w, e % w) = nxt[e];
+    cplx* t = cur; cur = nxt; nxt = t;
     __syncthreads();
   }
 }
@@ -666,8 +742,13 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     }
   }
   SharedFactors* sf = nullptr;
-  for (SharedFactors* c : g_shared)
-    if (c->prob_uid == prob->uid && c->axis == axis && c->N == n_strips && c->overlap == overlap && c->P == P) sf = c;
+  {
+    std::lock_guard<std::mutex> lk(g_shared_mu);
+    for (SharedFactors* c : g_shared)
+      if (c->prob_uid == prob->uid && c->axis == axis && c->N == n_strips && c->overlap == overlap && c->P == P) sf = c;
+    if (sf) sf->refs++;   // taken under the lock; released by sweep_destroy
+  }
+  h->shared = sf;
   h->d_a = h->d_w = h->d_own_lo = h->d_own_hi = h->d_seg_lo = h->d_seg_hi = nullptr;
   h->d_dg = h->d_al = h->d_cr = h->d_ne = h->d_tc = h->d_fac = h->d_red = nullptr;
   h->d_fac_off = h->d_red_off = nullptr;
@@ -727,7 +808,6 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     h->d_fac = sf->fac; h->d_red = sf->red; h->d_xinv = sf->xinv; h->d_fac2 = sf->fac2; h->d_facp = sf->facp;
     h->factor_bytes = sf->factor_bytes;
     h->shared = sf;
-    sf->refs++;
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       helm_set_error("sweep_setup: %s", cudaGetErrorString(e));
@@ -769,7 +849,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   }
   size_t smem = sizeof(cplx) * ((size_t)wmax * wmax + wmax) + sizeof(int) * (wmax + 4) + 64;
   cudaFuncSetAttribute(k_factor_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_reduced_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int threads = wmax * wmax >= 1024 ? 512 : 256;
   FacArgs fa{h->d_w, h->d_fac_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr, h->d_ne,
              nc, wmax, P, h->d_fac, scratch, sstride, d_status, h->d_fac2, h->d_facp, h->d_pfac_off};
@@ -784,7 +864,13 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   if (e == cudaSuccess && P > 1) {
     RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
                h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
-    k_reduced<<<n_strips, threads, smem, st>>>(ra);
+    if (wmax <= kRowW) {
+      const size_t smr = sizeof(cplx) * 6 * (size_t)wmax * wmax + sizeof(cplx) * 6 * wmax;
+      cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+      k_reduced<<<n_strips, kRowThreads, smr, st>>>(ra);
+    } else {
+      k_reduced_generic<<<n_strips, threads, smem, st>>>(ra);
+    }
     if (timing) cudaEventRecord(tev[3], st);
     g_helm_launches++;
     e = cudaGetLastError();
@@ -794,7 +880,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       if (e == cudaSuccess) {
         size_t sm3 = sizeof(cplx) * 3 * wmax * wmax;
         cudaFuncSetAttribute(k_reduced_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-        k_reduced_inverse<<<dim3(P - 1, n_strips), 256, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        k_reduced_inverse<<<dim3(P - 1, n_strips), 128, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
         if (timing) cudaEventRecord(tev[4], st);
         g_helm_launches++;
         e = cudaGetLastError();
@@ -802,7 +888,11 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       }
     }
   }
+  // wait for this setup's kernels first, then read the status: a pageable copy
+  // issued while the stream is busy blocks inside the driver and serialises
+  // setups running concurrently on other streams / host threads
   int status = 0;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (timing && e == cudaSuccess) {
@@ -830,7 +920,10 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   }
   sf = new SharedFactors{1, prob->uid, axis, n_strips, overlap, P, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc,
                          h->d_fac, h->d_red, h->d_xinv, h->d_fac2, h->d_facp, h->factor_bytes};
-  g_shared.push_back(sf);
+  {
+    std::lock_guard<std::mutex> lk(g_shared_mu);
+    g_shared.push_back(sf);
+  }
   h->shared = sf;
   *out = h;
   return HELM_OK;
@@ -870,6 +963,7 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
   helm_dev_free(h->d_red_off); helm_dev_free(h->d_xinv_off);
   bool free_factors = true;
   if (h->shared) {
+    std::lock_guard<std::mutex> lk(g_shared_mu);
     SharedFactors* sf = h->shared;
     if (--sf->refs > 0) {
       free_factors = false;

@@ -24,12 +24,18 @@ for rep in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     ts = []
-    dirs = []
-    for nm in cfg.dirs:
+    if os.environ.get("PAR_SETUP"):
         a = time.perf_counter()
-        dirs.append(hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap))
+        dirs = hs.make_sweeps(prob, cfg.dirs, n_strips=cfg.n_strips, overlap=cfg.overlap)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - a)
+    else:
+        dirs = []
+        for nm in cfg.dirs:
+            a = time.perf_counter()
+            dirs.append(hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap))
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - a)
     t2 = time.perf_counter()
     prob.load_vector(f, b)
     _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol)
