@@ -132,6 +132,34 @@ __device__ __forceinline__ int next_side(const DirArgs& D) { return D.order == 0
 // Correction (D8) for destination strip t, side, row c, from a source solution
 // x_s accessed by a functor X(c', q).  Positions of the interface line and the
 // outer line in the source strip (a_src).
+// Variant with the destination strip's first line `at` and width `wt` passed in
+// (no dependent loads of the strip geometry in front of the stencil loads).
+template <class XF>
+__device__ __forceinline__ cplx correction_aw(const DirArgs& D, int t, int at, int wt, int side, int c, int a_src,
+                                              XF X) {
+  const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * 5;
+  const int bt = at + wt - 1;
+  int qi, qo, dd;
+  if (side == 0) { qi = at - a_src; qo = at - 1 - a_src; dd = -1; }
+  else { qi = bt - a_src; qo = bt + 1 - a_src; dd = 1; }
+  const cplx k0 = c >= 1 ? __ldg(k + 0) : cmk(0, 0);
+  const cplx k1 = __ldg(k + 1);
+  const cplx k2 = c + 1 < D.nc ? __ldg(k + 2) : cmk(0, 0);
+  const cplx k3 = __ldg(k + 3);
+  const bool h4 = c + dd >= 0 && c + dd < D.nc;
+  const cplx k4 = h4 ? __ldg(k + 4) : cmk(0, 0);
+  const cplx x1 = X(c, qi), x3 = X(c, qo);
+  const cplx x0 = c >= 1 ? X(c - 1, qi) : cmk(0, 0);
+  const cplx x2 = c + 1 < D.nc ? X(c + 1, qi) : cmk(0, 0);
+  const cplx x4 = h4 ? X(c + dd, qo) : cmk(0, 0);
+  cplx acc = cmul(k1, x1);
+  cfma(acc, k3, x3);
+  cfma(acc, k0, x0);
+  cfma(acc, k2, x2);
+  cfma(acc, k4, x4);
+  return acc;
+}
+
 template <class XF>
 __device__ __forceinline__ cplx correction(const DirArgs& D, int t, int side, int c, int a_src, XF X) {
   const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * 5;

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   const int wi = gtid >> 5, lane = tid & 31;
   const int slot = lane >> 2, q = lane & 3;
   const long band_stride = (long)D_.nc * D_.wmax;
-  long long xwait = 0, t_sep = 0, t_pre = 0, t_xmv = 0;
+  long long xwait = 0, t_sep = 0, t_pre = 0, t_xmv = 0, t_gw = 0, t_nw = 0, t_g = 0;
   long long tprof[4] = {0, 0, 0, 0};   // step sub-phases (thread 0): mat-vec, loads+reduce, writer, barrier
   const long long t_start = clock64();
   auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         if (cc > hi) return xhi[qq];
         return cadd(xa[(cc - lo) * w + qq], fb[(cc - lo) * w + qq]);
       };
-      for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction(D_, tdst, side, c, a, X);
+      // the destination strip is the one solve i + 1 works on
+      const int at = i + 1 < nsolve ? tab[i + 1].a : D_.a[tdst];
+      const int wt = i + 1 < nsolve ? tab[i + 1].w : D_.w[tdst];
+      for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction_aw(D_, tdst, at, wt, side, c, a, X);
     }
   };
   // RHS of solve i (rows lo..hi) and the couplings of rows lo-1..hi
@@ -251,10 +254,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     const cplx* cband = D_.cr + s * band_stride;
     const cplx* nband = D_.ne + s * band_stride;
-    const long Kw = (long)K * w;
     if (p < P - 1 && tid < 32) {
       // stream this CTA's rows of the separator inverse (w x Kw, contiguous) into L2
       // while the all-gather completes; the mat-vec below then reads L2
+      const long Kw = (long)K * w;
       const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * Kw);
       const long bytes = (long)w * Kw * (long)sizeof(cplx);
       for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
@@ -264,6 +267,13 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     for (int e = tid; e < w; e += ncons) {
       yb[e] = zlo[e];
       yb[D_.wmax + e] = yseg[(m - 1) * w + e];
+    }
+    // the source at the separator rows does not depend on the all-gather: stage it
+    // now (fb is dead between the epilogue and phase 3)
+    cplx* gR = fb;
+    for (int e = tid; e < K * w; e += ncons) {
+      const int k = e / w, qq = e - k * w;
+      gR[e] = __ldg(D_.R + node_of(D_, a, D_.seg_hi[k] + 1, qq));
     }
     cbar();
     const long long cw0 = clock64();
@@ -275,6 +285,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     cbar();
     xwait += clock64() - cw0;
+    t_gw += clock64() - cw0;
+    const long long cg0 = clock64();
     // separator-row transmission corrections (from solve i-1) for every separator
     if (st > 0 || bwd) {
       const int aprev = i > 0 ? tab[i - 1].a : 0;
@@ -288,13 +300,13 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         cplx cp = cmk(0, 0), cn = cmk(0, 0);
         if (st > 0) {
           if (!bwd) {
-            cp = correction(D_, s, prev_side(D_), sk, aprev, X);
+            cp = correction_aw(D_, s, a, w, prev_side(D_), sk, aprev, X);
             if (k == p) D_.corr_prev[(long)st * D_.nc + sk] = cp;   // kept for the backward pass
           } else {
             cp = ldcg(D_.corr_prev + (long)st * D_.nc + sk);
           }
         }
-        if (bwd) cn = correction(D_, s, next_side(D_), sk, aprev, X);
+        if (bwd) cn = correction_aw(D_, s, a, w, next_side(D_), sk, aprev, X);
         cpv[k] = cp;
         cnv[k] = cn;
       }
@@ -302,23 +314,50 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     // g_k = b_{s_k} - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]  (all K separators)
     const cplx* ybp = D_.yb + par * exs;
-    for (int e = tid; e < K * w; e += ncons) {
-      const int k = e / w, qq = e % w;
-      const int hk = D_.seg_hi[k], sk = hk + 1;
-      cplx v = __ldg(D_.R + node_of(D_, a, sk, qq));
-      if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
-      if (bwd && qq == qn) v = cadd(v, cnv[k]);
-      const cplx* yh = ybp + (long)k * 2 * D_.wmax + D_.wmax;
-      const cplx* yl = ybp + (long)(k + 1) * 2 * D_.wmax;
-      cplx tt = cmul(__ldg(cband + (long)hk * D_.wmax + qq), ldcg(yh + qq));
-      if (qq >= 1) cfma(tt, __ldg(nband + (long)hk * D_.wmax + qq - 1), ldcg(yh + qq - 1));
-      cfma(tt, __ldg(cband + (long)sk * D_.wmax + qq), ldcg(yl + qq));
-      if (qq + 1 < w) cfma(tt, __ldg(nband + (long)sk * D_.wmax + qq), ldcg(yl + qq + 1));
-      gsm[k * w + qq] = csub(v, tt);
+    // two elements per thread and pass, every load issued before the arithmetic
+    for (int e0 = tid; e0 < K * w; e0 += 2 * ncons) {
+      cplx cb[2][4], yv[2][4];
+      int kk[2], qv[2];
+      bool ok[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = e0 + u * ncons;
+        ok[u] = e < K * w;
+        const int k = ok[u] ? e / w : 0, qq = ok[u] ? e - k * w : 0;
+        kk[u] = k;
+        qv[u] = qq;
+        const int hk = D_.seg_hi[k], sk = hk + 1;
+        const cplx* yh = ybp + (long)k * 2 * D_.wmax + D_.wmax;
+        const cplx* yl = ybp + (long)(k + 1) * 2 * D_.wmax;
+        const cplx z = cmk(0, 0);
+        cb[u][0] = __ldg(cband + (long)hk * D_.wmax + qq);
+        cb[u][1] = qq >= 1 ? __ldg(nband + (long)hk * D_.wmax + qq - 1) : z;
+        cb[u][2] = __ldg(cband + (long)sk * D_.wmax + qq);
+        cb[u][3] = qq + 1 < w ? __ldg(nband + (long)sk * D_.wmax + qq) : z;
+        yv[u][0] = ldcg(yh + qq);
+        yv[u][1] = qq >= 1 ? ldcg(yh + qq - 1) : z;
+        yv[u][2] = ldcg(yl + qq);
+        yv[u][3] = qq + 1 < w ? ldcg(yl + qq + 1) : z;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        const int k = kk[u], qq = qv[u];
+        cplx v = gR[k * w + qq];
+        if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
+        if (bwd && qq == qn) v = cadd(v, cnv[k]);
+        cplx tt = cmul(cb[u][0], yv[u][0]);
+        cfma(tt, cb[u][1], yv[u][1]);
+        cfma(tt, cb[u][2], yv[u][2]);
+        cfma(tt, cb[u][3], yv[u][3]);
+        gsm[k * w + qq] = csub(v, tt);
+      }
     }
     cbar();
     // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
     const long long cx0 = clock64();
+    t_g += cx0 - cg0;
+    const long Kw = (long)K * w;
     const int cw = tid >> 5, ncw = ncons >> 5;
     if (p < P - 1) {
       for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
@@ -379,6 +418,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       }
       cbar();
       xwait += clock64() - cw1;
+      t_nw += clock64() - cw1;
       for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D_.xs + par * xss + (long)(p - 1) * D_.wmax + e);
       cbar();
     }
@@ -593,6 +633,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     o[0] = t_pre; o[1] = t_sep; o[2] = t_xmv; o[3] = total; o[4] = xwait;
     o[5] = clock64() - t_start; o[6] = 1; o[7] = d;
     for (int k = 0; k < 4; ++k) o[8 + k] = tprof[k];
+    o[12] = t_gw; o[13] = t_nw; o[14] = t_g;
   }
 }
 

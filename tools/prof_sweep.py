@@ -58,6 +58,10 @@ if os.environ.get("HELM_CYCLES"):
         tp = sel[:, 8:12].mean(axis=0) / sel[:, 3].mean()
         print(f"  dual step sub-phases (cycles/step, thread 0): mat-vec {tp[0]:.0f}  loads+reduce+nb {tp[1]:.0f}  "
               f"writer {tp[2]:.0f}  barrier {tp[3]:.0f}")
+        ns = sel[:, 3].mean() / (2 * 31)
+        print(f"  separator stage per solve (cycles, thread 0): gather wait {sel[:,12].mean()/63:.0f}  "
+              f"corrections+g {sel[:,14].mean()/63:.0f}  X mat-vec {sel[:,2].mean()/63:.0f}  neighbour wait {sel[:,13].mean()/63:.0f}  "
+              f"total {sel[:,1].mean()/63:.0f};  pre-actions {sel[:,0].mean()/63:.0f}")
     for role in (0, 1):
         sel = b[b[:, 6] == role]
         if len(sel) == 0:
