@@ -77,6 +77,30 @@ extern std::atomic<long> g_helm_launches;   // host counter of this library's la
 cudaError_t helm_dev_alloc(void** p, size_t bytes);
 void helm_dev_free(void* p);
 
+// ------------------------------------------------------------------ padded packed triangles
+// A complex-symmetric w x w block is stored as its upper triangle, row r holding
+// columns r..w-1 from entry pk_start(r, w).  Row starts are padded so that
+// pk_start(r) = 2r (mod 8), i.e. (pk_start(r) - r) = r (mod 8): in the sweep
+// kernels a quarter-warp reads one column k of 8 consecutive rows; for k >= r the
+// eight 16-byte entries pk_start(r) + k - r then fall into 8 different bank groups,
+// for k < r they are 8 consecutive entries of row k -- both conflict-free.
+// Average padding 3.5 entries per row.
+__host__ __device__ inline int pk_start(int r, int w) {
+  int x = 0;
+  for (int i = 0; i < r; ++i) {
+    x += w - i;
+    const int want = (2 * (i + 1)) & 7;
+    while ((x & 7) != want) ++x;
+  }
+  return x;
+}
+// entries per padded block (a multiple of 8, so blocks stay 128-byte aligned)
+__host__ __device__ inline int pk_size(int w) { return ((pk_start(w - 1, w) + 1) + 7) / 8 * 8; }
+// index of entry (r, k) of the symmetric block
+__host__ __device__ inline int pk_index(int r, int k, int w) {
+  return k >= r ? pk_start(r, w) + (k - r) : pk_start(k, w) + (r - k);
+}
+
 // ------------------------------------------------------------------ handles
 struct helm_problem_s {
   int nx, ny;

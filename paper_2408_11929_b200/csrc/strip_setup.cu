@@ -338,13 +338,14 @@ __device__ __forceinline__ void row_store(cplx* dst, int w, const RowSmem& sm) {
   }
 }
 
-// packed upper triangle of the (symmetrised) block in sm.mat: row r holds columns r..w-1
+// padded packed upper triangle (common.cuh pk_start) of the symmetrised block in sm.mat
 __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem& sm) {
-  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-    const int r = e / w, q = e - r * w;
-    if (q < r) continue;
-    const cplx a = sm.mat[r * kRowW + q], b = sm.mat[q * kRowW + r];
-    dst[(long)r * w - (long)r * (r - 1) / 2 + (q - r)] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+  for (int r = threadIdx.x >> 3; r < w; r += blockDim.x >> 3) {
+    const int st = pk_start(r, w);
+    for (int q = r + (threadIdx.x & 7); q < w; q += 8) {
+      const cplx a = sm.mat[r * kRowW + q], b = sm.mat[q * kRowW + r];
+      dst[st + (q - r)] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+    }
   }
 }
 
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
         return;
       }
       row_store(fac + (long)c * w2, w, sm);
-      if (fa.facp) row_store_packed(fa.facp + fa.pfac_off[s] + (long)c * (w2 + w) / 2, w, sm);
+      if (fa.facp) row_store_packed(fa.facp + fa.pfac_off[s] + (long)c * pk_size(w), w, sm);
     }
     if (fa.P == 1) return;
     // X[lo,hi]: Y_hi = Sinv_hi (in sm.mat); Y_c = -Sinv_c (U_c Y_{c+1})
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
         if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
         return;
       }
-      if (fa.fac2) row_store_packed(fa.fac2 + fa.pfac_off[s] + (long)c * (w2 + w) / 2, w, sm);
+      if (fa.fac2) row_store_packed(fa.fac2 + fa.pfac_off[s] + (long)c * pk_size(w), w, sm);
     }
     row_store(scr + 2 * w2, w, sm);
   }
@@ -730,7 +731,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h->pfac_off.resize(n_strips);
   for (int s2 = 0; s2 < n_strips; ++s2) {
     h->pfac_off[s2] = pfac_total;
-    pfac_total += (long)nc * h->w[s2] * (h->w[s2] + 1) / 2;
+    pfac_total += (long)nc * pk_size(h->w[s2]);
   }
   if (want_fac2) h->factor_bytes += 2 * pfac_total * (long)sizeof(cplx);
   long xinv_total = 0;

@@ -63,7 +63,7 @@ struct DualTab {
   const cplx* fac;
   const cplx* fac2;
   const cplx* xinv;
-  int w, a, s, pad;
+  int w, a, s, pks;   // pks: entries per padded packed block (pk_size(w))
 };
 
 __device__ __forceinline__ int dslot_row(int wi, int slot, int high) {
@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* cpv = zlo + WM;                             // [pmax] prev-side separator corrections
   cplx* cnv = cpv + A.pmax;                         // [pmax] next-side separator corrections
   DualTab* tab = reinterpret_cast<DualTab*>(cnv + A.pmax);
+  int* pkst = reinterpret_cast<int*>(tab + A.nsolve_max);   // [WM] padded row starts of the current w
   cplx* vec0 = reinterpret_cast<cplx*>(
-      smem_raw + ((((char*)(tab + A.nsolve_max) - (char*)smem_raw) + 127) / 128) * 128);
+      smem_raw + ((((char*)(pkst + WM) - (char*)smem_raw) + 127) / 128) * 128);
   cplx* bseg = vec0;                                // RHS rows lo..hi
   cplx* yseg = bseg + A.vec_elems;                  // chain A phase 1 (y)
   cplx* xa = yseg + A.vec_elems;                    // chain A phase 3 (aliased by g in the separator stage)
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     tab[i].w = D_.w[s];
     tab[i].a = D_.a[s];
     tab[i].s = s;
+    tab[i].pks = pk_size(D_.w[s]);
   }
   for (int e = tid; e < 4 * WM; e += blockDim.x) vbuf[e] = cmk(0, 0);   // padding entries stay finite
   // the zero entry after each ring stage (target of out-of-range lanes)
@@ -166,7 +168,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   const int g = tid >= gsz ? 1 : 0;       // chain group
   const int gtid = tid - g * gsz;
   const int wi = gtid >> 5, lane = tid & 31;
-  const int slot = lane >> 2, q = lane & 3;
+  // lane -> (slot = row within the warp's 8, q = column residue mod 4); slot is the
+  // fast index so that a quarter-warp reads 8 rows of one column (conflict-free with
+  // the padded packed layout, common.cuh) and one broadcast input entry
+  const int slot = lane & 7, q = lane >> 3;
   const long band_stride = (long)D_.nc * D_.wmax;
   long long xwait = 0, t_sep = 0, t_pre = 0, t_xmv = 0, t_gw = 0, t_nw = 0, t_g = 0;
   long long tprof[4] = {0, 0, 0, 0};   // step sub-phases (thread 0): mat-vec, loads+reduce, writer, barrier
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   int pr_i = 0, pr_e = 0;
   auto produce_one = [&]() {
     if (pr_i >= nsolve) return;
-    const int w = tab[pr_i].w, pw = w * (w + 1) / 2;
+    const int pw = tab[pr_i].pks;
     const int ph = pr_e >= m ? 1 : 0, js = pr_e - ph * m;
     const bool up = (g == 0) == (ph == 0);
     const cplx* src = (g == 0 ? tab[pr_i].fac : tab[pr_i].fac2) + (long)(up ? lo + js : hi - js) * pw;
@@ -484,12 +489,12 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     // row `row`, k < row from row k (column `row`); others -> the zero entry
     uint32_t off[KPL];
     {
-      const int rs = row * w - (row * (row - 1)) / 2;
+      const int rs = act ? pkst[row] : 0;
 #pragma unroll
       for (int c = 0; c < KPL; ++c) {
         const int k = q + LPR * c;
         int idx = A.stage_elems - 1;
-        if (act && k < w) idx = k >= row ? rs + (k - row) : k * w - (k * (k - 1)) / 2 + (row - k);
+        if (act && k < w) idx = k >= row ? rs + (k - row) : pkst[k] + (row - k);
         off[c] = (uint32_t)idx * (uint32_t)sizeof(cplx);
       }
     }
@@ -510,8 +515,16 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         cplx vv[KPL], S[KPL];
 #pragma unroll
         for (int c = 0; c < KPL; ++c) {
+#ifdef HELM_DUAL_ABL_NOVIN
+          vv[c] = cmk(1e-3 * c, 0.0);     // ablation: no input-vector loads
+#else
           vv[c] = vin[q + LPR * c];       // entries k >= w of the input are zero-padded
+#endif
+#ifdef HELM_DUAL_ABL_CFREE
+          S[c] = lds128(sb + (uint32_t)((gtid * KPL + c) % 600) * 16u);   // ablation: conflict-free, wrong values
+#else
           S[c] = lds128(sb + off[c]);
+#endif
         }
 #pragma unroll
         for (int c = 0; c < KPL; ++c) {
@@ -522,19 +535,19 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         }
       }
       cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
       cplx o = acc;
       if (sub) o = act ? csub(yseg[ci * w + row], acc) : cmk(0, 0);
       cplx nb;
       if (high) {
-        nb.x = __shfl_down_sync(0xffffffffu, o.x, 4);
-        nb.y = __shfl_down_sync(0xffffffffu, o.y, 4);
+        nb.x = __shfl_down_sync(0xffffffffu, o.x, 1, 8);
+        nb.y = __shfl_down_sync(0xffffffffu, o.y, 1, 8);
       } else {
-        nb.x = __shfl_up_sync(0xffffffffu, o.x, 4);
-        nb.y = __shfl_up_sync(0xffffffffu, o.y, 4);
+        nb.x = __shfl_up_sync(0xffffffffu, o.x, 1, 8);
+        nb.y = __shfl_up_sync(0xffffffffu, o.y, 1, 8);
       }
       long long q2 = 0;
       if (A.prof && tid == 0) { q2 = clock64(); tprof[1] += q2 - q1; }
@@ -612,6 +625,14 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         vbuf[0 * 2 * WM + cur * WM + e] = bseg[e];                // chain A: b_lo
         vbuf[1 * 2 * WM + cur * WM + e] = bseg[(m - 1) * w + e];  // chain B: b_hi
       }
+      if (tid == 0 && (i == 0 || tab[i - 1].w != w)) {
+        for (int r = 0, x = 0; r < w; ++r) {   // padded packed row starts (common.cuh pk_start)
+          pkst[r] = x;
+          x += w - r;
+          const int want = (2 * (r + 1)) & 7;
+          while ((x & 7) != want) ++x;
+        }
+      }
       cbar();
       t_pre += clock64() - c0;
       run_phase(i, G_, I0{});
@@ -669,10 +690,9 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     ctas += h->P;
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
-  const long pwmax = (long)wmax * (wmax + 1) / 2;
-  const long stage_elems = (pwmax + 1 + 7) / 8 * 8;   // packed block + zero entry, 128-byte multiple
+  const long stage_elems = pk_size(wmax) + 8;   // padded packed block + a zero entry, 128-byte multiple
   size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * 2 * NST +
-                sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + 256;
+                sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * WM + 256;
   smem = (smem + 127) / 128 * 128 + sizeof(cplx) * 6 * vec_elems;
   if (smem > (size_t)kDualSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections

@@ -49,7 +49,7 @@ struct WarpTab {
   const cplx* fac;
   const cplx* fac2;
   const cplx* xinv;
-  int w, a, s, pad;
+  int w, a, s, pks;   // pks: entries per padded packed block (pk_size(w))
 };
 
 __device__ __forceinline__ uint64_t wl2_policy_last() {
@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(warpk::NTH, 1) k_sweep_warp(const __grid_const
     tab[i].w = D_.w[s];
     tab[i].a = D_.a[s];
     tab[i].s = s;
+    tab[i].pks = pk_size(D_.w[s]);
   }
   for (int e = tid; e < 4 * WM; e += blockDim.x) vbuf[e] = cmk(0, 0);   // padding stays finite
   // the zero entry after each ring stage (target of the out-of-range offsets)
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(warpk::NTH, 1) k_sweep_warp(const __grid_const
   int pr_i = 0, pr_e = 0;                  // producer cursor (solve, step within solve)
   auto produce_one = [&]() {
     if (pr_i >= nsolve) return;
-    const int w = tab[pr_i].w, pw = w * (w + 1) / 2;
+    const int pw = tab[pr_i].pks;
     const int ph = pr_e >= m ? 1 : 0, js = pr_e - ph * m;
     const bool up = (G == 0) == (ph == 0);
     const cplx* src = (G == 0 ? tab[pr_i].fac : tab[pr_i].fac2) + (long)(up ? lo + js : hi - js) * pw;
@@ -388,8 +389,7 @@ __global__ void __launch_bounds__(warpk::NTH, 1) k_sweep_warp(const __grid_const
         const int k = ga + 4 * c;
         int idx;
         if (r >= w || k >= w) idx = A.stage_elems - 1;
-        else if (k >= r) idx = r * w - (r * (r - 1)) / 2 + (k - r);
-        else idx = k * w - (k * (k - 1)) / 2 + (r - k);
+        else idx = pk_index(r, k, w);
         off[i][c] = (uint32_t)idx * (uint32_t)sizeof(cplx);
       }
     }
@@ -581,8 +581,7 @@ int sweep_apply_warp(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     ctas += h->P;
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
-  const long pwmax = (long)wmax * (wmax + 1) / 2;
-  const long stage_elems = (pwmax + 1 + 7) / 8 * 8;   // packed block + zero entry, 128-byte multiple
+  const long stage_elems = pk_size(wmax) + 8;   // padded packed block + a zero entry, 128-byte multiple
   size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * 2 * NST +
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(WarpTab) * nsolve_max + 256;
   smem = (smem + 127) / 128 * 128 + sizeof(cplx) * 6 * vec_elems;
