@@ -257,8 +257,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int par = i & 1, ppar = par ^ 1;
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
-    const cplx* cband = D_.cr + s * band_stride;
-    const cplx* nband = D_.ne + s * band_stride;
     if (p < P - 1 && tid < 32) {
       // stream this CTA's rows of the separator inverse (w x Kw, contiguous) into L2
       // while the all-gather completes; the mat-vec below then reads L2
@@ -268,10 +266,19 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
         dprefetch_l2(xp + o, (uint32_t)(bytes - o < 32768L ? bytes - o : 32768L), pol_first);
     }
+    // publish this segment's contributions to its two separator right-hand sides:
+    //   yb[0..w)   = U_{lo-1} x0_lo   (enters g_{p-1}),  yb[wmax..) = U_hi^T x0_hi  (enters g_p)
+    // with the staged couplings of rows lo-1 (bcr/bne row 0) and hi (row m)
     cplx* yb = D_.yb + par * exs + (long)p * 2 * D_.wmax;
     for (int e = tid; e < w; e += ncons) {
-      yb[e] = zlo[e];
-      yb[D_.wmax + e] = yseg[(m - 1) * w + e];
+      const cplx* xl = zlo;                       // x0_lo
+      const cplx* xh = yseg + (long)(m - 1) * w;  // x0_hi = y_hi
+      cplx tl = cmul(bcr[e], xl[e]);
+      if (e + 1 < w) cfma(tl, bne[e], xl[e + 1]);
+      cplx th = cmul(bcr[(long)m * w + e], xh[e]);
+      if (e >= 1) cfma(th, bne[(long)m * w + e - 1], xh[e - 1]);
+      yb[e] = tl;
+      yb[D_.wmax + e] = th;
     }
     // the source at the separator rows does not depend on the all-gather: stage it
     // now (fb is dead between the epilogue and phase 3)
@@ -319,43 +326,27 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     // g_k = b_{s_k} - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]  (all K separators)
     const cplx* ybp = D_.yb + par * exs;
-    // two elements per thread and pass, every load issued before the arithmetic
-    for (int e0 = tid; e0 < K * w; e0 += 2 * ncons) {
-      cplx cb[2][4], yv[2][4];
-      int kk[2], qv[2];
-      bool ok[2];
+    // g_k = b_{s_k} (+ corrections) - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]: the two
+    // products were formed by the owning segments; four elements per thread and pass
+    for (int e0 = tid; e0 < K * w; e0 += 4 * ncons) {
+      cplx th[4], tl[4];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int e = e0 + u * ncons;
-        ok[u] = e < K * w;
-        const int k = ok[u] ? e / w : 0, qq = ok[u] ? e - k * w : 0;
-        kk[u] = k;
-        qv[u] = qq;
-        const int hk = D_.seg_hi[k], sk = hk + 1;
-        const cplx* yh = ybp + (long)k * 2 * D_.wmax + D_.wmax;
-        const cplx* yl = ybp + (long)(k + 1) * 2 * D_.wmax;
-        const cplx z = cmk(0, 0);
-        cb[u][0] = __ldg(cband + (long)hk * D_.wmax + qq);
-        cb[u][1] = qq >= 1 ? __ldg(nband + (long)hk * D_.wmax + qq - 1) : z;
-        cb[u][2] = __ldg(cband + (long)sk * D_.wmax + qq);
-        cb[u][3] = qq + 1 < w ? __ldg(nband + (long)sk * D_.wmax + qq) : z;
-        yv[u][0] = ldcg(yh + qq);
-        yv[u][1] = qq >= 1 ? ldcg(yh + qq - 1) : z;
-        yv[u][2] = ldcg(yl + qq);
-        yv[u][3] = qq + 1 < w ? ldcg(yl + qq + 1) : z;
+        const bool ok = e < K * w;
+        const int k = ok ? e / w : 0, qq = ok ? e - k * w : 0;
+        th[u] = ok ? ldcg(ybp + (long)k * 2 * D_.wmax + D_.wmax + qq) : cmk(0, 0);
+        tl[u] = ok ? ldcg(ybp + (long)(k + 1) * 2 * D_.wmax + qq) : cmk(0, 0);
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!ok[u]) continue;
-        const int k = kk[u], qq = qv[u];
-        cplx v = gR[k * w + qq];
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * ncons;
+        if (e >= K * w) break;
+        const int k = e / w, qq = e - k * w;
+        cplx v = gR[e];
         if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
         if (bwd && qq == qn) v = cadd(v, cnv[k]);
-        cplx tt = cmul(cb[u][0], yv[u][0]);
-        cfma(tt, cb[u][1], yv[u][1]);
-        cfma(tt, cb[u][2], yv[u][2]);
-        cfma(tt, cb[u][3], yv[u][3]);
-        gsm[k * w + qq] = csub(v, tt);
+        gsm[e] = csub(csub(v, th[u]), tl[u]);
       }
     }
     cbar();
