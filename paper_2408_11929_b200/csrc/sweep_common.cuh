@@ -107,6 +107,14 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// 16-byte asynchronous global -> shared copies (LDGSTS); zfill: src-size 0 writes zeros
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool zfill = false) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+               "r"(zfill ? 0 : 16)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // 16-byte shared-memory load by byte address
 __device__ __forceinline__ cplx lds128(uint32_t addr) {
   cplx v;

@@ -226,26 +226,52 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction_aw(D_, tdst, at, wt, side, c, a, X);
     }
   };
-  // RHS of solve i (rows lo..hi) and the couplings of rows lo-1..hi
+  // Asynchronous staging (cp.async, 16 bytes per thread and element):
+  //  * the source rows lo..hi of solve i+1 go to bseg at the start of phase 3 of
+  //    solve i (bseg is only read in phase 1),
+  //  * the couplings of rows lo-1..hi go to bcr/bne at the start of the
+  //    pre-actions (free after phase 3), overlapping the epilogue,
+  //  * the source at the separator rows goes to fb (gR) at the start of phase 1.
+  auto stage_rhs_source = [&](int i) {
+    const int a = tab[i].a, w = tab[i].w;
+    for (int e = tid; e < m * w; e += ncons) {
+      const int cl = e / w, qq = e - cl * w;
+      cp_async16(bseg + e, D_.R + node_of(D_, a, lo + cl, qq));
+    }
+    cp_async_commit();
+  };
+  auto stage_bands = [&](int i) {
+    const int s = tab[i].s, w = tab[i].w;
+    const cplx* cband = D_.cr + s * band_stride;
+    const cplx* nband = D_.ne + s * band_stride;
+    for (int e = tid; e < (m + 1) * w; e += ncons) {
+      const int cl = e / w, qq = e - cl * w, c = lo - 1 + cl;
+      const long off = (long)(c >= 0 ? c : 0) * D_.wmax + qq;
+      cp_async16(bcr + e, cband + off, c < 0);
+      cp_async16(bne + e, nband + off, c < 0);
+    }
+    cp_async_commit();
+  };
+  auto stage_sep_source = [&](int i) {
+    const int a = tab[i].a, w = tab[i].w;
+    for (int e = tid; e < K * w; e += ncons) {
+      const int k = e / w, qq = e - k * w;
+      cp_async16(fb + e, D_.R + node_of(D_, a, D_.seg_hi[k] + 1, qq));
+    }
+    cp_async_commit();
+  };
+  // RHS of solve i (rows lo..hi): the staged source plus the transmission
+  // corrections on the interface columns (after cp.async.wait_all + barrier)
   auto seg_rhs = [&](int i) {
     const int st = step_of(D_, i);
     const bool bwd = is_bwd(D_, i);
-    const int s = tab[i].s, a = tab[i].a, w = tab[i].w;
+    const int w = tab[i].w;
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
-    const cplx* cband = D_.cr + s * band_stride;
-    const cplx* nband = D_.ne + s * band_stride;
-    for (int e = tid; e < m * w; e += ncons) {
-      int cl = e / w, qq = e % w, c = lo + cl;
-      cplx v = __ldg(D_.R + node_of(D_, a, c, qq));
-      if (st > 0 && qq == qp) v = cadd(v, D_.corr_prev[(long)st * D_.nc + c]);
-      if (bwd && qq == qn) v = cadd(v, D_.corr_next[c]);
-      bseg[cl * w + qq] = v;
-    }
-    for (int e = tid; e < (m + 1) * w; e += ncons) {
-      int cl = e / w, qq = e % w, c = lo - 1 + cl;
-      bcr[e] = c >= 0 ? __ldg(cband + (long)c * D_.wmax + qq) : cmk(0, 0);
-      bne[e] = c >= 0 ? __ldg(nband + (long)c * D_.wmax + qq) : cmk(0, 0);
+    for (int cl = tid; cl < m; cl += ncons) {
+      const int c = lo + cl;
+      if (st > 0) bseg[cl * w + qp] = cadd(bseg[cl * w + qp], ldcg(D_.corr_prev + (long)st * D_.nc + c));
+      if (bwd) bseg[cl * w + qn] = cadd(bseg[cl * w + qn], ldcg(D_.corr_next + c));
     }
   };
   // separator stage of solve i (after phase 1): all-gather of x0_lo / x0_hi, g,
@@ -280,13 +306,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       yb[e] = tl;
       yb[D_.wmax + e] = th;
     }
-    // the source at the separator rows does not depend on the all-gather: stage it
-    // now (fb is dead between the epilogue and phase 3)
+    // the source at the separator rows was staged into fb at the start of phase 1
     cplx* gR = fb;
-    for (int e = tid; e < K * w; e += ncons) {
-      const int k = e / w, qq = e - k * w;
-      gR[e] = __ldg(D_.R + node_of(D_, a, D_.seg_hi[k] + 1, qq));
-    }
+    cp_async_wait_all();
     cbar();
     const long long cw0 = clock64();
     if (tid == 0) {
@@ -606,10 +628,14 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       // ---- pre-actions: epilogue of the previous solve, RHS, phase-1 inputs
       long long c0 = clock64();
       cbar();
+      stage_bands(i);
+      if (i == 0) stage_rhs_source(0);   // later solves: staged during the previous phase 3
       if (i > 0) {
         seg_epilogue(i - 1);
         cbar();
       }
+      cp_async_wait_all();
+      cbar();
       seg_rhs(i);
       cbar();
       for (int e = tid; e < w; e += ncons) {
@@ -626,6 +652,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       }
       cbar();
       t_pre += clock64() - c0;
+      stage_sep_source(i);
       run_phase(i, G_, I0{});
       // ---- separator stage, phase-3 inputs
       c0 = clock64();
@@ -633,6 +660,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       seg_separators(i);
       cbar();
       t_sep += clock64() - c0;
+      if (i + 1 < nsolve) stage_rhs_source(i + 1);
       run_phase(i, G_, I1{});
     }
   };
