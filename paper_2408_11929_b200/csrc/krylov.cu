@@ -8,6 +8,7 @@
 // so reruns are bitwise reproducible.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <complex>
@@ -138,7 +139,7 @@ __global__ void k_axpy_sub(long n, const cplx* __restrict__ b, const cplx* __res
 // summed redundantly by every block, which saves the grid sync that would
 // broadcast the keep/drop decision.  ~5 grid syncs per column instead of ~10
 // launches and a host round trip per column.
-static constexpr int kOrthTile = 1024;
+static constexpr int kOrthTile = 512;
 static constexpr int kOrthThreads = 256;
 
 struct OrthArgs {
@@ -149,11 +150,13 @@ struct OrthArgs {
   cplx* part;       // nblk x S partial sums, S = (m + 1) * t
   cplx* out;        // [C1 m*t][C2 m*t][gram t*t][cv 2*t*t][nn t]  (host copy, one D2H)
   long rows;        // rows per block
+  long long* prof;  // optional phase clock stamps of block 0 (diagnostics, HELM_ORTH_PROF)
 };
 
 // One pass over this block's rows.  Optional update W[:, wc0+i] -= sum_j Vb[:, j] Cs[j*tc+i]
 // (i < tc); then optional projections outsm[j*tc+i] = sum conj(Vb[:, j]) W[:, wc0+i] (j < mcols)
 // and squared norms outsm[mcols*tc + q] = ||W[:, nc0+q]||^2 (q < nn).
+template <int TM>
 __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* outsm, const cplx* Vb, int mcols,
                           int wc0, int tc, bool upd, bool dots, int nc0, int nn, long r0, long r1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -164,14 +167,14 @@ __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* out
     const int rows = (int)min((long)kOrthTile, r1 - t0);
     for (int rr = threadIdx.x; rr < rows; rr += blockDim.x) {
       const long r = t0 + rr;
-      cplx w[kMaxT];
+      cplx w[TM];
 #pragma unroll
-      for (int i = 0; i < kMaxT; ++i)
+      for (int i = 0; i < TM; ++i)
         if (i < tc) w[i] = a.W[(long)(wc0 + i) * a.n + r];
       if (upd) {
-        cplx acc[kMaxT];
+        cplx acc[TM];
 #pragma unroll
-        for (int i = 0; i < kMaxT; ++i) acc[i] = cmk(0, 0);
+        for (int i = 0; i < TM; ++i) acc[i] = cmk(0, 0);
         int j = 0;
         for (; j + 8 <= mcols; j += 8) {   // eight independent loads in flight per thread
           cplx v[8];
@@ -180,33 +183,88 @@ __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* out
 #pragma unroll
           for (int u = 0; u < 8; ++u)
 #pragma unroll
-            for (int i = 0; i < kMaxT; ++i)
+            for (int i = 0; i < TM; ++i)
               if (i < tc) cfma(acc[i], v[u], Cs[(j + u) * tc + i]);
         }
         for (; j < mcols; ++j) {
           const cplx v = __ldcg(Vb + (long)j * a.n + r);
 #pragma unroll
-          for (int i = 0; i < kMaxT; ++i)
+          for (int i = 0; i < TM; ++i)
             if (i < tc) cfma(acc[i], v, Cs[j * tc + i]);
         }
 #pragma unroll
-        for (int i = 0; i < kMaxT; ++i)
+        for (int i = 0; i < TM; ++i)
           if (i < tc) {
             w[i] = csub(w[i], acc[i]);
             a.W[(long)(wc0 + i) * a.n + r] = w[i];
           }
       }
 #pragma unroll
-      for (int i = 0; i < kMaxT; ++i)
+      for (int i = 0; i < TM; ++i)
         if (i < tc) Wt[i * kOrthTile + rr] = w[i];
     }
     __syncthreads();
     const int jn = (dots ? mcols : 0) + nn;
-    for (int j = warp; j < jn; j += nw) {
-      const bool isdot = dots && j < mcols;
-      cplx acc[kMaxT];
+    // two projection columns per warp at a time (16 loads in flight per lane)
+    if (dots && tc == a.t) {
+      const int jd = mcols & ~1;
+      for (int j = 2 * warp; j < jd; j += 2 * nw) {
+        cplx acc0[TM], acc1[TM];
 #pragma unroll
-      for (int i = 0; i < kMaxT; ++i) acc[i] = cmk(0, 0);
+        for (int i = 0; i < TM; ++i) { acc0[i] = cmk(0, 0); acc1[i] = cmk(0, 0); }
+        const cplx* v0 = Vb + (long)j * a.n + t0;
+        const cplx* v1 = v0 + a.n;
+        int rr = lane;
+        for (; rr + 224 < rows; rr += 256) {
+          cplx x0[8], x1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) { x0[u] = __ldcg(v0 + rr + 32 * u); x1[u] = __ldcg(v1 + rr + 32 * u); }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+              if (i < tc) {
+                const cplx wv = Wt[i * kOrthTile + rr + 32 * u];
+                cfmaconj(acc0[i], x0[u], wv);
+                cfmaconj(acc1[i], x1[u], wv);
+              }
+        }
+        for (; rr < rows; rr += 32) {
+          const cplx y0 = __ldcg(v0 + rr), y1 = __ldcg(v1 + rr);
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+            if (i < tc) {
+              const cplx wv = Wt[i * kOrthTile + rr];
+              cfmaconj(acc0[i], y0, wv);
+              cfmaconj(acc1[i], y1, wv);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          if (i >= tc) break;
+          for (int off = 16; off > 0; off >>= 1) {
+            acc0[i].x += __shfl_xor_sync(0xffffffffu, acc0[i].x, off);
+            acc0[i].y += __shfl_xor_sync(0xffffffffu, acc0[i].y, off);
+            acc1[i].x += __shfl_xor_sync(0xffffffffu, acc1[i].x, off);
+            acc1[i].y += __shfl_xor_sync(0xffffffffu, acc1[i].y, off);
+          }
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+            if (i < tc) {
+              outsm[j * tc + i] = cadd(outsm[j * tc + i], acc0[i]);
+              outsm[(j + 1) * tc + i] = cadd(outsm[(j + 1) * tc + i], acc1[i]);
+            }
+        }
+      }
+    }
+    const int jstart = (dots && tc == a.t) ? (mcols & ~1) : 0;
+    for (int j = jstart + warp; j < jn; j += nw) {
+      const bool isdot = dots && j < mcols;
+      cplx acc[TM];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) acc[i] = cmk(0, 0);
       if (isdot) {
         const cplx* v = Vb + (long)j * a.n + t0;
         int rr = lane;
@@ -217,13 +275,13 @@ __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* out
 #pragma unroll
           for (int u = 0; u < 8; ++u)
 #pragma unroll
-            for (int i = 0; i < kMaxT; ++i)
+            for (int i = 0; i < TM; ++i)
               if (i < tc) cfmaconj(acc[i], vv[u], Wt[i * kOrthTile + rr + 32 * u]);
         }
         for (; rr < rows; rr += 32) {
           const cplx vv = __ldcg(v + rr);
 #pragma unroll
-          for (int i = 0; i < kMaxT; ++i)
+          for (int i = 0; i < TM; ++i)
             if (i < tc) cfmaconj(acc[i], vv, Wt[i * kOrthTile + rr]);
         }
       } else {
@@ -235,7 +293,7 @@ __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* out
       }
       const int na = isdot ? tc : 1;
 #pragma unroll
-      for (int i = 0; i < kMaxT; ++i) {
+      for (int i = 0; i < TM; ++i) {
         if (i >= na) break;
         for (int off = 16; off > 0; off >>= 1) {
           acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, off);
@@ -245,7 +303,7 @@ __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* out
       if (lane == 0) {
         if (isdot) {
 #pragma unroll
-          for (int i = 0; i < kMaxT; ++i)
+          for (int i = 0; i < TM; ++i)
             if (i < tc) outsm[j * tc + i] = cadd(outsm[j * tc + i], acc[i]);
         }
         else
@@ -260,24 +318,38 @@ __device__ void orth_pass(const OrthArgs& a, cplx* Wt, const cplx* Cs, cplx* out
 }
 
 // dst[e] = sum_b part[b][off + e] for e < count, fixed order over b (grid-strided)
-__device__ __forceinline__ void orth_reduce(const OrthArgs& a, int off, int count, cplx* dst) {
+// sum over the blocks' partials, one warp per element: lanes take blocks b = lane,
+// lane + 32, ... in order, then a fixed butterfly -- a fixed order, so the result
+// is bitwise reproducible (a serial sum over ~300 blocks per thread was ~40k cycles)
+__device__ __forceinline__ cplx warp_sum_partials(const OrthArgs& a, long idx) {
   const int S = (a.m + 1) * a.t;
-  const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x, gsz = (long)gridDim.x * blockDim.x;
-  for (long e = gtid; e < count; e += gsz) {
-    cplx acc = cmk(0, 0);
-    for (int b = 0; b < (int)gridDim.x; ++b) acc = cadd(acc, __ldcg(a.part + (long)b * S + off + e));
-    dst[e] = acc;
+  const int lane = threadIdx.x & 31;
+  cplx acc = cmk(0, 0);
+  for (int b = lane; b < (int)gridDim.x; b += 32) acc = cadd(acc, __ldcg(a.part + (long)b * S + idx));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  return acc;
+}
+
+// dst[e] = sum_b part[b][off + e] for e < count (warp per element, grid-strided)
+__device__ __forceinline__ void orth_reduce(const OrthArgs& a, int off, int count, cplx* dst) {
+  const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nwt = ((long)gridDim.x * blockDim.x) >> 5;
+  for (long e = gw; e < count; e += nwt) {
+    const cplx v = warp_sum_partials(a, off + e);
+    if ((threadIdx.x & 31) == 0) dst[e] = v;
   }
 }
 
 // every block: the same fixed-order sum of one norm partial (no broadcast sync needed)
 __device__ __forceinline__ double orth_norm2(const OrthArgs& a, int off) {
   __shared__ double s;
-  const int S = (a.m + 1) * a.t;
-  if (threadIdx.x == 0) {
-    double acc = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) acc += __ldcg(a.part + (long)b * S + off).x;
-    s = acc;
+  if (threadIdx.x < 32) {
+    const cplx v = warp_sum_partials(a, off);
+    if (threadIdx.x == 0) s = v.x;
   }
   __syncthreads();
   const double v = s;
@@ -285,7 +357,8 @@ __device__ __forceinline__ double orth_norm2(const OrthArgs& a, int off) {
   return v;
 }
 
-__global__ void __launch_bounds__(kOrthThreads) k_orth(OrthArgs a) {
+template <int TM>
+__global__ void __launch_bounds__(kOrthThreads, 2) k_orth(OrthArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ cplx osm[];
   const int m = a.m, t = a.t;
@@ -303,44 +376,53 @@ __global__ void __launch_bounds__(kOrthThreads) k_orth(OrthArgs a) {
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) Cs[e] = __ldcg(C + e);
     __syncthreads();
   };
+  const bool pr = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  if (pr) a.prof[0] = clock64();
   // C1 = V^H W and ||w_i||^2 (the Gram diagonal)
-  orth_pass(a, Wt, Cs, outsm, a.V, m, 0, t, false, true, 0, t, r0, r1);
+  orth_pass<TM>(a, Wt, Cs, outsm, a.V, m, 0, t, false, true, 0, t, r0, r1);
+  if (pr) a.prof[1] = clock64();
   grid.sync();
   orth_reduce(a, 0, m * t, C1);
   {
-    const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gtid < t) {
-      cplx acc = cmk(0, 0);
-      for (int b = 0; b < (int)gridDim.x; ++b) acc = cadd(acc, __ldcg(a.part + (long)b * (m + 1) * t + m * t + gtid));
-      gram[gtid * t + gtid] = acc;
+    // Gram diagonal: the t norm partials follow the m*t projections; the last t warps
+    const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long nwt = ((long)gridDim.x * blockDim.x) >> 5;
+    const long e = gw - (nwt - t);
+    if (e >= 0 && e < t) {
+      const cplx v = warp_sum_partials(a, (long)m * t + e);
+      if ((threadIdx.x & 31) == 0) gram[e * t + e] = v;
     }
   }
   grid.sync();
+  if (pr) a.prof[2] = clock64();
   // W -= V C1; C2 = V^H W
   load_C(C1, m * t);
-  orth_pass(a, Wt, Cs, outsm, a.V, m, 0, t, true, true, 0, 0, r0, r1);
+  orth_pass<TM>(a, Wt, Cs, outsm, a.V, m, 0, t, true, true, 0, 0, r0, r1);
+  if (pr) a.prof[3] = clock64();
   grid.sync();
   orth_reduce(a, 0, m * t, C2);
   grid.sync();
   // W -= V C2 and ||w_0||^2
+  if (pr) a.prof[4] = clock64();
   load_C(C2, m * t);
-  orth_pass(a, Wt, Cs, outsm, a.V, m, 0, t, true, false, 0, 1, r0, r1);
+  orth_pass<TM>(a, Wt, Cs, outsm, a.V, m, 0, t, true, false, 0, 1, r0, r1);
+  if (pr) a.prof[5] = clock64();
   for (int i = 0; i < t; ++i) {
     if (i > 0) {
       // pass 0: c = Vn[:, :i]^H w_i
-      orth_pass(a, Wt, Cs, outsm, Vn, i, i, 1, false, true, 0, 0, r0, r1);
+      orth_pass<TM>(a, Wt, Cs, outsm, Vn, i, i, 1, false, true, 0, 0, r0, r1);
       grid.sync();
       orth_reduce(a, 0, i, cv + (long)i * t);
       grid.sync();
       // pass 1: w_i -= Vn c; c' = Vn^H w_i
       load_C(cv + (long)i * t, i);
-      orth_pass(a, Wt, Cs, outsm, Vn, i, i, 1, true, true, 0, 0, r0, r1);
+      orth_pass<TM>(a, Wt, Cs, outsm, Vn, i, i, 1, true, true, 0, 0, r0, r1);
       grid.sync();
       orth_reduce(a, 0, i, cv + (long)t * t + (long)i * t);
       grid.sync();
       // w_i -= Vn c'; ||w_i||^2
       load_C(cv + (long)t * t + (long)i * t, i);
-      orth_pass(a, Wt, Cs, outsm, Vn, i, i, 1, true, false, i, 1, r0, r1);
+      orth_pass<TM>(a, Wt, Cs, outsm, Vn, i, i, 1, true, false, i, 1, r0, r1);
     }
     grid.sync();
     // keep iff ||w_i|| > 1e-10 ||A z_i|| (D10 step 5); gram[i] is visible after the syncs above
@@ -351,6 +433,7 @@ __global__ void __launch_bounds__(kOrthThreads) k_orth(OrthArgs a) {
     for (long r = r0 + threadIdx.x; r < r1; r += blockDim.x) Vn[(long)i * a.n + r] = cscale(a.W[(long)i * a.n + r], sc);
     grid.sync();
   }
+  if (pr) a.prof[6] = clock64();
 }
 
 namespace {
@@ -617,19 +700,36 @@ static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cuda
   if (!nsm) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_orth<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_orth<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_orth<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_orth<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
+  const void* kfun = t <= 1 ? (const void*)k_orth<1> : t <= 2 ? (const void*)k_orth<2>
+                   : t <= 4 ? (const void*)k_orth<4> : (const void*)k_orth<8>;
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_orth, kOrthThreads, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, kOrthThreads, smem);
   if (e != cudaSuccess || occ < 1) return 0;
   long nblk = std::min<long>((long)nsm * std::min(occ, 4), (n + kOrthThreads - 1) / kOrthThreads);
   if ((long)nblk * (m + 1) * t > ws->partial_cap) nblk = ws->partial_cap / ((long)(m + 1) * t);
   if (nblk < 1) return 0;
   OrthArgs a;
   a.n = n; a.V = V; a.m = m; a.t = t; a.W = W; a.part = ws->partial; a.out = ws->dsm;
+  static long long* prof = nullptr;
+  if (getenv("HELM_ORTH_PROF") && !prof) cudaMallocManaged((void**)&prof, 16 * sizeof(long long));
+  a.prof = prof;
+  if (prof) {
+    static int calls = 0;
+    if (calls++ > 0) {
+      cudaDeviceSynchronize();
+      fprintf(stderr, "[k_orth m=%d] C1 pass %lld, reduce %lld, update+C2 %lld, reduce %lld, update+norm %lld, intra %lld cycles\n", m,
+              prof[1] - prof[0], prof[2] - prof[1], prof[3] - prof[2], prof[4] - prof[3], prof[5] - prof[4],
+              prof[6] - prof[5]);
+    }
+  }
   a.rows = (n + nblk - 1) / nblk;
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel((const void*)k_orth, dim3((unsigned)nblk), dim3(kOrthThreads), args, smem, st);
+  e = cudaLaunchCooperativeKernel(kfun, dim3((unsigned)nblk), dim3(kOrthThreads), args, smem, st);
   if (e != cudaSuccess) {
     helm_set_error("mpgmres_solve: k_orth: %s", cudaGetErrorString(e));
     return -1;
