@@ -45,7 +45,7 @@ constexpr int OWN = 7;    // owned rows per warp (8 slots, 1 halo)
 constexpr int KPL = 9;    // complex entries per lane per block row (w <= 36)
 constexpr int WM = 40;    // vector stride
 constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
-constexpr int MAXT = 5 * 64;   // 2 groups of <= 5 warps (w <= 35)
+constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA producer warps
 }  // namespace dualk
 
 struct DualArgs {
@@ -122,8 +122,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 
   // ring stages first (TMA destinations, 128-byte aligned), then barriers, vectors
   cplx* ring = reinterpret_cast<cplx*>(smem_raw);                          // [2][NST][stage_elems]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 2L * NST * A.stage_elems);   // [2][NST]
-  cplx* vbuf = reinterpret_cast<cplx*>(full + 2 * NST);                    // [group][2][WM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 2L * NST * A.stage_elems);   // [2][NST] block landed
+  uint64_t* empty = full + 2 * NST;                                        // [2][NST] stage released
+  cplx* vbuf = reinterpret_cast<cplx*>(empty + 2 * NST);                   // [group][2][WM]
   cplx* xlo = vbuf + 4 * WM;                        // x_{p-1}
   cplx* xhi = xlo + WM;                             // x_p
   cplx* zlo = xhi + WM;                             // x0_lo (chain B phase 1)
@@ -156,13 +157,44 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // the zero entry after each ring stage (target of out-of-range lanes)
   for (int e = tid; e < 2 * NST; e += blockDim.x) ring[(long)e * A.stage_elems + A.stage_elems - 1] = cmk(0, 0);
   if (tid == 0) {
-    for (int e = 0; e < 2 * NST; ++e) mbar_init(&full[e], 1);
+    for (int e = 0; e < 2 * NST; ++e) {
+      mbar_init(&full[e], 1);
+      mbar_init(&empty[e], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
   const int m = hi - lo + 1;
   const int total = nsolve * 2 * m;      // block steps per chain
   __syncthreads();
+
+  if (tid >= ncons) {
+    // ============================================================ TMA producer warps
+    // warp ncons/32 + pg feeds chain pg: per solve, phase 0 then phase 1, m packed
+    // blocks each, NST stages ahead; a stage is refilled once the chain group has
+    // released it (empty barrier, arrived by the group after its step barrier)
+    const int pg = (tid - ncons) >> 5;
+    if ((tid & 31) == 0) {
+      const uint64_t polL = l2_policy_last(), polF = l2_policy_first();
+      uint32_t f = 0;
+      for (int i2 = 0; i2 < nsolve; ++i2) {
+        const int pw = tab[i2].pks;
+        const cplx* fbase = pg == 0 ? tab[i2].fac : tab[i2].fac2;
+        for (int e = 0; e < 2 * m; ++e, ++f) {
+          const int ph = e >= m ? 1 : 0, js = e - ph * m;
+          const bool up = (pg == 0) == (ph == 0);
+          const cplx* src = fbase + (long)(up ? lo + js : hi - js) * pw;
+          const int st = f % NST;
+          if (f >= (uint32_t)NST) mbar_wait(&empty[pg * NST + st], ((f / NST) - 1) & 1);
+          uint64_t* bar = &full[pg * NST + st];
+          const uint32_t bytes = (uint32_t)(pw * sizeof(cplx));
+          mbar_expect_tx(bar, bytes);
+          bulk_g2s_hint(ring + ((long)pg * NST + st) * A.stage_elems, src, bytes, bar, ph == 0 ? polL : polF);
+        }
+      }
+    }
+    return;
+  }
 
 
   const int g = tid >= gsz ? 1 : 0;       // chain group
@@ -460,26 +492,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // phase-3 chain), m block steps on solve i.  Factor blocks are loaded into
   // registers two steps ahead (per-lane packed offsets precomputed per phase),
   // the mode-specific writer is resolved at compile time.
-  // ---- TMA producer of this group's ring (thread gtid == 0): the block sequence
-  // of chain g is, per solve, phase 0 then phase 1, m blocks each
-  uint32_t fseq = 0, cseq = 0;          // blocks issued (producer) / consumed
-  int pr_i = 0, pr_e = 0;
-  auto produce_one = [&]() {
-    if (pr_i >= nsolve) return;
-    const int pw = tab[pr_i].pks;
-    const int ph = pr_e >= m ? 1 : 0, js = pr_e - ph * m;
-    const bool up = (g == 0) == (ph == 0);
-    const cplx* src = (g == 0 ? tab[pr_i].fac : tab[pr_i].fac2) + (long)(up ? lo + js : hi - js) * pw;
-    const int st = fseq % NST;
-    uint64_t* bar = &full[g * NST + st];
-    const uint32_t bytes = (uint32_t)(pw * sizeof(cplx));
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s_hint(ring + ((long)g * NST + st) * A.stage_elems, src, bytes, bar, ph == 0 ? pol_last : pol_first);
-    ++fseq;
-    if (++pr_e == 2 * m) { pr_e = 0; ++pr_i; }
-  };
-  if (gtid == 0)
-    for (int k = 0; k < NST - 1; ++k) produce_one();
+  uint32_t cseq = 0;   // blocks consumed by this chain group
   const uint32_t ring_base = smem_u32(ring + (long)g * NST * A.stage_elems);
   const uint32_t stage_bytes = (uint32_t)A.stage_elems * (uint32_t)sizeof(cplx);
 
@@ -514,7 +527,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     for (int js = 0; js < m; ++js) {
       long long q0 = 0;
       if (A.prof && tid == 0) q0 = clock64();
-      if (gtid == 0) produce_one();   // refill the stage consumed by the previous step
       const int st = cseq % NST;
       mbar_wait(&full[G * NST + st], (cseq / NST) & 1);
       ++cseq;
@@ -613,6 +625,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       long long q3 = 0;
       if (A.prof && tid == 0) { q3 = clock64(); tprof[2] += q3 - q2; }
       gbar();
+      if (gtid == 0) mbar_arrive(&empty[G * NST + st]);   // every lane of the group is done with the stage
       if (A.prof && tid == 0) tprof[3] += clock64() - q3;
       cur ^= 1;
     }
@@ -696,7 +709,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   }
   if (wmax > LPR * KPL || wmax > WM) return -1;
   const int nw = (wmax + OWN - 1) / OWN;
-  const int threads = 2 * nw * 32;
+  const int threads = 2 * nw * 32 + 64;   // two chain groups + two TMA producer warps
   if (threads > MAXT) return -1;
   long vec_elems = 0;
   int ctas = 0;
@@ -710,7 +723,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
   const long stage_elems = pk_size(wmax) + 8;   // padded packed block + a zero entry, 128-byte multiple
-  size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * 2 * NST +
+  size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * 4 * NST +
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * WM + 256;
   smem = (smem + 127) / 128 * 128 + sizeof(cplx) * 6 * vec_elems;
   if (smem > (size_t)kDualSmemMax) return -1;
