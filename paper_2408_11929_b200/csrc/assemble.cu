@@ -36,6 +36,20 @@ extern "C" const char* helm_strerror(int code) {
 }
 
 // ------------------------------------------------------------------ device memory
+// allocations and frees are ordered on a private non-blocking stream that carries no
+// other work: the synchronisation in helm_dev_alloc returns at once and never waits for
+// (or serialises with) kernels the caller runs on other streams -- e.g. the two axes'
+// sweep_setup calls running concurrently -- and memory freed by a destroyed handle is
+// reused by the next allocation without cross-stream ordering questions.  Handles must
+// be destroyed only after the work that uses them has completed (every ABI call that
+// launches work synchronises its stream before returning).
+static cudaStream_t g_alloc_stream = nullptr;
+static std::once_flag g_alloc_stream_ready;
+static cudaStream_t alloc_stream() {
+  std::call_once(g_alloc_stream_ready, []() { cudaStreamCreateWithFlags(&g_alloc_stream, cudaStreamNonBlocking); });
+  return g_alloc_stream;
+}
+
 cudaError_t helm_dev_alloc(void** p, size_t bytes) {
   static std::once_flag pool_ready;
   std::call_once(pool_ready, []() {
@@ -47,20 +61,14 @@ cudaError_t helm_dev_alloc(void** p, size_t bytes) {
     }
     cudaGetLastError();
   });
-  // allocations are ordered on a private non-blocking stream that carries no
-  // other work: the synchronisation returns at once and never waits for (or
-  // serialises with) kernels the caller runs on other streams -- e.g. the two
-  // axes' sweep_setup calls running concurrently
-  static cudaStream_t alloc_stream = nullptr;
-  static std::once_flag stream_ready;
-  std::call_once(stream_ready, []() { cudaStreamCreateWithFlags(&alloc_stream, cudaStreamNonBlocking); });
-  cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 16, alloc_stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(alloc_stream);
+  cudaStream_t as = alloc_stream();
+  cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 16, as);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(as);
   return e;
 }
 
 void helm_dev_free(void* p) {
-  if (p) cudaFreeAsync(p, 0);
+  if (p) cudaFreeAsync(p, alloc_stream());
 }
 
 // ------------------------------------------------------------------ staging
