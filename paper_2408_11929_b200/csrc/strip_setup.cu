@@ -246,6 +246,9 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
         a[jj] = cmul(v, dinv);
         sm.prow[2 * jj + h] = a[jj];
       }
+      // the pivot column is broadcast as 1 + 1/piv, so the generic update of the
+      // other rows, a_ik - f (1 + 1/piv) with f = a_ik, leaves -f/piv there
+      if (h == kh) sm.prow[k] = cmk(1.0 + dinv.x, dinv.y);
       used = true;
       kstep = k;
       if (h == 0) sm.pivrow[k] = p;
@@ -254,12 +257,12 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
     if (active && i != p) {
       const cplx f = akk;
 #pragma unroll
-      for (int jj = 0; jj < kRowHW; ++jj) {
+      for (int jj = 0; jj < kRowHW; ++jj) {   // a -= f r, four fused multiply-adds
         const cplx r = sm.prow[2 * jj + h];
-        cplx v = (h == kh && jj == kj) ? cmk(0.0, 0.0) : a[jj];
-        v.x -= f.x * r.x - f.y * r.y;
-        v.y -= f.x * r.y + f.y * r.x;
-        a[jj] = v;
+        a[jj].x = fma(-f.x, r.x, a[jj].x);
+        a[jj].x = fma(f.y, r.y, a[jj].x);
+        a[jj].y = fma(-f.x, r.y, a[jj].y);
+        a[jj].y = fma(-f.y, r.x, a[jj].y);
       }
     }
   }
