@@ -109,6 +109,40 @@ __device__ inline void blk_mm_tiled(cplx* C, int ldc, const cplx* A, int lda, bo
   __syncthreads();
 }
 
+// 2 x 2-tiled variant for large CTAs (324 tiles at w = 35)
+__device__ inline void blk_mm_tiled2(cplx* C, int ldc, const cplx* A, int lda, bool transA, const cplx* B, int ldb,
+                                     int w, double alpha, bool accumulate) {
+  const int nt = (w + 1) / 2;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+    const int i0 = (t / nt) * 2, j0 = (t % nt) * 2;
+    cplx acc[2][2] = {{cmk(0, 0), cmk(0, 0)}, {cmk(0, 0), cmk(0, 0)}};
+    for (int r = 0; r < w; ++r) {
+      cplx av[2], bv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = i0 + u, j = j0 + u;
+        av[u] = i < w ? (transA ? A[(long)r * lda + i] : A[(long)i * lda + r]) : cmk(0, 0);
+        bv[u] = j < w ? B[(long)r * ldb + j] : cmk(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) cfma(acc[u][v], av[u], bv[v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = i0 + u, j = j0 + v;
+        if (i < w && j < w) {
+          const cplx val = cscale(acc[u][v], alpha);
+          C[(long)i * ldc + j] = accumulate ? cadd(C[(long)i * ldc + j], val) : val;
+        }
+      }
+  }
+  __syncthreads();
+}
+
 __device__ inline void blk_copy(cplx* dst, const cplx* src, int w) {
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) dst[e] = src[e];
   __syncthreads();

@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "p1_entries.cuh"
+#include "sweep_common.cuh"
 
 static constexpr int kXinvMaxW = 36;   // explicit separator inverse for the register-streaming kernel
 
@@ -225,7 +226,7 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
     const unsigned key = (active && !used && h == kh) ? (unsigned)__double2hiint(mag) + 1u : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     const unsigned who = __ballot_sync(0xffffffffu, key == kmax);
-    if (lane == 0) { sm.redk[warp] = kmax; sm.redi[warp] = warp * 16 + ((__ffs(who) - 1) >> 1); }
+    if (lane == 0 && warp < kRowWarps) { sm.redk[warp] = kmax; sm.redi[warp] = warp * 16 + ((__ffs(who) - 1) >> 1); }
     __syncthreads();
     unsigned k0 = sm.redk[0];
     int p = sm.redi[0];
@@ -451,7 +452,12 @@ struct RedArgs {
 // separator block-Thomas is a chain).  Block inverses use the register-row
 // Gauss-Jordan of k_factor_rows; products use register-tiled smem matmuls.
 // Shared memory: RowSmem (static) + S, T1 (R_{k,k+1}), T2 (F_k) (dynamic).
-__global__ void __launch_bounds__(kRowThreads) k_reduced(RedArgs ra) {
+__device__ long long g_red_prof[8];   // diagnostics (HELM_SETUP_TIMING): block 0 sub-phase cycles
+
+// 384 threads: the register-row Gauss-Jordan uses the first 96 (the others only
+// join its barriers); the products, stencil applications and copies use all.
+static constexpr int kRedThreads = 384;
+__global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   __shared__ RowSmem sm;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = blockIdx.x;
@@ -460,48 +466,61 @@ __global__ void __launch_bounds__(kRowThreads) k_reduced(RedArgs ra) {
   cplx* S = reinterpret_cast<cplx*>(smem_raw);
   cplx* T1 = S + w2;   // R_{k-1,k} of the previous separator, then R_{k,k+1}
   cplx* T2 = T1 + w2;  // F_{k-1}, then F_k
-  cplx* Bh = T2 + w2;  // staged Sinv_{h_k}
-  cplx* Bl = Bh + w2;  // staged X_{k+1}[lo,lo]
-  cplx* Bx = Bl + w2;  // staged X_{k+1}[lo,hi]
-  cplx* bands = Bx + w2;   // cr, ne of rows h_k, s_k, h_{k+1}: [6][w]
+  // staged operands of separator k, double-buffered: [buf][Bh | Bl | Bx | bands(6w)]
+  cplx* stage0 = T2 + w2;
+  const long stage_sz = 3 * w2 + 6L * w;
   const long band = (long)s * ra.nc * ra.wmax;
   const cplx* fac = ra.fac + ra.fac_off[s];
   cplx* red = ra.red + ra.red_off[s];
   auto scr = [&](int p) { return ra.scratch + ((long)s * ra.P + p) * ra.scratch_stride; };
   const int P = ra.P;
   const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  // cp.async the operands of separator k into buffer k & 1: Sinv_{h_k}, X_{k+1}[lo,lo],
+  // X_{k+1}[lo,hi] and the couplings of rows h_k, s_k, h_{k+1}
+  auto stage = [&](int k) {
+    cplx* d = stage0 + (k & 1) * stage_sz;
+    const int hk = ra.seg_hi[k], sk = hk + 1, hk1 = ra.seg_hi[k + 1];
+    const cplx* g0 = fac + (long)hk * w2;
+    const cplx* g1 = scr(k + 1) + 2 * w2;
+    const cplx* g2 = scr(k + 1) + 3 * w2;
+    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+      cp_async16(d + e, g0 + e);
+      cp_async16(d + w2 + e, g1 + e);
+      cp_async16(d + 2 * w2 + e, g2 + e);
+    }
+    const int rows[3] = {hk, sk, hk1};
+    for (int e = threadIdx.x; e < 3 * w; e += blockDim.x) {
+      const int rr = e / w, q2 = e - rr * w;
+      cp_async16(d + 3 * w2 + (2 * rr) * w + q2, ra.cr + band + (long)rows[rr] * ra.wmax + q2);
+      cp_async16(d + 3 * w2 + (2 * rr + 1) * w + q2, ra.ne + band + (long)rows[rr] * ra.wmax + q2);
+    }
+    cp_async_commit();
+  };
+  stage(0);
   for (int k = 0; k <= P - 2; ++k) {
     const int hk = ra.seg_hi[k];          // last row of segment k
     const int sk = hk + 1;                // separator row
-    const int hk1 = ra.seg_hi[k + 1];     // last row of segment k+1
     cplx* Rinv = red + (long)k * 3 * w2;
     cplx* G = Rinv + w2;
     cplx* F = Rinv + 2 * w2;
-    // stage this separator's operands in shared memory (independent loads, one latency)
-    {
-      const cplx* g0 = fac + (long)hk * w2;
-      const cplx* g1 = scr(k + 1) + 2 * w2;
-      const cplx* g2 = scr(k + 1) + 3 * w2;
-      for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-        Bh[e] = __ldcg(g0 + e);
-        Bl[e] = __ldcg(g1 + e);
-        Bx[e] = __ldcg(g2 + e);
-      }
-      const int rows[3] = {hk, sk, hk1};
-      for (int e = threadIdx.x; e < 3 * w; e += blockDim.x) {
-        const int rr = e / w, q2 = e - rr * w;
-        bands[(2 * rr) * w + q2] = ra.cr[band + (long)rows[rr] * ra.wmax + q2];
-        bands[(2 * rr + 1) * w + q2] = ra.ne[band + (long)rows[rr] * ra.wmax + q2];
-      }
-      __syncthreads();
-    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (k + 1 <= P - 2) stage(k + 1);     // overlaps this separator's work
+    cplx* Bh = stage0 + (k & 1) * stage_sz;
+    cplx* Bl = Bh + w2;
+    cplx* Bx = Bl + w2;
+    cplx* bands = Bx + w2;
     auto Ub = [&](int rr, int mode) { return Bidi{mode, bands + (2 * rr) * w, bands + (2 * rr + 1) * w}; };
+    const bool pr = blockIdx.x == 0 && threadIdx.x == 0;
+    long long c0 = pr ? clock64() : 0;
     // R_kk = D_sk - U_hk^T X_k[hi,hi] U_hk - U_sk X_{k+1}[lo,lo] U_sk^T
     build_D(S, ra.dg + band + (long)sk * ra.wmax, ra.al + band + (long)sk * ra.wmax, w);
     blk_lxr(S, Bh, Ub(0, BD_UT), Ub(0, BD_U), w, -1.0, true);
     blk_lxr(S, Bl, Ub(1, BD_U), Ub(1, BD_UT), w, -1.0, true);
     // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
-    if (k >= 1) blk_mm_tiled(S, w, T1, w, true, T2, w, w, -1.0, true);
+    if (k >= 1) blk_mm_tiled2(S, w, T1, w, true, T2, w, w, -1.0, true);
+    long long c1 = pr ? clock64() : 0;
+    if (pr) g_red_prof[0] += c1 - c0;
     // Rinv_k (register-row Gauss-Jordan; result in sm.mat, row stride kRowW)
     cplx a[kRowHW];
 #pragma unroll
@@ -513,6 +532,8 @@ __global__ void __launch_bounds__(kRowThreads) k_reduced(RedArgs ra) {
       if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
       return;
     }
+    long long c2 = pr ? clock64() : 0;
+    if (pr) g_red_prof[1] += c2 - c1;
     row_store(Rinv, w, sm);
     if (k >= 1) {
       // G_k = Rinv_k R_{k,k-1} = Rinv_k R_{k-1,k}^T   (S <- T1^T; S is free now)
@@ -521,15 +542,16 @@ __global__ void __launch_bounds__(kRowThreads) k_reduced(RedArgs ra) {
         S[e] = T1[q2 * w + p2];
       }
       __syncthreads();
-      blk_mm_tiled(G, w, sm.mat, kRowW, false, S, w, w, 1.0, false);
+      blk_mm_tiled2(G, w, sm.mat, kRowW, false, S, w, w, 1.0, false);
     }
     if (k <= P - 3) {
       // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1};  F_k = Rinv_k R_{k,k+1}
       blk_lxr(T1, Bx, Ub(1, BD_U), Ub(2, BD_U), w, -1.0, false);
-      blk_mm_tiled(T2, w, sm.mat, kRowW, false, T1, w, w, 1.0, false);
+      blk_mm_tiled2(T2, w, sm.mat, kRowW, false, T1, w, w, 1.0, false);
       for (int e = threadIdx.x; e < w * w; e += blockDim.x) F[e] = T2[e];
     }
     __syncthreads();
+    if (pr) g_red_prof[2] += clock64() - c2;
   }
 }
 
@@ -599,7 +621,8 @@ __global__ void k_reduced_generic(RedArgs ra) {
 // (strip, column block j):  Z_j = Rinv_j E_j, Z_k = -G_k Z_{k-1} (k > j),
 // X_{K-1} = Z_{K-1}, X_k = Z_k - F_k X_{k+1}.  Storage per strip:
 // X[k] is w x (K w) row-major (the rows of separator k), contiguous.
-__global__ void __launch_bounds__(128) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = blockIdx.y, j = blockIdx.x;
   const int K = ra.P - 1;
@@ -608,39 +631,57 @@ __global__ void __launch_bounds__(128) k_reduced_inverse(RedArgs ra, cplx* xinv,
   const long w2 = (long)w * w, Kw = (long)K * w;
   const cplx* red = ra.red + ra.red_off[s];
   cplx* X = xinv + xinv_off[s];
-  cplx* cur = reinterpret_cast<cplx*>(smem_raw);   // w x w: column block j of Z_k / X_k
-  cplx* M = cur + w2;                               // w x w factor
-  cplx* nxt = M + w2;
+  // three rotating w x w column blocks (current X_k / Z_k, next, prefetch target)
+  // and a double-buffered factor block, all staged one step ahead with cp.async
+  cplx* vb[3] = {reinterpret_cast<cplx*>(smem_raw), reinterpret_cast<cplx*>(smem_raw) + w2,
+                 reinterpret_cast<cplx*>(smem_raw) + 2 * w2};
+  cplx* Mb = vb[2] + w2;
   auto blkX = [&](int k, int r, int c) -> cplx& { return X[(long)k * w * Kw + (long)r * Kw + (long)j * w + c]; };
-  // forward: rows k < j are zero; k = j: Rinv_j; k > j: -G_k Z_{k-1}
-  for (int k = 0; k < j; ++k)
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) blkX(k, e / w, e % w) = cmk(0, 0);
-  for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-    cur[e] = red[(long)j * 3 * w2 + e];
-    blkX(j, e / w, e % w) = cur[e];
-  }
-  __syncthreads();
-  for (int k = j + 1; k < K; ++k) {
-    const cplx* G = red + ((long)k * 3 + 1) * w2;
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) M[e] = G[e];
-    __syncthreads();
-    blk_mm_tiled(nxt, w, M, w, false, cur, w, w, -1.0, false);
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) blkX(k, e / w, e % w) = nxt[e];
-    cplx* t = cur; cur = nxt; nxt = t;
-    __syncthreads();
-  }
-  // backward: cur holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}
-  for (int k = K - 2; k >= 0; --k) {
-    const cplx* F = red + ((long)k * 3 + 2) * w2;
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-      M[e] = F[e];
-      nxt[e] = blkX(k, e / w, e % w);
+  auto mm = [&](cplx* C, const cplx* A, const cplx* B, bool acc) {
+    if (NT >= 256) blk_mm_tiled2(C, w, A, w, false, B, w, w, -1.0, acc);
+    else blk_mm_tiled(C, w, A, w, false, B, w, w, -1.0, acc);
+  };
+  auto stage_M = [&](int k, int which) {   // which = 1: G_k (forward), 2: F_k (backward)
+    const cplx* G = red + ((long)k * 3 + which) * w2;
+    cplx* d = Mb + (k & 1) * w2;
+    for (int e = threadIdx.x; e < w2; e += NT) cp_async16(d + e, G + e);
+  };
+  auto stage_Z = [&](int k, cplx* d) {
+    for (int e = threadIdx.x; e < w2; e += NT) {
+      const int r = e / w, c = e - r * w;
+      cp_async16(d + e, &blkX(k, r, c));
     }
+  };
+  // forward: rows k < j are zero; k = j: Rinv_j; k > j: Z_k = -G_k Z_{k-1}
+  if (j + 1 < K) { stage_M(j + 1, 1); cp_async_commit(); }
+  for (int k = 0; k < j; ++k)
+    for (int e = threadIdx.x; e < w2; e += NT) blkX(k, e / w, e % w) = cmk(0, 0);
+  int ic = 0;
+  for (int e = threadIdx.x; e < w2; e += NT) {
+    const cplx v = red[(long)j * 3 * w2 + e];
+    vb[0][e] = v;
+    blkX(j, e / w, e % w) = v;
+  }
+  for (int k = j + 1; k < K; ++k) {
+    cp_async_wait_all();
     __syncthreads();
-    blk_mm_tiled(nxt, w, M, w, false, cur, w, w, -1.0, true);
-    for (int e = threadIdx.x; e < w2; e += blockDim.x) blkX(k, e / w, e % w) = nxt[e];
-    cplx* t = cur; cur = nxt; nxt = t;
+    if (k + 1 < K) { stage_M(k + 1, 1); cp_async_commit(); }
+    cplx* nx = vb[(ic + 1) % 3];
+    mm(nx, Mb + (k & 1) * w2, vb[ic], false);
+    for (int e = threadIdx.x; e < w2; e += NT) blkX(k, e / w, e % w) = nx[e];
+    ic = (ic + 1) % 3;
+  }
+  // backward: vb[ic] holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}
+  __syncthreads();   // every thread's forward stores precede the read-back
+  if (K >= 2) { stage_M(K - 2, 2); stage_Z(K - 2, vb[(ic + 1) % 3]); cp_async_commit(); }
+  for (int k = K - 2; k >= 0; --k) {
+    cp_async_wait_all();
     __syncthreads();
+    cplx* z = vb[(ic + 1) % 3];
+    if (k >= 1) { stage_M(k - 1, 2); stage_Z(k - 1, vb[(ic + 2) % 3]); cp_async_commit(); }
+    mm(z, Mb + (k & 1) * w2, vb[ic], true);
+    for (int e = threadIdx.x; e < w2; e += NT) blkX(k, e / w, e % w) = z[e];
+    ic = (ic + 1) % 3;
   }
 }
 
@@ -869,9 +910,9 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
                h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
     if (wmax <= kRowW) {
-      const size_t smr = sizeof(cplx) * 6 * (size_t)wmax * wmax + sizeof(cplx) * 6 * wmax;
+      const size_t smr = sizeof(cplx) * (9 * (size_t)wmax * wmax + 12 * (size_t)wmax);
       cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-      k_reduced<<<n_strips, kRowThreads, smr, st>>>(ra);
+      k_reduced<<<n_strips, kRedThreads, smr, st>>>(ra);
     } else {
       k_reduced_generic<<<n_strips, threads, smem, st>>>(ra);
     }
@@ -882,9 +923,15 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       // explicit separator inverse rows for the register-streaming kernel
       const long tot = xinv_total;
       if (e == cudaSuccess) {
-        size_t sm3 = sizeof(cplx) * 3 * wmax * wmax;
-        cudaFuncSetAttribute(k_reduced_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-        k_reduced_inverse<<<dim3(P - 1, n_strips), 128, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
+        static const int ri_nt = getenv("HELM_RI_NT") ? atoi(getenv("HELM_RI_NT")) : 128;
+        if (ri_nt >= 256) {
+          cudaFuncSetAttribute(k_reduced_inverse<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+          k_reduced_inverse<256><<<dim3(P - 1, n_strips), 256, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        } else {
+          cudaFuncSetAttribute(k_reduced_inverse<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+          k_reduced_inverse<128><<<dim3(P - 1, n_strips), 128, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        }
         if (timing) cudaEventRecord(tev[4], st);
         g_helm_launches++;
         e = cudaGetLastError();
@@ -907,6 +954,13 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     if (P > 1 && want_xinv) cudaEventElapsedTime(&t4, tev[3], tev[4]);
     fprintf(stderr, "[sweep_setup] bands %.2f ms, segment factors %.2f ms, separator factors %.2f ms, separator inverse %.2f ms\n",
             t1, t2, t3, t4);
+    long long rp[8];
+    if (cudaMemcpyFromSymbol(rp, g_red_prof, sizeof(rp)) == cudaSuccess && P > 1) {
+      fprintf(stderr, "[k_reduced] per separator (block 0): build+RtF %lld, invert %lld, store+G+F %lld cycles\n",
+              rp[0] / (P - 1), rp[1] / (P - 1), rp[2] / (P - 1));
+      long long z[8] = {0};
+      cudaMemcpyToSymbol(g_red_prof, z, sizeof(z));
+    }
   }
   helm_dev_free(d_status);
   helm_dev_free(scratch);
