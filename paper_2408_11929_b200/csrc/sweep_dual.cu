@@ -39,6 +39,9 @@
 
 #include "sweep_common.cuh"
 
+#ifndef HELM_DUAL_SNPOS
+#define HELM_DUAL_SNPOS 1   // where the next block's entries are read (see step(); 1 = interleaved with the FMAs)
+#endif
 namespace dualk {
 constexpr int LPR = 4;    // lanes per block row
 constexpr int OWN = 7;    // owned rows per warp (8 slots, 1 halo)
@@ -47,6 +50,18 @@ constexpr int WM = 40;    // vector stride
 constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
 constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA producer warps
 }  // namespace dualk
+
+// per-CTA cycle counters (tools/prof_sweep.py) only in the -DHELM_DUAL_PROF build
+// (python -m paper_2408_11929_b200.build --prof): the counters cost registers
+#ifdef HELM_DUAL_PROF
+constexpr bool kProf = true;
+#else
+constexpr bool kProf = false;
+#endif
+__device__ __forceinline__ long long pclk() {
+  if constexpr (kProf) return clock64();
+  else return 0;
+}
 
 struct DualArgs {
   DirArgs d[HELM_MAXDIR];
@@ -196,7 +211,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     return;
   }
 
-
   const int g = tid >= gsz ? 1 : 0;       // chain group
   const int gtid = tid - g * gsz;
   const int wi = gtid >> 5, lane = tid & 31;
@@ -207,7 +221,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   const long band_stride = (long)D_.nc * D_.wmax;
   long long xwait = 0, t_sep = 0, t_pre = 0, t_xmv = 0, t_gw = 0, t_nw = 0, t_g = 0;
   long long tprof[4] = {0, 0, 0, 0};   // step sub-phases (thread 0): mat-vec, loads+reduce, writer, barrier
-  const long long t_start = clock64();
+  const long long t_start = pclk();
   auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
   auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory"); };
   const long exs = 2L * P * D_.wmax;   // parity stride of yb / xb
@@ -342,19 +356,21 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     cplx* gR = fb;
     cp_async_wait_all();
     cbar();
-    const long long cw0 = clock64();
+    const long long cw0 = pclk();
+    const bool need_corr = st > 0 || bwd;
     if (tid == 0) {
       __threadfence();
-      red_release_add(&D_.cnt[0], 1u);
-      while (ld_relaxed(&D_.cnt[0]) < (unsigned)(P * (i + 1))) __nanosleep(20);
-      (void)ld_acquire(&D_.cnt[0]);
+      red_release_add(&D_.cnt[0], 1u);   // arrive: this segment's yb is published
+      if (need_corr) {
+        // every segment has published solve i-1's boundary rows (epilogue counter),
+        // so the corrections can be formed while the slower segments finish phase 1
+        while (ld_relaxed(&D_.cnt[1]) < (unsigned)(P * i)) __nanosleep(20);
+        (void)ld_acquire(&D_.cnt[1]);
+      }
     }
     cbar();
-    xwait += clock64() - cw0;
-    t_gw += clock64() - cw0;
-    const long long cg0 = clock64();
     // separator-row transmission corrections (from solve i-1) for every separator
-    if (st > 0 || bwd) {
+    if (need_corr) {
       const int aprev = i > 0 ? tab[i - 1].a : 0;
       for (int k = tid; k < K; k += ncons) {
         const int sk = D_.seg_hi[k] + 1;
@@ -376,8 +392,17 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         cpv[k] = cp;
         cnv[k] = cn;
       }
-      cbar();
     }
+    if (tid == 0) {
+#ifndef HELM_DUAL_ABL_NOGW
+      while (ld_relaxed(&D_.cnt[0]) < (unsigned)(P * (i + 1))) __nanosleep(20);
+#endif
+      (void)ld_acquire(&D_.cnt[0]);
+    }
+    cbar();
+    xwait += pclk() - cw0;
+    t_gw += pclk() - cw0;
+    const long long cg0 = pclk();
     // g_k = b_{s_k} - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]  (all K separators)
     const cplx* ybp = D_.yb + par * exs;
     // g_k = b_{s_k} (+ corrections) - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]: the two
@@ -405,11 +430,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     cbar();
     // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
-    const long long cx0 = clock64();
+    const long long cx0 = pclk();
     t_g += cx0 - cg0;
     const long Kw = (long)K * w;
     const int cw = tid >> 5, ncw = ncons >> 5;
+#ifdef HELM_DUAL_ABL_NOXMV
+    if (false) {
+#else
     if (p < P - 1) {
+#endif
       for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
         const cplx* Xr[4];
         bool ok[4];
@@ -449,7 +478,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (p == P - 1) xhi[e] = cmk(0, 0);
     }
     cbar();
-    t_xmv += clock64() - cx0;
+    t_xmv += pclk() - cx0;
     // publish x_p (parity buffer; also the next solve's correction source),
     // then take x_{p-1} from the left neighbour
     if (p < P - 1) {
@@ -461,14 +490,14 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       }
     }
     if (p > 0) {
-      const long long cw1 = clock64();
+      const long long cw1 = pclk();
       if (tid == 0) {
         while (ld_relaxed(&D_.flag[p - 1]) < (unsigned)(i + 1)) __nanosleep(20);
         (void)ld_acquire(&D_.flag[p - 1]);
       }
       cbar();
-      xwait += clock64() - cw1;
-      t_nw += clock64() - cw1;
+      xwait += pclk() - cw1;
+      t_nw += pclk() - cw1;
       for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D_.xs + par * xss + (long)(p - 1) * D_.wmax + e);
       cbar();
     }
@@ -524,48 +553,90 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         off[c] = (uint32_t)idx * (uint32_t)sizeof(cplx);
       }
     }
-    for (int js = 0; js < m; ++js) {
-      long long q0 = 0;
-      if (A.prof && tid == 0) q0 = clock64();
-      const int st = cseq % NST;
-      mbar_wait(&full[G * NST + st], (cseq / NST) & 1);
-      ++cseq;
+    // this lane's nine entries of the block consumed as sequence number `seq`
+    auto load_S = [&](cplx (&S)[KPL], uint32_t seq) {
+      const int st = seq % NST;
+      mbar_wait(&full[G * NST + st], (seq / NST) & 1);
       const uint32_t sb = ring_base + st * stage_bytes;
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+#if defined(HELM_DUAL_ABL_CFREE)
+        S[c] = lds128(sb + (uint32_t)((gtid * KPL + c) % 600) * 16u);   // ablation: conflict-free, wrong values
+#elif defined(HELM_DUAL_ABL_NOS)
+        S[c] = cmk(1e-3 * c + 1e-4 * (sb & 7), 1e-3);                    // ablation: no block loads
+#else
+        S[c] = lds128(sb + off[c]);
+#endif
+      }
+    };
+    // one block step with this block's entries in Sc; the next block's entries are
+    // read into Sn while the reductions, the writer and the barrier of this step
+    // run, so only the input-vector loads sit on the dependent path
+    auto step = [&](int js, cplx (&Sc)[KPL], cplx (&Sn)[KPL]) {
+      long long q0 = 0;
+      if (kProf && A.prof && tid == 0) q0 = pclk();
+      const int st = cseq % NST;
       const int ci = up ? js : m - 1 - js;   // local block row
+      const bool last = js == m - 1;
       const cplx* vin = myv + cur * WM;
-      long long q1 = 0;
-      if (A.prof && tid == 0) { q1 = clock64(); tprof[0] += q1 - q0; }
-      cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
-      {
-        cplx vv[KPL], S[KPL];
+      // writer operands (independent of this step's result): couplings of the
+      // next input and, for the sweeps that subtract, the source row
+      constexpr bool cplus = (G == 0 && PH == 0) || (G == 1 && PH == 1);   // A1, B3: row ci+1 of the staged bands
+      cplx wc = cmk(0, 0), wn = cmk(0, 0), wb = cmk(0, 0), ysub = cmk(0, 0);
+      if (owned && !last) {
+        const int crow = cplus ? ci + 1 : ci;
+        wc = bcr[crow * w + row];
+        if (cplus) { if (row >= 1) wn = bne[crow * w + row - 1]; }
+        else if (row + 1 < w) wn = bne[crow * w + row];
+        if (G == 0 && PH == 0) wb = bseg[(ci + 1) * w + row];
+        if (G == 1 && PH == 0) wb = bseg[(ci - 1) * w + row];
+      }
+      if (sub && act) ysub = yseg[ci * w + row];
+      cplx vv[KPL];
 #pragma unroll
-        for (int c = 0; c < KPL; ++c) {
+      for (int c = 0; c < KPL; ++c) {
 #ifdef HELM_DUAL_ABL_NOVIN
-          vv[c] = cmk(1e-3 * c, 0.0);     // ablation: no input-vector loads
+        vv[c] = cmk(1e-3 * c, 0.0);     // ablation: no input-vector loads
 #else
-          vv[c] = vin[q + LPR * c];       // entries k >= w of the input are zero-padded
+        vv[c] = vin[q + LPR * c];       // entries k >= w of the input are zero-padded
 #endif
-#ifdef HELM_DUAL_ABL_CFREE
-          S[c] = lds128(sb + (uint32_t)((gtid * KPL + c) % 600) * 16u);   // ablation: conflict-free, wrong values
-#else
-          S[c] = lds128(sb + off[c]);
+      }
+      long long q1 = 0;
+      if (kProf && A.prof && tid == 0) { q1 = pclk(); tprof[0] += q1 - q0; }
+      cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
+#if HELM_DUAL_SNPOS == 1
+      // next block: wait for it, then read each entry right after its register pair is consumed
+      uint32_t sbn = 0;
+      if (!last) {
+        const int stn = (cseq + 1) % NST;
+        mbar_wait(&full[G * NST + stn], ((cseq + 1) / NST) & 1);
+        sbn = ring_base + stn * stage_bytes;
+      }
+#elif HELM_DUAL_SNPOS == 2
+      if (!last) load_S(Sn, cseq + 1);
 #endif
-        }
 #pragma unroll
-        for (int c = 0; c < KPL; ++c) {
-          if ((c & 3) == 0) cfma(a0, S[c], vv[c]);
-          else if ((c & 3) == 1) cfma(a1, S[c], vv[c]);
-          else if ((c & 3) == 2) cfma(a2, S[c], vv[c]);
-          else cfma(a3, S[c], vv[c]);
-        }
+      for (int c = 0; c < KPL; ++c) {
+        if ((c & 3) == 0) cfma(a0, Sc[c], vv[c]);
+        else if ((c & 3) == 1) cfma(a1, Sc[c], vv[c]);
+        else if ((c & 3) == 2) cfma(a2, Sc[c], vv[c]);
+        else cfma(a3, Sc[c], vv[c]);
+#if HELM_DUAL_SNPOS == 1
+        if (!last) Sn[c] = lds128(sbn + off[c]);
+#endif
       }
       cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
+#if HELM_DUAL_SNPOS == 0
+      if (!last) load_S(Sn, cseq + 1);   // Sc is dead: Sn can take its registers
+#endif
+#ifndef HELM_DUAL_ABL_NOSHFL
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+#endif
       cplx o = acc;
-      if (sub) o = act ? csub(yseg[ci * w + row], acc) : cmk(0, 0);
+      if (sub) o = act ? csub(ysub, acc) : cmk(0, 0);
       cplx nb;
       if (high) {
         nb.x = __shfl_down_sync(0xffffffffu, o.x, 1, 8);
@@ -575,60 +646,39 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         nb.y = __shfl_up_sync(0xffffffffu, o.y, 1, 8);
       }
       long long q2 = 0;
-      if (A.prof && tid == 0) { q2 = clock64(); tprof[1] += q2 - q1; }
+      if (kProf && A.prof && tid == 0) { q2 = pclk(); tprof[1] += q2 - q1; }
       if (owned) {
         cplx* vn = myv + (cur ^ 1) * WM;
-        const bool last = js == m - 1;
-        if (G == 0 && PH == 0) {
-          // A1: y_c; next input b_{c+1} - U_c^T y_c
-          yseg[ci * w + row] = o;
-          if (!last) {
-            const cplx* cr = bcr + (long)(ci + 1) * w;
-            const cplx* ne = bne + (long)(ci + 1) * w;
-            cplx v = csub(bseg[(ci + 1) * w + row], cmul(cr[row], o));
-            if (row >= 1) v = csub(v, cmul(ne[row - 1], nb));
-            vn[row] = v;
-          }
-        } else if (G == 0) {
-          // A3: xa_c; next input U_{c-1} xa_c
-          xa[ci * w + row] = o;
-          if (!last) {
-            const cplx* cr = bcr + (long)ci * w;
-            const cplx* ne = bne + (long)ci * w;
-            cplx v = cmul(cr[row], o);
-            if (row + 1 < w) cfma(v, ne[row], nb);
-            vn[row] = v;
-          }
-        } else if (PH == 0) {
-          // B1: z_c; next input b_{c-1} - U_{c-1} z_c; z_lo = x0_lo
-          if (last) {
-            zlo[row] = o;
-          } else {
-            const cplx* cr = bcr + (long)ci * w;
-            const cplx* ne = bne + (long)ci * w;
-            cplx v = cmul(cr[row], o);
-            if (row + 1 < w) cfma(v, ne[row], nb);
-            vn[row] = csub(bseg[(ci - 1) * w + row], v);
-          }
-        } else {
-          // B3: f_c; next input -U_c^T f_c
-          fb[ci * w + row] = o;
-          if (!last) {
-            const cplx* cr = bcr + (long)(ci + 1) * w;
-            const cplx* ne = bne + (long)(ci + 1) * w;
-            cplx v = cmul(cr[row], o);
-            if (row >= 1) cfma(v, ne[row - 1], nb);
-            vn[row] = cscale(v, -1.0);
-          }
+        if (G == 0 && PH == 0) yseg[ci * w + row] = o;          // A1: y_c; next b_{c+1} - U_c^T y_c
+        else if (G == 0) xa[ci * w + row] = o;                  // A3: xa_c; next U_{c-1} xa_c
+        else if (PH == 1) fb[ci * w + row] = o;                 // B3: f_c; next -U_c^T f_c
+        else if (last) zlo[row] = o;                            // B1: z_lo = x0_lo
+        if (!last) {                                            // B1: next b_{c-1} - U_{c-1} z_c
+          cplx t = cmul(wc, o);
+          cfma(t, wn, nb);
+          if (PH == 0) vn[row] = csub(wb, t);
+          else vn[row] = G == 0 ? t : cscale(t, -1.0);
         }
       }
+#if HELM_DUAL_SNPOS == 3
+      if (!last) load_S(Sn, cseq + 1);
+#endif
       long long q3 = 0;
-      if (A.prof && tid == 0) { q3 = clock64(); tprof[2] += q3 - q2; }
+      if (kProf && A.prof && tid == 0) { q3 = pclk(); tprof[2] += q3 - q2; }
       gbar();
       if (gtid == 0) mbar_arrive(&empty[G * NST + st]);   // every lane of the group is done with the stage
-      if (A.prof && tid == 0) tprof[3] += clock64() - q3;
+      if (kProf && A.prof && tid == 0) tprof[3] += pclk() - q3;
+      ++cseq;
       cur ^= 1;
+    };
+    cplx SA[KPL], SB[KPL];
+    load_S(SA, cseq);
+    int js = 0;
+    for (; js + 1 < m; js += 2) {
+      step(js, SA, SB);
+      step(js + 1, SB, SA);
     }
+    if (js < m) step(js, SA, SB);
   };
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
@@ -639,13 +689,16 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     for (int i = 0; i < nsolve; ++i) {
       const int w = tab[i].w;
       // ---- pre-actions: epilogue of the previous solve, RHS, phase-1 inputs
-      long long c0 = clock64();
+      long long c0 = pclk();
       cbar();
       stage_bands(i);
       if (i == 0) stage_rhs_source(0);   // later solves: staged during the previous phase 3
       if (i > 0) {
         seg_epilogue(i - 1);
         cbar();
+        // epilogue counter: solve i-1's boundary rows (xb) and separators (xs) are
+        // published; the separator stage of solve i forms its corrections from them
+        if (tid == 0) red_release_add(&D_.cnt[1], 1u);
       }
       cp_async_wait_all();
       cbar();
@@ -664,15 +717,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         }
       }
       cbar();
-      t_pre += clock64() - c0;
+      t_pre += pclk() - c0;
       stage_sep_source(i);
       run_phase(i, G_, I0{});
       // ---- separator stage, phase-3 inputs
-      c0 = clock64();
+      c0 = pclk();
       cbar();
       seg_separators(i);
       cbar();
-      t_sep += clock64() - c0;
+      t_sep += pclk() - c0;
       if (i + 1 < nsolve) stage_rhs_source(i + 1);
       run_phase(i, G_, I1{});
     }
@@ -681,10 +734,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   else solve_loop(I1{});
   cbar();
   seg_epilogue(nsolve - 1);
-  if (A.prof && tid == 0) {
+  if (kProf && A.prof && tid == 0) {
     long long* o = A.prof + (long)blockIdx.x * 16;
     o[0] = t_pre; o[1] = t_sep; o[2] = t_xmv; o[3] = total; o[4] = xwait;
-    o[5] = clock64() - t_start; o[6] = 1; o[7] = d;
+    o[5] = pclk() - t_start; o[6] = 1; o[7] = d;
     for (int k = 0; k < 4; ++k) o[8 + k] = tprof[k];
     o[12] = t_gw; o[13] = t_nw; o[14] = t_g;
   }
