@@ -42,6 +42,9 @@
 #ifndef HELM_DUAL_SNPOS
 #define HELM_DUAL_SNPOS 1   // where the next block's entries are read (see step(); 1 = interleaved with the FMAs)
 #endif
+#ifndef HELM_DUAL_RHS_TMA
+#define HELM_DUAL_RHS_TMA 0   // stage the next RHS by bulk copies (1) or per-element cp.async (0)
+#endif
 namespace dualk {
 constexpr int LPR = 4;    // lanes per block row
 constexpr int OWN = 7;    // owned rows per warp (8 slots, 1 halo)
@@ -52,11 +55,17 @@ constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA 
 }  // namespace dualk
 
 // per-CTA cycle counters (tools/prof_sweep.py) only in the -DHELM_DUAL_PROF build
-// (python -m paper_2408_11929_b200.build --prof): the counters cost registers
+// (python -m paper_2408_11929_b200.build --prof); the per-step sub-phase counters
+// (-DHELM_DUAL_PROF_STEP) keep clock values live across the step and spill
 #ifdef HELM_DUAL_PROF
 constexpr bool kProf = true;
 #else
 constexpr bool kProf = false;
+#endif
+#ifdef HELM_DUAL_PROF_STEP
+constexpr bool kProfStep = kProf;
+#else
+constexpr bool kProfStep = false;
 #endif
 __device__ __forceinline__ long long pclk() {
   if constexpr (kProf) return clock64();
@@ -71,6 +80,7 @@ struct DualArgs {
   int nsolve_max;
   int pmax;
   int stage_elems;  // cplx per ring stage (>= largest packed block + 1 zero entry)
+  int mmax;         // largest segment (rows)
   long long* prof;  // optional per-CTA counters (16 per CTA)
 };
 
@@ -139,7 +149,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* ring = reinterpret_cast<cplx*>(smem_raw);                          // [2][NST][stage_elems]
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + 2L * NST * A.stage_elems);   // [2][NST] block landed
   uint64_t* empty = full + 2 * NST;                                        // [2][NST] stage released
-  cplx* vbuf = reinterpret_cast<cplx*>(empty + 2 * NST);                   // [group][2][WM]
+  // staging barriers (bulk copies, complete_tx): [0] inputs of the next solve, staged
+  // during phase 3; [1] the couplings of the current solve; [2] the first RHS
+  uint64_t* sbar = empty + 2 * NST;
+  cplx* vbuf = reinterpret_cast<cplx*>(sbar + 4);                         // [group][2][WM]
   cplx* xlo = vbuf + 4 * WM;                        // x_{p-1}
   cplx* xhi = xlo + WM;                             // x_p
   cplx* zlo = xhi + WM;                             // x0_lo (chain B phase 1)
@@ -147,15 +160,19 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* cnv = cpv + A.pmax;                         // [pmax] next-side separator corrections
   DualTab* tab = reinterpret_cast<DualTab*>(cnv + A.pmax);
   int* pkst = reinterpret_cast<int*>(tab + A.nsolve_max);   // [WM] padded row starts of the current w
+  int* sepr = pkst + WM;                                     // [pmax] separator rows s_k
   cplx* vec0 = reinterpret_cast<cplx*>(
-      smem_raw + ((((char*)(pkst + WM) - (char*)smem_raw) + 127) / 128) * 128);
-  cplx* bseg = vec0;                                // RHS rows lo..hi
+      smem_raw + ((((char*)(sepr + A.pmax) - (char*)smem_raw) + 127) / 128) * 128);
+  cplx* bseg = vec0;                                // RHS rows lo..hi, entry (cl, q) at cl * bsc + q * bsq
   cplx* yseg = bseg + A.vec_elems;                  // chain A phase 1 (y)
   cplx* xa = yseg + A.vec_elems;                    // chain A phase 3 (aliased by g in the separator stage)
   cplx* fb = xa + A.vec_elems;                      // chain B phase 3
-  cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi
+  cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi (row stride wmax)
   cplx* bne = bcr + A.vec_elems;
   cplx* gsm = xa;                                   // separator RHS g (K x w), dead before phase 3
+  cplx* cs = bne + A.vec_elems;                     // [mmax] corrections formed by the last epilogue (next RHS)
+  cplx* cps = cs + A.mmax;                          // [mmax] forward-pass corr_prev rows (backward RHS), staged
+  cplx* tcs = cps + A.mmax;                         // [5 mmax] transmission coefficients of the next epilogue, staged
 
   const int nsolve = n_solves(D_);
   for (int i = tid; i < nsolve; i += blockDim.x) {
@@ -176,10 +193,18 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       mbar_init(&full[e], 1);
       mbar_init(&empty[e], 1);
     }
+    for (int e = 0; e < 3; ++e) mbar_init(&sbar[e], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
   const int m = hi - lo + 1;
+  const int bw = D_.wmax;                         // band row stride in bcr / bne
+  // RHS layout: rows (x axis: a row of the strip is contiguous in the grid) or
+  // columns (y axis: a line of the strip is contiguous), odd column stride
+  const int bsq = D_.axis == 0 ? 1 : (m | 1);
+  for (int k = tid; k < K; k += blockDim.x) sepr[k] = D_.seg_hi[k] + 1;
+  if (lo == 0)
+    for (int e = tid; e < bw; e += blockDim.x) bcr[e] = bne[e] = cmk(0, 0);   // row -1 (never staged)
   const int total = nsolve * 2 * m;      // block steps per chain
   __syncthreads();
 
@@ -219,8 +244,18 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // the padded packed layout, common.cuh) and one broadcast input entry
   const int slot = lane & 7, q = lane >> 3;
   const long band_stride = (long)D_.nc * D_.wmax;
-  long long xwait = 0, t_sep = 0, t_pre = 0, t_xmv = 0, t_gw = 0, t_nw = 0, t_g = 0;
-  long long tprof[4] = {0, 0, 0, 0};   // step sub-phases (thread 0): mat-vec, loads+reduce, writer, barrier
+  // cycle counters of thread 0 (prof build only), kept in shared memory so that
+  // they cost no registers: [0] pre-actions [1] separator stage [2] X mat-vec
+  // [4] waits [8..11] step sub-phases (mat-vec, loads+reduce, writer, barrier)
+  // [12] gather wait [13] neighbour wait [14] corrections + g
+  __shared__ long long profs[16];
+  auto pacc = [&](int k, long long v) {
+    if constexpr (kProf) {
+      if (tid == 0) profs[k] += v;
+    }
+  };
+  if (kProf && tid == 0)
+    for (int k = 0; k < 16; ++k) profs[k] = 0;
   const long long t_start = pclk();
   auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
   auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory"); };
@@ -232,6 +267,20 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   int cur = 0;
 
   // ------------------------------------------------------------ per-solve actions (all consumers)
+  // the transmission correction the epilogue of solve i forms for solve i + 1:
+  // destination strip, its side and the global buffer (none after the last solve)
+  auto epi_target = [&](int i, int& tdst, int& side, cplx*& target) {
+    const int st = step_of(D_, i);
+    tdst = -1;
+    side = 0;
+    target = nullptr;
+    if (!is_bwd(D_, i)) {
+      if (st < D_.N - 1) { tdst = sigma(D_, st + 1); side = prev_side(D_); target = D_.corr_prev + (long)(st + 1) * D_.nc; }
+      else if (D_.is_double && D_.N > 1) { tdst = sigma(D_, D_.N - 2); side = next_side(D_); target = D_.corr_next; }
+    } else if (st >= 1) {
+      tdst = sigma(D_, st - 1); side = next_side(D_); target = D_.corr_next;
+    }
+  };
   // epilogue of solve i: x = xa + fb gathered into Z, boundary rows published, next correction
   auto seg_epilogue = [&](int i) {
     const int st = step_of(D_, i);
@@ -254,12 +303,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     int tdst = -1, side = 0;
     cplx* target = nullptr;
-    if (!bwd) {
-      if (st < D_.N - 1) { tdst = sigma(D_, st + 1); side = prev_side(D_); target = D_.corr_prev + (long)(st + 1) * D_.nc; }
-      else if (D_.is_double && D_.N > 1) { tdst = sigma(D_, D_.N - 2); side = next_side(D_); target = D_.corr_next; }
-    } else if (st >= 1) {
-      tdst = sigma(D_, st - 1); side = next_side(D_); target = D_.corr_next;
-    }
+    epi_target(i, tdst, side, target);
     if (tdst >= 0) {
       auto X = [&](int cc, int qq) -> cplx {
         if (cc < lo) return xlo[qq];
@@ -269,42 +313,105 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       // the destination strip is the one solve i + 1 works on
       const int at = i + 1 < nsolve ? tab[i + 1].a : D_.a[tdst];
       const int wt = i + 1 < nsolve ? tab[i + 1].w : D_.w[tdst];
-      for (int c = lo + tid; c <= hi; c += ncons) target[c] = correction_aw(D_, tdst, at, wt, side, c, a, X);
+      const int bt = at + wt - 1;
+      const int qi = side == 0 ? at - a : bt - a, qo = side == 0 ? at - 1 - a : bt + 1 - a;
+      const int dd = side == 0 ? -1 : 1;
+      for (int c = lo + tid; c <= hi; c += ncons) {
+        // D8 stencil with the coefficients staged in tcs (sweep_common.cuh correction_aw)
+        const cplx* kk = tcs + (c - lo) * 5;
+        const bool h4 = c + dd >= 0 && c + dd < D_.nc;
+        cplx v = cmul(kk[1], X(c, qi));
+        cfma(v, kk[3], X(c, qo));
+        if (c >= 1) cfma(v, kk[0], X(c - 1, qi));
+        if (c + 1 < D_.nc) cfma(v, kk[2], X(c + 1, qi));
+        if (h4) cfma(v, kk[4], X(c + dd, qo));
+        target[c] = v;
+        cs[c - lo] = v;
+      }
     }
   };
-  // Asynchronous staging (cp.async, 16 bytes per thread and element):
+  // Staging by bulk copies (TMA, mbarrier complete_tx), issued by the lanes of warp 0:
   //  * the source rows lo..hi of solve i+1 go to bseg at the start of phase 3 of
-  //    solve i (bseg is only read in phase 1),
+  //    solve i (bseg is only read in phase 1), with the coefficients of epilogue
+  //    i's correction and, for a backward solve i+1, its forward-pass corr_prev rows
+  //    (barrier sbar[0], waited at the pre-actions of solve i+1);
   //  * the couplings of rows lo-1..hi go to bcr/bne at the start of the
-  //    pre-actions (free after phase 3), overlapping the epilogue,
-  //  * the source at the separator rows goes to fb (gR) at the start of phase 1.
-  auto stage_rhs_source = [&](int i) {
-    const int a = tab[i].a, w = tab[i].w;
-    for (int e = tid; e < m * w; e += ncons) {
-      const int cl = e / w, qq = e - cl * w;
-      cp_async16(bseg + e, D_.R + node_of(D_, a, lo + cl, qq));
+  //    pre-actions (free after phase 3), overlapping the epilogue (sbar[1]).
+  // The copies replace per-element cp.async, whose LSU traffic competed with the
+  // block steps running at the same time.
+  auto issue_copies = [&](int ncp, auto desc, uint64_t* bar) {
+    // desc(j, dst, src, bytes) describes copy j; lane 0 arms the barrier with the total
+    if (tid < 32) {
+      uint32_t tot = 0;
+      for (int j = 0; j < ncp; ++j) {
+        cplx* dd;
+        const cplx* sr;
+        uint32_t by;
+        desc(j, dd, sr, by);
+        tot += by;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic accesses of the targets
+      if (tid == 0) mbar_expect_tx(bar, tot);
+      __syncwarp();
+      for (int j = tid; j < ncp; j += 32) {
+        cplx* dd;
+        const cplx* sr;
+        uint32_t by;
+        desc(j, dd, sr, by);
+        if (by) bulk_g2s_hint(dd, sr, by, bar, pol_first);
+      }
     }
-    cp_async_commit();
+  };
+  auto rhs_copy = [&](int i, int j, cplx*& dd, const cplx*& sr, uint32_t& by) {
+    const int a = tab[i].a, w = tab[i].w;
+    if (D_.axis == 0) { dd = bseg + (long)j * w; sr = D_.R + node_of(D_, a, lo + j, 0); by = (uint32_t)(w * sizeof(cplx)); }
+    else { dd = bseg + (long)j * bsq; sr = D_.R + node_of(D_, a, lo, j); by = (uint32_t)(m * sizeof(cplx)); }
+  };
+  auto stage_rhs0 = [&]() {
+    const int nr = D_.axis == 0 ? m : tab[0].w;
+    issue_copies(nr, [&](int j, cplx*& dd, const cplx*& sr, uint32_t& by) { rhs_copy(0, j, dd, sr, by); }, &sbar[2]);
+  };
+  auto stage_next = [&](int i) {
+    int tdst, side;
+    cplx* target;
+    epi_target(i, tdst, side, target);
+    const bool rhs = i + 1 < nsolve;
+    const bool cpb = rhs && is_bwd(D_, i + 1) && step_of(D_, i + 1) > 0;
+#if HELM_DUAL_RHS_TMA
+    const int nr = !rhs ? 0 : (D_.axis == 0 ? m : tab[i + 1].w);
+#else
+    // the source rows: per-element cp.async by all consumers (bulk copies of the
+    // m rows / w lines queue in front of the factor stream in the TMA unit)
+    const int nr = 0;
+    if (rhs) {
+      const int a1 = tab[i + 1].a, w1 = tab[i + 1].w;
+      for (int e = tid; e < m * w1; e += ncons) {
+        const int cl = e / w1, qq = e - cl * w1;
+        cp_async16(bseg + (D_.axis == 0 ? cl * w1 + qq : qq * bsq + cl), D_.R + node_of(D_, a1, lo + cl, qq));
+      }
+      cp_async_commit();
+    }
+#endif
+    issue_copies(nr + 2, [&](int j, cplx*& dd, const cplx*& sr, uint32_t& by) {
+      if (j < nr) { rhs_copy(i + 1, j, dd, sr, by); return; }
+      dd = j == nr ? tcs : cps;
+      sr = j == nr ? D_.tc + (((long)(tdst < 0 ? 0 : tdst) * 2 + side) * D_.nc + lo) * 5
+                   : D_.corr_prev + (long)step_of(D_, i + 1 < nsolve ? i + 1 : i) * D_.nc + lo;
+      by = j == nr ? (tdst >= 0 ? (uint32_t)(5 * m * sizeof(cplx)) : 0u) : (cpb ? (uint32_t)(m * sizeof(cplx)) : 0u);
+    }, &sbar[0]);
   };
   auto stage_bands = [&](int i) {
-    const int s = tab[i].s, w = tab[i].w;
-    const cplx* cband = D_.cr + s * band_stride;
-    const cplx* nband = D_.ne + s * band_stride;
-    for (int e = tid; e < (m + 1) * w; e += ncons) {
-      const int cl = e / w, qq = e - cl * w, c = lo - 1 + cl;
-      const long off = (long)(c >= 0 ? c : 0) * D_.wmax + qq;
-      cp_async16(bcr + e, cband + off, c < 0);
-      cp_async16(bne + e, nband + off, c < 0);
-    }
-    cp_async_commit();
-  };
-  auto stage_sep_source = [&](int i) {
-    const int a = tab[i].a, w = tab[i].w;
-    for (int e = tid; e < K * w; e += ncons) {
-      const int k = e / w, qq = e - k * w;
-      cp_async16(fb + e, D_.R + node_of(D_, a, D_.seg_hi[k] + 1, qq));
-    }
-    cp_async_commit();
+    const int s = tab[i].s;
+    const int c0 = lo > 0 ? lo - 1 : 0;
+    const long off = (long)s * band_stride + (long)c0 * bw;
+    const uint32_t by = (uint32_t)((hi - c0 + 1) * bw * sizeof(cplx));
+    cplx* d0 = lo > 0 ? bcr : bcr + bw;
+    cplx* d1 = lo > 0 ? bne : bne + bw;
+    issue_copies(2, [&](int j, cplx*& dd, const cplx*& sr, uint32_t& b2) {
+      dd = j == 0 ? d0 : d1;
+      sr = (j == 0 ? D_.cr : D_.ne) + off;
+      b2 = by;
+    }, &sbar[1]);
   };
   // RHS of solve i (rows lo..hi): the staged source plus the transmission
   // corrections on the interface columns (after cp.async.wait_all + barrier)
@@ -315,9 +422,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     for (int cl = tid; cl < m; cl += ncons) {
-      const int c = lo + cl;
-      if (st > 0) bseg[cl * w + qp] = cadd(bseg[cl * w + qp], ldcg(D_.corr_prev + (long)st * D_.nc + c));
-      if (bwd) bseg[cl * w + qn] = cadd(bseg[cl * w + qn], ldcg(D_.corr_next + c));
+      // corrections of the previous epilogue (cs) and, backward, the forward pass's (cps)
+      const int bsc = D_.axis == 0 ? w : 1;
+      if (st > 0) bseg[cl * bsc + qp * bsq] = cadd(bseg[cl * bsc + qp * bsq], bwd ? cps[cl] : cs[cl]);
+      if (bwd) bseg[cl * bsc + qn * bsq] = cadd(bseg[cl * bsc + qn * bsq], cs[cl]);
     }
   };
   // separator stage of solve i (after phase 1): all-gather of x0_lo / x0_hi, g,
@@ -347,14 +455,11 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       const cplx* xh = yseg + (long)(m - 1) * w;  // x0_hi = y_hi
       cplx tl = cmul(bcr[e], xl[e]);
       if (e + 1 < w) cfma(tl, bne[e], xl[e + 1]);
-      cplx th = cmul(bcr[(long)m * w + e], xh[e]);
-      if (e >= 1) cfma(th, bne[(long)m * w + e - 1], xh[e - 1]);
+      cplx th = cmul(bcr[(long)m * bw + e], xh[e]);
+      if (e >= 1) cfma(th, bne[(long)m * bw + e - 1], xh[e - 1]);
       yb[e] = tl;
       yb[D_.wmax + e] = th;
     }
-    // the source at the separator rows was staged into fb at the start of phase 1
-    cplx* gR = fb;
-    cp_async_wait_all();
     cbar();
     const long long cw0 = pclk();
     const bool need_corr = st > 0 || bwd;
@@ -373,7 +478,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     if (need_corr) {
       const int aprev = i > 0 ? tab[i - 1].a : 0;
       for (int k = tid; k < K; k += ncons) {
-        const int sk = D_.seg_hi[k] + 1;
+        const int sk = sepr[k];
         auto X = [&](int cc, int qq) -> cplx {
           if (cc == sk) return ldcg(D_.xs + ppar * xss + (long)k * D_.wmax + qq);
           if (cc == sk - 1) return ldcg(D_.xb + ppar * exs + (long)k * 2 * D_.wmax + D_.wmax + qq);
@@ -400,15 +505,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       (void)ld_acquire(&D_.cnt[0]);
     }
     cbar();
-    xwait += pclk() - cw0;
-    t_gw += pclk() - cw0;
+    pacc(4, pclk() - cw0);
+    pacc(12, pclk() - cw0);
     const long long cg0 = pclk();
     // g_k = b_{s_k} - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]  (all K separators)
     const cplx* ybp = D_.yb + par * exs;
     // g_k = b_{s_k} (+ corrections) - U_{h_k}^T x0_k[hi] - U_{s_k} x0_{k+1}[lo]: the two
     // products were formed by the owning segments; four elements per thread and pass
     for (int e0 = tid; e0 < K * w; e0 += 4 * ncons) {
-      cplx th[4], tl[4];
+      cplx th[4], tl[4], gs[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int e = e0 + u * ncons;
@@ -416,13 +521,14 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         const int k = ok ? e / w : 0, qq = ok ? e - k * w : 0;
         th[u] = ok ? ldcg(ybp + (long)k * 2 * D_.wmax + D_.wmax + qq) : cmk(0, 0);
         tl[u] = ok ? ldcg(ybp + (long)(k + 1) * 2 * D_.wmax + qq) : cmk(0, 0);
+        gs[u] = ok ? ldcg(D_.R + node_of(D_, a, sepr[k], qq)) : cmk(0, 0);   // source at the separator rows
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int e = e0 + u * ncons;
         if (e >= K * w) break;
         const int k = e / w, qq = e - k * w;
-        cplx v = gR[e];
+        cplx v = gs[u];
         if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
         if (bwd && qq == qn) v = cadd(v, cnv[k]);
         gsm[e] = csub(csub(v, th[u]), tl[u]);
@@ -431,7 +537,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     cbar();
     // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
     const long long cx0 = pclk();
-    t_g += cx0 - cg0;
+    pacc(14, cx0 - cg0);
     const long Kw = (long)K * w;
     const int cw = tid >> 5, ncw = ncons >> 5;
 #ifdef HELM_DUAL_ABL_NOXMV
@@ -478,7 +584,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (p == P - 1) xhi[e] = cmk(0, 0);
     }
     cbar();
-    t_xmv += pclk() - cx0;
+    pacc(2, pclk() - cx0);
     // publish x_p (parity buffer; also the next solve's correction source),
     // then take x_{p-1} from the left neighbour
     if (p < P - 1) {
@@ -496,8 +602,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         (void)ld_acquire(&D_.flag[p - 1]);
       }
       cbar();
-      xwait += pclk() - cw1;
-      t_nw += pclk() - cw1;
+      pacc(4, pclk() - cw1);
+      pacc(13, pclk() - cw1);
       for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D_.xs + par * xss + (long)(p - 1) * D_.wmax + e);
       cbar();
     }
@@ -505,8 +611,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     cplx* vA = vbuf + 0 * 2 * WM + cur * WM;
     cplx* vB = vbuf + 1 * 2 * WM + cur * WM;
     for (int qq = tid; qq < w; qq += ncons) {
-      const cplx* crr = bcr + (long)m * w;      // row hi
-      const cplx* ner = bne + (long)m * w;
+      const cplx* crr = bcr + (long)m * bw;     // row hi
+      const cplx* ner = bne + (long)m * bw;
       cplx ta = cmul(crr[qq], xhi[qq]);
       if (qq + 1 < w) cfma(ta, ner[qq], xhi[qq + 1]);
       vA[qq] = ta;
@@ -537,6 +643,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     constexpr int high = up ? 0 : 1;             // lo -> hi steps need o[r-1]: low-halo mapping
     constexpr bool sub = G == 0 && PH == 1;      // chain A back substitution: o = y_c - Sinv v
     const int w = tab[i].w;
+    const int bsc = D_.axis == 0 ? w : 1;
     const int row = dslot_row(wi, slot, high);
     const bool act = row >= 0 && row < w;
     const bool owned = q == 0 && act && dslot_owned(slot, high);
@@ -574,7 +681,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     // run, so only the input-vector loads sit on the dependent path
     auto step = [&](int js, cplx (&Sc)[KPL], cplx (&Sn)[KPL]) {
       long long q0 = 0;
-      if (kProf && A.prof && tid == 0) q0 = pclk();
+      if (kProfStep && A.prof && tid == 0) q0 = pclk();
       const int st = cseq % NST;
       const int ci = up ? js : m - 1 - js;   // local block row
       const bool last = js == m - 1;
@@ -585,11 +692,11 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       cplx wc = cmk(0, 0), wn = cmk(0, 0), wb = cmk(0, 0), ysub = cmk(0, 0);
       if (owned && !last) {
         const int crow = cplus ? ci + 1 : ci;
-        wc = bcr[crow * w + row];
-        if (cplus) { if (row >= 1) wn = bne[crow * w + row - 1]; }
-        else if (row + 1 < w) wn = bne[crow * w + row];
-        if (G == 0 && PH == 0) wb = bseg[(ci + 1) * w + row];
-        if (G == 1 && PH == 0) wb = bseg[(ci - 1) * w + row];
+        wc = bcr[crow * bw + row];
+        if (cplus) { if (row >= 1) wn = bne[crow * bw + row - 1]; }
+        else if (row + 1 < w) wn = bne[crow * bw + row];
+        if (G == 0 && PH == 0) wb = bseg[(ci + 1) * bsc + row * bsq];
+        if (G == 1 && PH == 0) wb = bseg[(ci - 1) * bsc + row * bsq];
       }
       if (sub && act) ysub = yseg[ci * w + row];
       cplx vv[KPL];
@@ -602,7 +709,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
       }
       long long q1 = 0;
-      if (kProf && A.prof && tid == 0) { q1 = pclk(); tprof[0] += q1 - q0; }
+      if (kProfStep && A.prof && tid == 0) { q1 = pclk(); pacc(8, q1 - q0); }
       cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
 #if HELM_DUAL_SNPOS == 1
       // next block: wait for it, then read each entry right after its register pair is consumed
@@ -646,7 +753,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         nb.y = __shfl_up_sync(0xffffffffu, o.y, 1, 8);
       }
       long long q2 = 0;
-      if (kProf && A.prof && tid == 0) { q2 = pclk(); tprof[1] += q2 - q1; }
+      if (kProfStep && A.prof && tid == 0) { q2 = pclk(); pacc(9, q2 - q1); }
       if (owned) {
         cplx* vn = myv + (cur ^ 1) * WM;
         if (G == 0 && PH == 0) yseg[ci * w + row] = o;          // A1: y_c; next b_{c+1} - U_c^T y_c
@@ -664,10 +771,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (!last) load_S(Sn, cseq + 1);
 #endif
       long long q3 = 0;
-      if (kProf && A.prof && tid == 0) { q3 = pclk(); tprof[2] += q3 - q2; }
+      if (kProfStep && A.prof && tid == 0) { q3 = pclk(); pacc(10, q3 - q2); }
       gbar();
       if (gtid == 0) mbar_arrive(&empty[G * NST + st]);   // every lane of the group is done with the stage
-      if (kProf && A.prof && tid == 0) tprof[3] += pclk() - q3;
+      if (kProfStep && A.prof && tid == 0) pacc(11, pclk() - q3);
       ++cseq;
       cur ^= 1;
     };
@@ -692,21 +799,26 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       long long c0 = pclk();
       cbar();
       stage_bands(i);
-      if (i == 0) stage_rhs_source(0);   // later solves: staged during the previous phase 3
-      if (i > 0) {
+      if (i == 0) {
+        stage_rhs0();
+        mbar_wait(&sbar[2], 0);
+      } else {
+        mbar_wait(&sbar[0], (i - 1) & 1);   // staged during phase 3 of solve i-1
+        cp_async_wait_all();
         seg_epilogue(i - 1);
         cbar();
         // epilogue counter: solve i-1's boundary rows (xb) and separators (xs) are
         // published; the separator stage of solve i forms its corrections from them
         if (tid == 0) red_release_add(&D_.cnt[1], 1u);
       }
-      cp_async_wait_all();
+      mbar_wait(&sbar[1], i & 1);
       cbar();
       seg_rhs(i);
       cbar();
       for (int e = tid; e < w; e += ncons) {
-        vbuf[0 * 2 * WM + cur * WM + e] = bseg[e];                // chain A: b_lo
-        vbuf[1 * 2 * WM + cur * WM + e] = bseg[(m - 1) * w + e];  // chain B: b_hi
+        const int bsc = D_.axis == 0 ? w : 1;
+        vbuf[0 * 2 * WM + cur * WM + e] = bseg[e * bsq];                  // chain A: b_lo
+        vbuf[1 * 2 * WM + cur * WM + e] = bseg[(m - 1) * bsc + e * bsq];  // chain B: b_hi
       }
       if (tid == 0 && (i == 0 || tab[i - 1].w != w)) {
         for (int r = 0, x = 0; r < w; ++r) {   // padded packed row starts (common.cuh pk_start)
@@ -717,29 +829,32 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         }
       }
       cbar();
-      t_pre += pclk() - c0;
-      stage_sep_source(i);
+      pacc(0, pclk() - c0);
       run_phase(i, G_, I0{});
       // ---- separator stage, phase-3 inputs
       c0 = pclk();
       cbar();
       seg_separators(i);
       cbar();
-      t_sep += pclk() - c0;
-      if (i + 1 < nsolve) stage_rhs_source(i + 1);
+      pacc(1, pclk() - c0);
+#ifndef HELM_DUAL_ABL_NONEXT
+      stage_next(i);
+#else
+      if (tid == 0) mbar_expect_tx(&sbar[0], 0);
+#endif
       run_phase(i, G_, I1{});
     }
   };
   if (g == 0) solve_loop(I0{});
   else solve_loop(I1{});
   cbar();
+  mbar_wait(&sbar[0], (nsolve - 1) & 1);
   seg_epilogue(nsolve - 1);
   if (kProf && A.prof && tid == 0) {
     long long* o = A.prof + (long)blockIdx.x * 16;
-    o[0] = t_pre; o[1] = t_sep; o[2] = t_xmv; o[3] = total; o[4] = xwait;
+    for (int k = 0; k < 16; ++k) o[k] = profs[k];
+    o[3] = total;
     o[5] = pclk() - t_start; o[6] = 1; o[7] = d;
-    for (int k = 0; k < 4; ++k) o[8 + k] = tprof[k];
-    o[12] = t_gw; o[13] = t_nw; o[14] = t_g;
   }
 }
 
@@ -765,20 +880,21 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   const int threads = 2 * nw * 32 + 64;   // two chain groups + two TMA producer warps
   if (threads > MAXT) return -1;
   long vec_elems = 0;
-  int ctas = 0;
+  int ctas = 0, mmax_all = 1;
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     int mmax = 0;
     for (int p = 0; p < h->P; ++p) mmax = std::max(mmax, h->seg_hi[p] - h->seg_lo[p] + 1);
     vec_elems = std::max(vec_elems, (long)(mmax + 1) * h->wmax);
+    mmax_all = std::max(mmax_all, mmax);
     vec_elems = std::max(vec_elems, (long)(h->P - 1) * h->wmax);
     ctas += h->P;
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
   const long stage_elems = pk_size(wmax) + 8;   // padded packed block + a zero entry, 128-byte multiple
-  size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * 4 * NST +
-                sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * WM + 256;
-  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * 6 * vec_elems;
+  size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * (4 * NST + 4) +
+                sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * (WM + pmax) + 256;
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + 7L * mmax_all);
   if (smem > (size_t)kDualSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
   std::vector<size_t> off(t);
@@ -808,6 +924,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   A.nsolve_max = nsolve_max;
   A.pmax = pmax;
   A.stage_elems = (int)stage_elems;
+  A.mmax = mmax_all;
   A.prof = helm_sweep_prof_buffer();
   int base = 0;
   for (int d = 0; d < t; ++d) {
