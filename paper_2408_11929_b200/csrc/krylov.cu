@@ -139,8 +139,10 @@ __global__ void k_axpy_sub(long n, const cplx* __restrict__ b, const cplx* __res
 // summed redundantly by every block, which saves the grid sync that would
 // broadcast the keep/drop decision.  ~5 grid syncs per column instead of ~10
 // launches and a host round trip per column.
-static constexpr int kOrthTile = 512;
+static constexpr int kOrthTile = 1024;
 static constexpr int kOrthThreads = 256;
+static constexpr int kIntraNV = 2 * 8 + 1;     // intra-block partial values per block (t <= 8)
+static constexpr long kIntraMaxBlk = 1024;     // blocks the intra-block partial region covers
 
 struct OrthArgs {
   long n;
@@ -151,6 +153,7 @@ struct OrthArgs {
   cplx* out;        // [C1 m*t][C2 m*t][gram t*t][cv 2*t*t][nn t]  (host copy, one D2H)
   long rows;        // rows per block
   long long* prof;  // optional phase clock stamps of block 0 (diagnostics, HELM_ORTH_PROF)
+  cplx* ipart;      // [2][nblk][kIntraNV] intra-block partials, alternating per pass
 };
 
 // One pass over this block's rows.  Optional update W[:, wc0+i] -= sum_j Vb[:, j] Cs[j*tc+i]
@@ -357,6 +360,127 @@ __device__ __forceinline__ double orth_norm2(const OrthArgs& a, int off) {
   return v;
 }
 
+// One pass of the intra-block CGS2 over this block's rows (thread per row; a
+// block only ever touches its own rows, so no grid sync is needed between a
+// store and a later read of the same rows).  Column i of W:
+//   vprev >= 0: first store Vn[:, vprev] = W[:, vprev] * sc_prev
+//   upd:  w_i -= sum_{j<i} Vn_j c[j]
+//   dself: projections Vn_j^H w_i (j < i)                       -> outputs [0, i)
+//   nrm:  ||w_i||^2                                             -> output  o_n
+//   nxt:  Vn_j^H w_{i+1} (j < i) and w_i^H w_{i+1}              -> outputs o_x .. o_x + i
+// Per-block partial sums in a fixed order go to a.part[blockIdx.x * S + e].
+template <int TM>
+__device__ void intra_pass(const OrthArgs& a, int i, const cplx* c, int vprev, double sc_prev, bool upd, bool dself,
+                           bool nrm, bool nxt, long r0, long r1, cplx* red, int par) {
+  constexpr int NV = 2 * TM + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  cplx* Vn = a.V + (long)a.m * a.n;
+  const int o_n = dself ? i : 0, o_x = o_n + (nrm ? 1 : 0);
+  const int nv = o_x + (nxt ? i + 1 : 0);
+  cplx accd[TM], accx[TM + 1];
+  double accn = 0.0;
+#pragma unroll
+  for (int e = 0; e < TM; ++e) accd[e] = cmk(0, 0);
+#pragma unroll
+  for (int e = 0; e <= TM; ++e) accx[e] = cmk(0, 0);
+  // four rows per thread and iteration: all loads of the four rows are issued
+  // before their arithmetic (the stores to W / Vn would otherwise serialise them)
+  constexpr int RU = TM <= 2 ? 4 : (TM <= 4 ? 2 : 1);
+  for (long rb = r0 + threadIdx.x; rb < r1; rb += (long)RU * blockDim.x) {
+    cplx vj[RU][TM], w[RU], wn[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const long r = rb + (long)u * blockDim.x;
+      const bool in = r < r1;
+#pragma unroll
+      for (int j = 0; j < TM; ++j)
+        if (j < i) vj[u][j] = in ? __ldcg((j == vprev ? a.W : Vn) + (long)j * a.n + r) : cmk(0, 0);
+      w[u] = in ? __ldcg(a.W + (long)i * a.n + r) : cmk(0, 0);
+      wn[u] = (nxt && in) ? __ldcg(a.W + (long)(i + 1) * a.n + r) : cmk(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const long r = rb + (long)u * blockDim.x;
+      const bool in = r < r1;
+      if (vprev >= 0) {
+#pragma unroll
+        for (int j = 0; j < TM; ++j)
+          if (j == vprev) {
+            vj[u][j] = cscale(vj[u][j], sc_prev);
+            if (in) Vn[(long)vprev * a.n + r] = vj[u][j];
+          }
+      }
+      if (upd) {
+#pragma unroll
+        for (int j = 0; j < TM; ++j)
+          if (j < i) w[u] = csub(w[u], cmul(vj[u][j], c[j]));
+        if (in) a.W[(long)i * a.n + r] = w[u];
+      }
+      if (dself) {
+#pragma unroll
+        for (int j = 0; j < TM; ++j)
+          if (j < i) cfmaconj(accd[j], vj[u][j], w[u]);
+      }
+      if (nrm) accn += w[u].x * w[u].x + w[u].y * w[u].y;
+      if (nxt) {
+#pragma unroll
+        for (int j = 0; j < TM; ++j)
+          if (j < i) cfmaconj(accx[j], vj[u][j], wn[u]);
+#pragma unroll
+        for (int j = 0; j < TM; ++j)
+          if (j == i) cfmaconj(accx[j], w[u], wn[u]);
+      }
+    }
+  }
+  // block reduction in a fixed order: butterflies, then warps in order
+  auto wred = [&](cplx v, int e) {
+    for (int off = 16; off > 0; off >>= 1) {
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+    }
+    if (lane == 0) red[warp * NV + e] = v;
+  };
+  if (dself) {
+#pragma unroll
+    for (int j = 0; j < TM; ++j)
+      if (j < i) wred(accd[j], j);
+  }
+  if (nrm) wred(cmk(accn, 0.0), o_n);
+  if (nxt) {
+#pragma unroll
+    for (int j = 0; j <= TM; ++j)
+      if (j <= i) wred(accx[j], o_x + j);
+  }
+  __syncthreads();
+  // alternate partial regions per pass: a fast block's next pass must not
+  // overwrite partials a slower block is still summing
+  cplx* dst = a.ipart + ((long)par * gridDim.x + blockIdx.x) * kIntraNV;
+  for (int e = threadIdx.x; e < nv; e += blockDim.x) {
+    cplx v = red[e];
+    for (int q = 1; q < nw; ++q) v = cadd(v, red[q * NV + e]);
+    dst[e] = v;
+  }
+  __syncthreads();
+}
+
+// after a grid sync: every block sums the first nv partials in the same fixed
+// order (warp per value) into dst (shared memory); no broadcast sync is needed
+__device__ __forceinline__ void intra_reduce(const OrthArgs& a, int nv, cplx* dst, int par) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const cplx* src = a.ipart + (long)par * gridDim.x * kIntraNV;
+  for (int e = warp; e < nv; e += nw) {
+    cplx acc = cmk(0, 0);
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc = cadd(acc, __ldcg(src + (long)b * kIntraNV + e));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) dst[e] = acc;
+  }
+  __syncthreads();
+}
+
 template <int TM>
 __global__ void __launch_bounds__(kOrthThreads, 2) k_orth(OrthArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -402,37 +526,57 @@ __global__ void __launch_bounds__(kOrthThreads, 2) k_orth(OrthArgs a) {
   grid.sync();
   orth_reduce(a, 0, m * t, C2);
   grid.sync();
-  // W -= V C2 and ||w_0||^2
+  // W -= V C2
   if (pr) a.prof[4] = clock64();
   load_C(C2, m * t);
-  orth_pass<TM>(a, Wt, Cs, outsm, a.V, m, 0, t, true, false, 0, 1, r0, r1);
+  orth_pass<TM>(a, Wt, Cs, outsm, a.V, m, 0, t, true, false, 0, 0, r0, r1);
   if (pr) a.prof[5] = clock64();
+  // intra-block CGS2 (D10 step 5), two passes and two grid syncs per column:
+  //   round 1 of column i comes with the norm pass of column i-1:
+  //     c_j = Vn_j^H w_i (j < i-1),  c_{i-1} = sc_{i-1} w_{i-1}^H w_i  (Vn_{i-1} = sc_{i-1} w_{i-1})
+  //   pass B: w_i -= Vn c;  c' = Vn^H w_i
+  //   pass C: w_i -= Vn c'; ||w_i||^2 (and round 1 of column i+1)
+  //   keep iff ||w_i|| > 1e-10 ||A z_i||; Vn_i = w_i / ||w_i|| (else 0), stored by the next pass
+  cplx* red = outsm + (long)(m + 1) * t;   // [nw][2 TM + 1] block partials (beyond the BCGS2 outputs)
+  cplx* vals = red + 8 * (2 * TM + 1);      // reduced values
+  cplx* cc = Cs;                           // current projection coefficients
+  double sc = 0.0;
+  int par = 0;
   for (int i = 0; i < t; ++i) {
     if (i > 0) {
-      // pass 0: c = Vn[:, :i]^H w_i
-      orth_pass<TM>(a, Wt, Cs, outsm, Vn, i, i, 1, false, true, 0, 0, r0, r1);
+      // pass B (stores Vn_{i-1} first)
+      intra_pass<TM>(a, i, cc, i - 1, sc, true, true, false, false, r0, r1, red, par);
       grid.sync();
-      orth_reduce(a, 0, i, cv + (long)i * t);
-      grid.sync();
-      // pass 1: w_i -= Vn c; c' = Vn^H w_i
-      load_C(cv + (long)i * t, i);
-      orth_pass<TM>(a, Wt, Cs, outsm, Vn, i, i, 1, true, true, 0, 0, r0, r1);
-      grid.sync();
-      orth_reduce(a, 0, i, cv + (long)t * t + (long)i * t);
-      grid.sync();
-      // w_i -= Vn c'; ||w_i||^2
-      load_C(cv + (long)t * t + (long)i * t, i);
-      orth_pass<TM>(a, Wt, Cs, outsm, Vn, i, i, 1, true, false, i, 1, r0, r1);
+      intra_reduce(a, i, vals, par);
+      par ^= 1;
+      for (int j = threadIdx.x; j < i; j += blockDim.x) {
+        cc[j] = vals[j];
+        if (blockIdx.x == 0) cv[(long)t * t + (long)i * t + j] = vals[j];
+      }
+      __syncthreads();
     }
+    // pass C: w_i -= Vn c' (i > 0); ||w_i||^2; round 1 of column i+1
+    const bool nx = i + 1 < t;
+    intra_pass<TM>(a, i, cc, -1, 0.0, i > 0, false, true, nx, r0, r1, red, par);
     grid.sync();
-    // keep iff ||w_i|| > 1e-10 ||A z_i|| (D10 step 5); gram[i] is visible after the syncs above
-    const double nrm = sqrt(fmax(orth_norm2(a, 0), 0.0));
+    intra_reduce(a, 1 + (nx ? i + 1 : 0), vals, par);
+    par ^= 1;
+    // keep iff ||w_i|| > 1e-10 ||A z_i||; gram[i] is visible after the syncs above
+    const double nrm = sqrt(fmax(vals[0].x, 0.0));
     const double naz = sqrt(fmax(__ldcg(gram + i * t + i).x, 0.0));
-    const double sc = nrm > 1e-10 * naz ? 1.0 / nrm : 0.0;
+    sc = nrm > 1e-10 * naz ? 1.0 / nrm : 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) nn[i] = cmk(nrm, 0.0);
-    for (long r = r0 + threadIdx.x; r < r1; r += blockDim.x) Vn[(long)i * a.n + r] = cscale(a.W[(long)i * a.n + r], sc);
-    grid.sync();
+    if (nx) {
+      for (int j = threadIdx.x; j <= i; j += blockDim.x) {
+        const cplx v = j < i ? vals[1 + j] : cscale(vals[1 + i], sc);
+        cc[j] = v;
+        if (blockIdx.x == 0) cv[(long)(i + 1) * t + j] = v;
+      }
+    }
+    __syncthreads();
   }
+  // the last new basis vector (own rows; the kernel's end orders it for the host)
+  for (long r = r0 + threadIdx.x; r < r1; r += blockDim.x) Vn[(long)(t - 1) * a.n + r] = cscale(a.W[(long)(t - 1) * a.n + r], sc);
   if (pr) a.prof[6] = clock64();
 }
 
@@ -674,7 +818,7 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dC2, sizeof(cplx) * vc * t);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dsm, sizeof(cplx) * w->small_cap);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dy, sizeof(cplx) * zc);
-    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->partial, sizeof(cplx) * w->partial_cap);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->partial, sizeof(cplx) * (w->partial_cap + 2 * kIntraMaxBlk * kIntraNV));
     if (e == cudaSuccess) {
       w->hsmall = pinned_small(w->small_cap);
       if (!w->hsmall) e = cudaErrorMemoryAllocation;
@@ -693,7 +837,7 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
 // the multi-launch sequence), -1 on a CUDA error (message set).
 static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cudaStream_t st) {
   if (getenv("HELM_ORTH_UNFUSED")) return 0;
-  const size_t smem = sizeof(cplx) * ((size_t)kOrthTile * t + (size_t)m * t + (size_t)(m + 1) * t);
+  const size_t smem = sizeof(cplx) * ((size_t)kOrthTile * t + (size_t)m * t + (size_t)(m + 1) * t + 9 * kIntraNV);
   if (smem > 200 * 1024) return 0;
   static int nsm = 0;
   int dev = 0;
@@ -715,6 +859,8 @@ static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cuda
   if (nblk < 1) return 0;
   OrthArgs a;
   a.n = n; a.V = V; a.m = m; a.t = t; a.W = W; a.part = ws->partial; a.out = ws->dsm;
+  a.ipart = ws->partial + ws->partial_cap;   // the tail region of the partial buffer
+  if (nblk > kIntraMaxBlk) return 0;
   static long long* prof = nullptr;
   if (getenv("HELM_ORTH_PROF") && !prof) cudaMallocManaged((void**)&prof, 16 * sizeof(long long));
   a.prof = prof;
