@@ -215,10 +215,32 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
 #pragma unroll 1
   for (int k = 0; k < w; ++k) {
     const int kh = k & 1, kj = k >> 1;
-    cplx mine = a[0];
+    // a[kj] by a select tree on the bits of kj (depth 5, not a chain of 17)
+    cplx mine;
+    {
+      cplx t1[(kRowHW + 1) / 2];
 #pragma unroll
-    for (int jj = 1; jj < kRowHW; ++jj)
-      if (jj == kj) mine = a[jj];
+      for (int u = 0; u < kRowHW / 2; ++u) t1[u] = (kj & 1) ? a[2 * u + 1] : a[2 * u];
+      if (kRowHW & 1) t1[kRowHW / 2] = a[kRowHW - 1];
+      constexpr int n1 = (kRowHW + 1) / 2;
+      cplx t2[(n1 + 1) / 2];
+#pragma unroll
+      for (int u = 0; u < n1 / 2; ++u) t2[u] = (kj & 2) ? t1[2 * u + 1] : t1[2 * u];
+      if (n1 & 1) t2[n1 / 2] = t1[n1 - 1];
+      constexpr int n2 = (n1 + 1) / 2;
+      cplx t3[(n2 + 1) / 2];
+#pragma unroll
+      for (int u = 0; u < n2 / 2; ++u) t3[u] = (kj & 4) ? t2[2 * u + 1] : t2[2 * u];
+      if (n2 & 1) t3[n2 / 2] = t2[n2 - 1];
+      constexpr int n3 = (n2 + 1) / 2;
+      cplx t4[(n3 + 1) / 2];
+#pragma unroll
+      for (int u = 0; u < n3 / 2; ++u) t4[u] = (kj & 8) ? t3[2 * u + 1] : t3[2 * u];
+      if (n3 & 1) t4[n3 / 2] = t3[n3 - 1];
+      constexpr int n4 = (n3 + 1) / 2;
+      static_assert(n4 == 2, "select tree depth");
+      mine = (kj & 16) ? t4[1] : t4[0];
+    }
     // pivot search: the largest |a_ik|^2 among unused rows, compared on the high
     // 32 bits of the (non-negative) double -- monotonic; candidates equal to ~1e-6
     // relative go to the lowest row -- with one warp max-reduction and a ballot
@@ -353,7 +375,10 @@ __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem
   }
 }
 
-__global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
+#ifndef HELM_FAC_MINB
+#define HELM_FAC_MINB 5   // 5 CTAs per SM (a few spills) beat 4 without
+#endif
+__global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacArgs fa) {
   __shared__ RowSmem sm;
   const int s = blockIdx.y, pseg = blockIdx.x, kind = blockIdx.z;
   if (kind == 1 && fa.P == 1) return;
@@ -391,29 +416,49 @@ __global__ void __launch_bounds__(kRowThreads, 4) k_factor_rows(FacArgs fa) {
         }
       }
       __syncthreads();
-      if (i < w) {
-        // row i of Sinv_c: all loads issued before the products (one latency, not w)
-        const cplx* srow = fac + (long)c * w2 + (long)i * w;
-        cplx acc[kRowHW];
+      // mat is free now: Sinv_c into it, then Y_c = -Sinv_c tmat with 4 x 4 register
+      // tiles (each shared-memory operand load feeds four products; a row per
+      // thread fed one, and the loop was bound by shared-memory bandwidth)
+      {
+        const cplx* src = fac + (long)c * w2;
+        for (int e = threadIdx.x; e < w2; e += blockDim.x) {
+          const int r = e / w;
+          sm.mat[r * kRowW + (e - r * w)] = __ldcg(src + e);
+        }
+      }
+      __syncthreads();
+      {
+        const int nt = (w + 3) >> 2;
+        const int t = threadIdx.x;
+        cplx acc[4][4];
 #pragma unroll
-        for (int jj = 0; jj < kRowHW; ++jj) acc[jj] = cmk(0, 0);
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int r0 = 0; r0 < kRowW; r0 += 12) {
-          cplx sr[12];
+          for (int v = 0; v < 4; ++v) acc[u][v] = cmk(0, 0);
+        const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+        const bool on = t < nt * nt;
+        if (on) {
+          for (int k = 0; k < w; ++k) {
+            cplx av[4], bv[4];
 #pragma unroll
-          for (int u = 0; u < 12; ++u) sr[u] = r0 + u < w ? __ldcg(srow + r0 + u) : cmk(0, 0);
-#pragma unroll
-          for (int u = 0; u < 12; ++u) {
-            if (r0 + u < w) {
-#pragma unroll
-              for (int jj = 0; jj < kRowHW; ++jj) cfma(acc[jj], sr[u], sm.tmat[(r0 + u) * kRowW + 2 * jj + h]);
+            for (int u = 0; u < 4; ++u) {
+              av[u] = sm.mat[(i0 + u) * kRowW + k];     // rows >= w hold finite leftovers, never stored
+              bv[u] = sm.tmat[k * kRowW + j0 + u];
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) cfma(acc[u][v], av[u], bv[v]);
           }
         }
-        // mat is not read in this phase: overwrite row i with Y_c directly
+        __syncthreads();
+        if (on) {
 #pragma unroll
-        for (int jj = 0; jj < kRowHW; ++jj)
-          if (2 * jj + h < w) sm.mat[i * kRowW + 2 * jj + h] = cscale(acc[jj], -1.0);
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              if (i0 + u < w && j0 + v < w) sm.mat[(i0 + u) * kRowW + j0 + v] = cscale(acc[u][v], -1.0);
+        }
       }
       __syncthreads();
     }
