@@ -95,6 +95,10 @@ __host__ __device__ inline int pk_start(int r, int w) {
   return x;
 }
 // entries per padded block (a multiple of 8, so blocks stay 128-byte aligned)
+// Row stride of the explicit separator-inverse rows (k_reduced_inverse, sweep
+// kernels): K w entries padded to a multiple of 8 (128-byte aligned rows, so the
+// separator mat-vec's warp loads are whole cache lines for every P).
+__host__ __device__ inline long x_ld(int K, int w) { return ((long)K * w + 7) / 8 * 8; }
 __host__ __device__ inline int pk_size(int w) { return ((pk_start(w - 1, w) + 1) + 7) / 8 * 8; }
 // index of entry (r, k) of the symmetric block
 __host__ __device__ inline int pk_index(int r, int k, int w) {

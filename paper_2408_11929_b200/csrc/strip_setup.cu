@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   const int K = ra.P - 1;
   if (j >= K) return;
   const int w = ra.w[s];
-  const long w2 = (long)w * w, Kw = (long)K * w;
+  const long w2 = (long)w * w;
   const cplx* red = ra.red + ra.red_off[s];
   cplx* X = xinv + xinv_off[s];
   // three rotating w x w column blocks (current X_k / Z_k, next, prefetch target)
@@ -681,7 +681,8 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   cplx* vb[3] = {reinterpret_cast<cplx*>(smem_raw), reinterpret_cast<cplx*>(smem_raw) + w2,
                  reinterpret_cast<cplx*>(smem_raw) + 2 * w2};
   cplx* Mb = vb[2] + w2;
-  auto blkX = [&](int k, int r, int c) -> cplx& { return X[(long)k * w * Kw + (long)r * Kw + (long)j * w + c]; };
+  const long ld = x_ld(K, w);   // row stride (128-byte aligned rows)
+  auto blkX = [&](int k, int r, int c) -> cplx& { return X[((long)k * w + r) * ld + (long)j * w + c]; };
   auto mm = [&](cplx* C, const cplx* A, const cplx* B, bool acc) {
     if (NT >= 256) blk_mm_tiled2(C, w, A, w, false, B, w, w, -1.0, acc);
     else blk_mm_tiled(C, w, A, w, false, B, w, w, -1.0, acc);
@@ -731,9 +732,13 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
 }
 
 // ------------------------------------------------------------------ host
+// Segments per strip: start at 33 (C5, t = 4, 128-byte aligned separator-inverse
+// rows: P = 29..37 measured 4.35, 4.32, 4.11, 4.19, 4.05, 4.20, 4.13, 4.12,
+// 4.11 ms per apply -- P = 33 is the best; 4 directions x 33 segments =
+// 132 CTAs fit the 148 SMs), halved until segments have >= 8 rows.
 static int choose_segments(int nc, int requested) {
   if (requested > 0) return requested;
-  int P = 32;
+  int P = 33;
   while (P > 1 && (nc - (P - 1)) / P < 8) P /= 2;
   return P;
 }
@@ -828,7 +833,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     h->xinv_off.resize(n_strips);
     for (int s2 = 0; s2 < n_strips; ++s2) {
       h->xinv_off[s2] = xinv_total;
-      xinv_total += (long)(P - 1) * h->w[s2] * (long)(P - 1) * h->w[s2];
+      xinv_total += (long)(P - 1) * h->w[s2] * x_ld(P - 1, h->w[s2]);
     }
   }
   SharedFactors* sf = nullptr;

@@ -438,11 +438,11 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     if (p < P - 1 && tid < 32) {
-      // stream this CTA's rows of the separator inverse (w x Kw, contiguous) into L2
-      // while the all-gather completes; the mat-vec below then reads L2
-      const long Kw = (long)K * w;
-      const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * Kw);
-      const long bytes = (long)w * Kw * (long)sizeof(cplx);
+      // stream this CTA's rows of the separator inverse (w rows of stride x_ld,
+      // contiguous) into L2 while the all-gather completes; the mat-vec reads L2
+      const long ld = x_ld(K, w);
+      const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * ld);
+      const long bytes = (long)w * ld * (long)sizeof(cplx);
       for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
         dprefetch_l2(xp + o, (uint32_t)(bytes - o < 32768L ? bytes - o : 32768L), pol_first);
     }
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
     const long long cx0 = pclk();
     pacc(14, cx0 - cg0);
-    const long Kw = (long)K * w;
+    const long Kw = (long)K * w, xld = x_ld(K, w);
     const int cw = tid >> 5, ncw = ncons >> 5;
 #ifdef HELM_DUAL_ABL_NOXMV
     if (false) {
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           ok[u] = rb + u < w;
-          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * Kw;
+          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
         }
         cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
         for (long jj = lane; jj < Kw; jj += 128) {

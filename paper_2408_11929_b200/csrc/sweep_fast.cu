@@ -184,12 +184,12 @@ __global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant_
         const int w = tab[i].w;
         const long Kw = (long)K * w;
         const uint32_t bytes = (uint32_t)(Kw * sizeof(cplx));
-        const cplx* X = tab[i].xinv + (long)p * w * Kw;
+        const cplx* X = tab[i].xinv + (long)p * w * x_ld(K, w);
         for (int r = 0; r < w; ++r, ++f) {
           const int sidx = f % A.nsx;
           if (f >= (uint32_t)A.nsx) mbar_wait(&xempty[sidx], ((f / A.nsx) - 1) & 1);
           mbar_expect_tx(&xfull[sidx], bytes);
-          bulk_g2s(xring + (long)sidx * A.xrow_elems, X + (long)r * Kw, bytes, &xfull[sidx]);
+          bulk_g2s(xring + (long)sidx * A.xrow_elems, X + (long)r * x_ld(K, w), bytes, &xfull[sidx]);
         }
       }
     }
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant_
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           ok[u] = rb + u < w;
-          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * Kw;
+          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * x_ld(K, w);
         }
         cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
         for (long jj = lane; jj < Kw; jj += 64) {

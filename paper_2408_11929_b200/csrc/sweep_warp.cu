@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(warpk::NTH, 1) k_sweep_warp(const __grid_const
     if (p < P - 1 && tid < 32) {
       // stream this CTA's rows of the separator inverse (w x Kw, contiguous) into L2
       // while the all-gather completes; the mat-vec below then reads L2
-      const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * Kw);
-      const long bytes = (long)w * Kw * (long)sizeof(cplx);
+      const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * x_ld(K, w));
+      const long bytes = (long)w * x_ld(K, w) * (long)sizeof(cplx);
       for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
         wprefetch_l2(xp + o, (uint32_t)(bytes - o < 32768L ? bytes - o : 32768L), pol_first);
     }
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(warpk::NTH, 1) k_sweep_warp(const __grid_const
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           ok[u] = rb + u < w;
-          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * Kw;
+          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * x_ld(K, w);
         }
         cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
         for (long jj = lane; jj < Kw; jj += 128) {
