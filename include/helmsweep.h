@@ -85,7 +85,8 @@ int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols, void* str
  *   is_double  1 = double sweep (2N-1 local solves), 0 = forward sweep only
  *   gather     0 = "recent" (P:L93 literal rule), 1 = "core" ownership (A16)
  *   n_segments P >= 1 cross-row segments per strip for the partitioned
- *              (separator) strip solve; 0 = choose automatically
+ *              (separator) strip solve; 0 = choose automatically (33, halved
+ *              until every segment has >= 8 cross rows)
  * Each strip's local block-tridiagonal matrix is factored once on the device
  * (block-Thomas per segment plus the separator Schur complement).
  * Errors: HELM_EINVAL, HELM_ESINGULAR, HELM_ENOMEM, HELM_ECUDA.  Synchronous. */
