@@ -187,6 +187,10 @@ __global__ void k_factor_segments(FacArgs fa) {
 //   kind 1: bottom-up S'_c = D_c - U_c S'^{-1}_{c+1} U_c^T, X[lo,lo] = S'^{-1}_lo
 // Pivot choice (largest |a_ik| among the rows not yet used, ties to the lower
 // row) and the elementary operations are those of gj_invert.
+// e / w for 0 <= e < w^2 <= 36^2 without an integer division: (e + 1/2) / w in
+// single precision stays at least 1/(2w) away from the next integer
+__device__ __forceinline__ int div_w(int e, float invw) { return (int)(((float)e + 0.5f) * invw); }
+
 static constexpr int kRowW = 36;
 static constexpr int kRowHW = kRowW / 2;
 static constexpr int kRowThreads = 96;
@@ -358,8 +362,9 @@ __device__ __forceinline__ void row_schur(cplx (&a)[kRowHW], int w, const cplx* 
 }
 
 __device__ __forceinline__ void row_store(cplx* dst, int w, const RowSmem& sm) {
+  const float invw = 1.0f / (float)w;
   for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-    const int r = e / w;
+    const int r = div_w(e, invw);
     dst[e] = sm.mat[r * kRowW + (e - r * w)];
   }
 }
@@ -421,8 +426,9 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
       // thread fed one, and the loop was bound by shared-memory bandwidth)
       {
         const cplx* src = fac + (long)c * w2;
+        const float invw = 1.0f / (float)w;
         for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-          const int r = e / w;
+          const int r = div_w(e, invw);
           sm.mat[r * kRowW + (e - r * w)] = __ldcg(src + e);
         }
       }
@@ -582,8 +588,9 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     row_store(Rinv, w, sm);
     if (k >= 1) {
       // G_k = Rinv_k R_{k,k-1} = Rinv_k R_{k-1,k}^T   (S <- T1^T; S is free now)
+      const float invw = 1.0f / (float)w;
       for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-        const int p2 = e / w, q2 = e - p2 * w;
+        const int p2 = div_w(e, invw), q2 = e - p2 * w;
         S[e] = T1[q2 * w + p2];
       }
       __syncthreads();
@@ -683,6 +690,8 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   cplx* Mb = vb[2] + w2;
   const long ld = x_ld(K, w);   // row stride (128-byte aligned rows)
   auto blkX = [&](int k, int r, int c) -> cplx& { return X[((long)k * w + r) * ld + (long)j * w + c]; };
+  const float invw = 1.0f / (float)w;   // e -> e / w by div_w (no integer division)
+  auto rowof = [&](int e) { return div_w(e, invw); };
   auto mm = [&](cplx* C, const cplx* A, const cplx* B, bool acc) {
     if (NT >= 256) blk_mm_tiled2(C, w, A, w, false, B, w, w, -1.0, acc);
     else blk_mm_tiled(C, w, A, w, false, B, w, w, -1.0, acc);
@@ -694,19 +703,20 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   };
   auto stage_Z = [&](int k, cplx* d) {
     for (int e = threadIdx.x; e < w2; e += NT) {
-      const int r = e / w, c = e - r * w;
+      const int r = rowof(e), c = e - r * w;
       cp_async16(d + e, &blkX(k, r, c));
     }
   };
   // forward: rows k < j are zero; k = j: Rinv_j; k > j: Z_k = -G_k Z_{k-1}
   if (j + 1 < K) { stage_M(j + 1, 1); cp_async_commit(); }
   for (int k = 0; k < j; ++k)
-    for (int e = threadIdx.x; e < w2; e += NT) blkX(k, e / w, e % w) = cmk(0, 0);
+    for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = cmk(0, 0); }
   int ic = 0;
   for (int e = threadIdx.x; e < w2; e += NT) {
     const cplx v = red[(long)j * 3 * w2 + e];
     vb[0][e] = v;
-    blkX(j, e / w, e % w) = v;
+    const int r = rowof(e);
+    blkX(j, r, e - r * w) = v;
   }
   for (int k = j + 1; k < K; ++k) {
     cp_async_wait_all();
@@ -714,7 +724,7 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
     if (k + 1 < K) { stage_M(k + 1, 1); cp_async_commit(); }
     cplx* nx = vb[(ic + 1) % 3];
     mm(nx, Mb + (k & 1) * w2, vb[ic], false);
-    for (int e = threadIdx.x; e < w2; e += NT) blkX(k, e / w, e % w) = nx[e];
+    for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = nx[e]; }
     ic = (ic + 1) % 3;
   }
   // backward: vb[ic] holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}
@@ -726,7 +736,7 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
     cplx* z = vb[(ic + 1) % 3];
     if (k >= 1) { stage_M(k - 1, 2); stage_Z(k - 1, vb[(ic + 2) % 3]); cp_async_commit(); }
     mm(z, Mb + (k & 1) * w2, vb[ic], true);
-    for (int e = threadIdx.x; e < w2; e += NT) blkX(k, e / w, e % w) = z[e];
+    for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = z[e]; }
     ic = (ic + 1) % 3;
   }
 }
