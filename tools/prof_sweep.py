@@ -17,10 +17,12 @@ ap.add_argument("--t", type=int, default=4)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--warm", type=int, default=2)
 ap.add_argument("--nseg", type=int, default=0)
+ap.add_argument("--names", default="", help="comma-separated directions (overrides --t)")
 a = ap.parse_args()
 
 cfg = make_config(a.config)
-names = {1: ["LRL"], 2: ["LRL", "BTB"], 4: ["LRL", "RLR", "BTB", "TBT"]}[a.t]
+names = a.names.split(",") if a.names else {1: ["LRL"], 2: ["LRL", "BTB"], 4: ["LRL", "RLR", "BTB", "TBT"]}[a.t]
+a.t = len(names)
 dev = torch.device("cuda:0")
 prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev))
 dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap, n_segments=a.nseg) for nm in names]
