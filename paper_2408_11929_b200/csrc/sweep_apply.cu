@@ -658,6 +658,26 @@ extern "C" const char* helm_sweep_kernel_name(void) { return g_sweep_kernel; }
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                     cudaStream_t st) {
   const helm_problem_s* prob = dirs[0]->prob;
+  // The batched kernels are persistent and cooperative: all CTAs of all t
+  // directions (P segment CTAs each, plus a reducer in the general kernel) must
+  // be co-resident, one per SM.  A batch that cannot be (e.g. t = 8 with 33
+  // segments) runs as two half batches, in order on the same stream.
+  if (t > 1) {
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    long need = 0;
+    for (int d = 0; d < t; ++d) need += dirs[d]->P + 1;
+    if (need > nsm) {
+      const int h = t / 2;
+      int rc = sweep_apply_dev(dirs, h, Rdev, ldr, Zdev, ldz, st);
+      if (rc != HELM_OK) return rc;
+      return sweep_apply_dev(dirs + h, t - h, Rdev + (ldr == 0 ? 0 : (long)h * ldr), ldr, Zdev + (long)h * ldz, ldz, st);
+    }
+  }
   // kernel choice: the two-chain block kernel (sweep_dual.cu) where it applies
   // (w <= 36, P > 1), else the single-chain register-streaming kernel
   // (sweep_fast.cu, w <= 36), else the general TMA-ring kernel.

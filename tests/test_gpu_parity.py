@@ -140,6 +140,24 @@ def test_single_sweeps_and_broadcast(names):
         assert rel(Z[k].cpu().numpy(), P.apply(r)) <= 1e-10
 
 
+def test_eight_directions_split_batch():
+    """t = 8 with 33 segments needs 8 x 33 CTAs, more than the SMs: the apply
+    runs as two co-resident half batches; every direction must equal its
+    single-direction apply bit for bit (single applies are oracle-tested above)."""
+    cfg = CFGS["C3"]()
+    names = ["LRL", "RLR", "BTB", "TBT", "LR", "RL", "BT", "TB"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+    assert dirs[0].info().n_segments * len(names) > 148
+    r = to_dev(random_vector(cfg.n, 21))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, r, Z, ldr=0)
+    for k, d in enumerate(dirs):
+        z1 = torch.zeros((1, cfg.n), dtype=torch.complex128, device=DEV)
+        hs.sweep_apply([d], r, z1, ldr=0)
+        assert torch.equal(Z[k], z1[0]), names[k]
+
+
 def test_core_gather_and_overlap0():
     cfg = small_problem(48, 36, 20.0, seed=8, variable_c=True, n_strips=4, overlap=0)
     A = p1.assemble(cfg)
