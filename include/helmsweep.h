@@ -106,9 +106,10 @@ int sweep_info(helm_sweep_t s, long* info /* >= 10 */);
  *   R   [dev|host] n x t col-major with leading dim ldr; ldr = 0 broadcasts one
  *       vector to all t directions (k = 1 and the t >= 3 sum rule).
  *   Z   [dev|host] n x t col-major, leading dim ldz (>= n).
- * All handles must belong to the same problem size.  1 <= t <= 8.
- * Errors: HELM_EINVAL, HELM_EDIM, HELM_ECUDA (incl. grid too large for
- * co-residency: reduce n_segments). */
+ * All handles must belong to the same problem size.  1 <= t <= 8.  The t
+ * directions run in one persistent launch when all their CTAs (n_segments
+ * each, plus one) fit the SMs, else as consecutive half batches.
+ * Errors: HELM_EINVAL, HELM_EDIM, HELM_ECUDA. */
 int sweep_apply(const helm_sweep_t* dirs, int t, const double* R, long ldr,
                 double* Z, long ldz, void* stream);
 
