@@ -634,10 +634,18 @@ int to_host(Work& wk, const cplx* dsrc, size_t count, std::vector<std::complex<d
 
 // Incremental Householder QR of the block Hessenberg matrix H~ (host)
 // "minimises the Euclidean norm of the residual": min_y || beta e1 - H~ y ||.
+// H~ can be rank deficient: a deflated column (D10 step 6) keeps its H~ column
+// but gets no new row, and duplicate preconditioners give (numerically) equal
+// columns.  A column whose part below the current rank vanishes after the
+// previous reflectors (|tail| <= 1e-12 |column|) lies in the span of the
+// earlier independent columns: it gets no reflector and y = 0 there, which
+// leaves the minimal residual unchanged (the oracle's lstsq reaches the same
+// residual and, for equal columns, the same x = Z y).
 struct HouseholderLSQ {
   typedef std::complex<double> C;
-  std::vector<std::vector<C>> R;   // columns of the triangularised H~ (length nrows at append time)
-  std::vector<std::vector<C>> v;   // reflector vectors (start at their column index)
+  std::vector<std::vector<C>> R;   // columns of the triangularised H~ (entries 0..rank at append time)
+  std::vector<int> piv;            // row of each column's pivot, -1 for a dependent column
+  std::vector<std::vector<C>> v;   // reflector vectors (reflector q acts on rows q..)
   std::vector<C> tau;
   std::vector<C> g;                // transformed rhs
   int nrows = 0;
@@ -646,13 +654,13 @@ struct HouseholderLSQ {
     g.assign(1, C(beta, 0.0));
     nrows = 1;
   }
-  // apply reflector j to vector x (length >= its extent)
-  void apply(int j, std::vector<C>& x) const {
-    const std::vector<C>& vj = v[j];
+  // apply reflector q (rows q..) to vector x
+  void apply(int q, std::vector<C>& x) const {
+    const std::vector<C>& vq = v[q];
     C s = 0;
-    for (size_t k = 0; k < vj.size(); ++k) s += std::conj(vj[k]) * x[j + k];
-    s *= tau[j];
-    for (size_t k = 0; k < vj.size(); ++k) x[j + k] -= vj[k] * s;
+    for (size_t k = 0; k < vq.size(); ++k) s += std::conj(vq[k]) * x[q + k];
+    s *= tau[q];
+    for (size_t k = 0; k < vq.size(); ++k) x[q + k] -= vq[k] * s;
   }
   // append a column (length new_nrows >= nrows); rows grow to new_nrows
   void append(std::vector<C> col, int new_nrows) {
@@ -661,52 +669,56 @@ struct HouseholderLSQ {
       nrows = new_nrows;
     }
     col.resize(nrows, C(0));
-    const int j = (int)R.size();
-    for (int i = 0; i < j; ++i) apply(i, col);
-    // reflector for rows j..nrows-1 (complex Householder, zeroes col[j+1..])
-    std::vector<C> x(col.begin() + std::min(j, nrows), col.end());
-    C tj = 0;
-    std::vector<C> vj;
-    if (!x.empty()) {
-      double xn = 0;
-      for (auto& e : x) xn += std::norm(e);
-      xn = std::sqrt(xn);
-      // x -> beta e1 with beta = -e^{i arg x0} ||x||, v = x - beta e1, tau = 2/||v||^2
-      C alpha = x[0];
-      double aa = std::abs(alpha);
-      C phase = aa > 0 ? alpha / aa : C(1.0, 0.0);
-      C beta = -phase * xn;
-      vj = x;
-      vj[0] = alpha - beta;
-      double vn = 0;
-      for (auto& e : vj) vn += std::norm(e);
-      tj = vn > 0 ? C(2.0 / vn) : C(0);
+    double cn = 0;
+    for (auto& e : col) cn += std::norm(e);
+    cn = std::sqrt(cn);
+    const int rank = (int)v.size();
+    for (int q = 0; q < rank; ++q) apply(q, col);
+    // the part below the rank: a reflector rows rank.. (complex Householder)
+    double xn = 0;
+    for (int i = rank; i < nrows; ++i) xn += std::norm(col[i]);
+    xn = std::sqrt(xn);
+    if (rank >= nrows || !(xn > 1e-12 * cn)) {
+      piv.push_back(-1);            // dependent: in the span of the earlier columns
+      col.resize(rank);
+      R.push_back(col);
+      return;
     }
-    v.push_back(vj);
-    tau.push_back(tj);
-    if (!vj.empty()) {
-      apply(j, col);
-      apply(j, g);
-    }
+    std::vector<C> x(col.begin() + rank, col.end());
+    // x -> beta e1 with beta = -e^{i arg x0} ||x||, v = x - beta e1, tau = 2/||v||^2
+    C alpha = x[0];
+    double aa = std::abs(alpha);
+    C phase = aa > 0 ? alpha / aa : C(1.0, 0.0);
+    C beta = -phase * xn;
+    std::vector<C> vq = x;
+    vq[0] = alpha - beta;
+    double vn = 0;
+    for (auto& e : vq) vn += std::norm(e);
+    v.push_back(vq);
+    tau.push_back(vn > 0 ? C(2.0 / vn) : C(0));
+    apply(rank, col);
+    apply(rank, g);
+    col.resize(rank + 1);
+    piv.push_back(rank);
     R.push_back(col);
   }
-  // solve R y = g[0..ncols); entries with negligible |R_jj| are set to zero
+  // y = argmin: back substitution over the independent columns (y = 0 on the
+  // dependent ones); res = || g[rank..] ||
   void solve(std::vector<C>& y, double& res) const {
     const int nc = (int)R.size();
+    const int rank = (int)v.size();
     y.assign(nc, C(0));
-    double rmax = 0;
-    for (int j = 0; j < nc; ++j) rmax = std::max(rmax, std::abs(R[j][j]));
-    for (int j = nc - 1; j >= 0; --j) {
-      C s = g[j];
-      for (int k = j + 1; k < nc; ++k) s -= R[k][j] * y[k];
-      double d = std::abs(R[j][j]);
-      y[j] = d > 1e-14 * rmax ? s / R[j][j] : C(0);
+    std::vector<int> colof(rank, -1);   // independent column of each pivot row
+    for (int j = 0; j < nc; ++j)
+      if (piv[j] >= 0) colof[piv[j]] = j;
+    for (int q = rank - 1; q >= 0; --q) {
+      const int j = colof[q];
+      C s = g[q];
+      for (int q2 = q + 1; q2 < rank; ++q2) s -= R[colof[q2]][q] * y[colof[q2]];
+      y[j] = s / R[j][q];
     }
     double r2 = 0;
-    for (int i = nc; i < nrows; ++i) r2 += std::norm(g[i]);
-    // columns with dropped pivots leave their g entry unmatched
-    for (int j = 0; j < nc; ++j)
-      if (!(std::abs(R[j][j]) > 1e-14 * rmax)) r2 += std::norm(g[j]);
+    for (int i = rank; i < nrows; ++i) r2 += std::norm(g[i]);
     res = std::sqrt(r2);
   }
 };

@@ -208,6 +208,31 @@ def test_mpgmres_parity(name, t):
         assert rel(x.cpu().numpy(), x2) <= 1e-8
 
 
+@pytest.mark.parametrize("names", [["LRL", "LRL"], ["LRL", "BTB", "LRL", "BTB"]])
+def test_mpgmres_deflation(names):
+    """Duplicate preconditioners (D10 step 5, A21): the duplicate columns deflate
+    in every iteration (||w|| <= 1e-10 ||A z||) inside the fused
+    orthogonalisation -- zero V slots, intra-block projections through them --
+    and the iterates match the oracle run with the same preconditioners."""
+    cfg = CFGS["var"]()
+    A = p1.assemble(cfg)
+    b_ref = p1.load_vector(cfg)
+    precs = _oracle_precs(cfg, A, names)
+    x_ref, st_ref = krylov.mpgmres(A, [P.apply for P in precs], b_ref, tol=cfg.tol, maxit=200)
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    prob.load_vector(to_dev(cfg.f.ravel()), b)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol, maxit=200)
+    ndup = len(names) - len(set(names))
+    assert st_ref.deflations == ndup * st_ref.iterations
+    assert st["deflations"] == ndup * st["iterations"], (st["deflations"], st["iterations"])
+    assert abs(st["iterations"] - st_ref.iterations) <= 1
+    if st["iterations"] == st_ref.iterations:
+        assert rel(x.cpu().numpy(), x_ref) <= 1e-8
+
+
 def test_host_buffers_end_to_end():
     """The C ABI accepts host pointers (the end-to-end path stages them)."""
     cfg = CFGS["C1"]()
