@@ -106,6 +106,27 @@ def test_sweep_apply_parity(name, nseg):
         assert rel(Zh[k], z_ref) <= 1e-10, (name, names[k], rel(Zh[k], z_ref))
 
 
+@pytest.mark.parametrize("kernel", ["dual", "fast", "general"])
+@pytest.mark.parametrize("nseg", [16, 30])
+def test_short_segments(kernel, nseg, monkeypatch):
+    """Degenerate segment lengths: C1 (65 cross rows) with 16 / 30 segments has
+    segments of 1-4 rows (odd and even, the step loop's tail, the ring across
+    solves with very short phases) -- every kernel vs the oracle."""
+    monkeypatch.setenv("HELM_SWEEP_KERNEL", kernel)
+    cfg = CFGS["C1"]()
+    A = p1.assemble(cfg)
+    names = ["LRL", "BTB"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap, n_segments=nseg) for nm in names]
+    R = random_vector(cfg.n, 13, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    assert hs.sweep_kernel_name().endswith({"dual": "dual", "fast": "fast", "general": "apply"}[kernel])
+    Zh = Z.cpu().numpy()
+    for k, P in enumerate(_oracle_precs(cfg, A, names)):
+        assert rel(Zh[k], P.apply(R[k])) <= 1e-10, (kernel, nseg, names[k])
+
+
 @pytest.mark.parametrize("kernel", ["dual", "warp", "fast", "general"])
 @pytest.mark.parametrize("name", ["var", "C2", "C5s"])
 def test_sweep_kernels_parity(kernel, name, monkeypatch):
