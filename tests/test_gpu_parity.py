@@ -254,6 +254,30 @@ def test_mpgmres_deflation(names):
         assert rel(x.cpu().numpy(), x_ref) <= 1e-8
 
 
+@pytest.mark.parametrize("nx,ny,n_strips,overlap", [(4, 4, 2, 0), (6, 6, 2, 1), (3, 7, 1, 0)])
+def test_tiny_grids(nx, ny, n_strips, overlap):
+    """Smallest grids the method admits (strips of max(2l+1, 2) cells, 3-row
+    cross directions, a single strip): every direction's apply and a t = 3
+    solve (sum rule, A17/P:L154) against the oracle."""
+    cfg = small_problem(nx, ny, 3.0, seed=nx * 10 + ny, variable_c=True, n_strips=n_strips, overlap=overlap)
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=n_strips, overlap=overlap) for nm in names]
+    R = random_vector(cfg.n, 17, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    precs = _oracle_precs(cfg, A, names, n_strips=n_strips, overlap=overlap)
+    for k, P in enumerate(precs):
+        assert rel(Z[k].cpu().numpy(), P.apply(R[k])) <= 1e-10, names[k]
+    b_ref = cfg.f.ravel()
+    x_ref, st_ref = krylov.mpgmres(A, [P.apply for P in precs], b_ref, tol=1e-8, maxit=50)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st = hs.mpgmres_solve(prob, dirs, to_dev(b_ref), x, tol=1e-8, maxit=50)
+    assert abs(st["iterations"] - st_ref.iterations) <= 1
+    assert rel(A @ x.cpu().numpy(), b_ref) <= 1e-7
+
+
 def test_host_buffers_end_to_end():
     """The C ABI accepts host pointers (the end-to-end path stages them)."""
     cfg = CFGS["C1"]()
