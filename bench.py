@@ -63,12 +63,16 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.window = None       # (t0, t1) of the timed region
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -77,7 +81,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
     def stop(self):
         if self.proc is None:
@@ -89,7 +93,11 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None:
+            inside = [(t, ln) for t, ln in lines if self.window[0] <= t <= self.window[1]]
+            lines = inside if inside else lines[-1:]
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -164,17 +172,20 @@ def run_ours(args):
         last.update(st=st, setup_s=t1 - t0, dirs_info=[d.info() for d in dirs])
         return st
 
+    # the clock sampler runs from before the warm-up; only its samples inside the
+    # timed region are reported
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
-    sampler = ClockSampler(local)
-    sampler.start()
     l0 = hs.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    tw0 = time.monotonic()
     ev0.record(stream)
     its, sweep_ms, spmv_ms, orth_ms, setup_s = [], 0.0, 0.0, 0.0, 0.0
     for _ in range(args.steps):
@@ -186,6 +197,7 @@ def run_ours(args):
         setup_s += last["setup_s"]
     ev1.record(stream)
     torch.cuda.synchronize()
+    sampler.mark(tw0, time.monotonic())
     launches = hs.kernel_launches() - l0
     clocks = sampler.stop()
     total_ms, applies = reduce_over_ranks(ev0.elapsed_time(ev1), sum(its) * t, pg, dev)
