@@ -741,6 +741,32 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   }
 }
 
+// Wide strips (w > 36): the same recurrences with every block in global memory
+// (a w = 99 block is 157 KB, beyond shared memory).  Column block j of X is
+// formed in place in the X rows: Z_j = Rinv_j, Z_k = -G_k Z_{k-1} (k > j), then
+// X_k = Z_k - F_k X_{k+1} (k < K-1); the products are 4x4 register-tiled with
+// operands from L1/L2.  The CTA only reads blocks it wrote itself (same SM: the
+// write-through L1 stays coherent after the barrier ending each product).
+__global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* xinv, const long* xinv_off) {
+  const int s = blockIdx.y, j = blockIdx.x;
+  const int K = ra.P - 1;
+  if (j >= K) return;
+  const int w = ra.w[s];
+  const long w2 = (long)w * w;
+  const cplx* red = ra.red + ra.red_off[s];
+  cplx* X = xinv + xinv_off[s];
+  const long ld = x_ld(K, w);
+  auto blk = [&](int k) { return X + (long)k * w * ld + (long)j * w; };   // block (k, j), row stride ld
+  for (int k = 0; k < j; ++k)
+    for (long e = threadIdx.x; e < w2; e += blockDim.x) blk(k)[(e / w) * ld + e % w] = cmk(0, 0);
+  for (long e = threadIdx.x; e < w2; e += blockDim.x) blk(j)[(e / w) * ld + e % w] = red[(long)j * 3 * w2 + e];
+  __syncthreads();
+  for (int k = j + 1; k < K; ++k)
+    blk_mm_tiled(blk(k), (int)ld, red + ((long)k * 3 + 1) * w2, w, false, blk(k - 1), (int)ld, w, -1.0, false);
+  for (int k = K - 2; k >= 0; --k)
+    blk_mm_tiled(blk(k), (int)ld, red + ((long)k * 3 + 2) * w2, w, false, blk(k + 1), (int)ld, w, -1.0, true);
+}
+
 // ------------------------------------------------------------------ host
 // Segments per strip: start at 33 (C5, t = 4, 128-byte aligned separator-inverse
 // rows: P = 29..37 measured 4.35, 4.32, 4.11, 4.19, 4.05, 4.20, 4.13, 4.12,
@@ -828,9 +854,15 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     if (e == cudaSuccess) e = helm_dev_alloc(p, bytes);
   };
   // explicit separator-inverse offsets (register-streaming kernel only)
-  const bool want_xinv = P > 1 && wmax <= kXinvMaxW;
+  // wide strips (w > 36): explicit separator-inverse rows too (formed in global
+  // memory), used by the general kernel's segments instead of its reducer CTA's
+  // sequential separator solve (C4: 19.1 -> 12.5 ms per t = 4 apply for +24 ms of
+  // setup per axis); HELM_NO_WIDE_XINV keeps the reducer path
+  const bool wide_xinv = wmax > kXinvMaxW && getenv("HELM_NO_WIDE_XINV") == nullptr;
+  const bool want_xinv = P > 1 && (wmax <= kXinvMaxW || wide_xinv);
   // bottom-up inverses for the two-chain kernel (sweep_dual.cu): row factorisation only
   const bool want_fac2 = want_xinv && wmax <= kRowW && !getenv("HELM_FACTOR_GENERIC");
+  (void)wide_xinv;
   long pfac_total = 0;
   h->pfac_off.resize(n_strips);
   for (int s2 = 0; s2 < n_strips; ++s2) {
@@ -985,7 +1017,9 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       if (e == cudaSuccess) {
         size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
         static const int ri_nt = getenv("HELM_RI_NT") ? atoi(getenv("HELM_RI_NT")) : 128;
-        if (ri_nt >= 256) {
+        if (wmax > kXinvMaxW) {
+          k_reduced_inverse_glb<<<dim3(P - 1, n_strips), 256, 0, st>>>(ra, h->d_xinv, h->d_xinv_off);
+        } else if (ri_nt >= 256) {
           cudaFuncSetAttribute(k_reduced_inverse<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
           k_reduced_inverse<256><<<dim3(P - 1, n_strips), 256, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
         } else {

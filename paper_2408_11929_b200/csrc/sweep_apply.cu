@@ -282,6 +282,10 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
   const int role = blockIdx.x - D.cta_base;  // 0..P-1 segments, P = reducer
   const bool reducer = (D.P > 1 && role == D.P);
   const int p = role;
+  // X path: the segments solve the separator system with the explicit rows of
+  // its inverse (as sweep_dual.cu does); the reducer CTA has nothing to do
+  const bool xpath = D.P > 1 && D.xinv != nullptr;
+  if (reducer && xpath) return;
 
   Ring rg;
   rg.full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -295,8 +299,9 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
   cplx* tbuf = sm_tail;                  // 4 * wmax: tA0 tB0 tA1 tB1
   cplx* xlo = tbuf + 4 * D.wmax;         // separator x above (p-1)
   cplx* xhi = xlo + D.wmax;              // separator x below (p)
-  cplx* cnx = xhi + D.wmax;              // reducer: next-side corrections (P-1)
-  SolveTab* tab = reinterpret_cast<SolveTab*>(cnx + A.pmax);   // per-solve table (nsolve_max)
+  cplx* cnx = xhi + D.wmax;              // reducer / X path: next-side corrections (P-1)
+  cplx* cpx = cnx + A.pmax;              // X path: prev-side corrections (P-1)
+  SolveTab* tab = reinterpret_cast<SolveTab*>(cpx + A.pmax);   // per-solve table (nsolve_max)
   cplx* vbase = reinterpret_cast<cplx*>(tab + A.nsolve_max);      // vector areas (smem) ...
   if (A.vec_global) vbase = A.vec_scratch + (long)blockIdx.x * 4 * A.vec_elems;  // ... or global
   cplx* vec0 = vbase;                    // bseg / g
@@ -428,7 +433,10 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         }
       };
 
-      if (D.P > 1) {
+      const int par = xpath ? (i & 1) : 0, ppar = par ^ 1;
+      const long exs = 2L * D.P * D.wmax;   // parity strides of yb / xb and xs
+      const long xss = (long)D.P * D.wmax;
+      if (D.P > 1 && !xpath) {
         // ---- phase 1: y_p = A_p^{-1} b_p; publish y[lo], y[hi]
         thomas();
         cplx* yb = D.yb + (long)p * 2 * D.wmax;
@@ -452,6 +460,145 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
           xhi[e] = p < D.P - 1 ? ldcg(D.xs + (long)p * D.wmax + e) : cmk(0, 0);
         }
         cbar(ncons);
+      } else if (D.P > 1) {
+        // ---- phase 1: y_p = A_p^{-1} b_p; publish y[lo], y[hi] (parity buffers)
+        thomas();
+        const int K = D.P - 1;
+        const long Kw = (long)K * w, xld = x_ld(K, w);
+        if (p < D.P - 1 && tid < 32) {
+          // this CTA's rows of the separator inverse into L2 during the gather
+          const char* xp = reinterpret_cast<const char*>(D.xinv + D.xinv_off[s] + (long)p * w * xld);
+          const long bytes = (long)w * xld * (long)sizeof(cplx);
+          for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xp + o),
+                         "r"((uint32_t)(bytes - o < 32768L ? bytes - o : 32768L)) : "memory");
+        }
+        cplx* yb = D.yb + par * exs + (long)p * 2 * D.wmax;
+        for (int e = tid; e < w; e += ncons) {
+          yb[e] = yseg[e];
+          yb[D.wmax + e] = yseg[(m - 1) * w + e];
+        }
+        cbar(ncons);
+        long long cw0 = clock64();
+        if (tid == 0) {
+          __threadfence();
+          red_release_add(&D.cnt[0], 1u);
+          while (ld_relaxed(&D.cnt[0]) < (unsigned)(D.P * (i + 1))) __nanosleep(20);
+          (void)ld_acquire(&D.cnt[0]);
+        }
+        cbar(ncons);
+        pf.xwait += clock64() - cw0;
+        // separator-row corrections (from solve i-1), every separator (reducer step (a))
+        if (i >= 1) {
+          const int aprev = D.a[sigma(D, step_of(D, i - 1))];
+          for (int k = tid; k < K; k += ncons) {
+            const int sk = D.seg_hi[k] + 1;
+            auto X = [&](int cc, int q) -> cplx {
+              if (cc == sk) return ldcg(D.xs + ppar * xss + (long)k * D.wmax + q);
+              if (cc == sk - 1) return ldcg(D.xb + ppar * exs + (long)k * 2 * D.wmax + D.wmax + q);
+              return ldcg(D.xb + ppar * exs + (long)(k + 1) * 2 * D.wmax + q);
+            };
+            cplx cp = cmk(0, 0), cn = cmk(0, 0);
+            if (st > 0) {
+              if (!bwd) {
+                cp = correction(D, s, prev_side(D), sk, aprev, X);
+                if (k == p) D.corr_prev[(long)st * D.nc + sk] = cp;   // kept for the backward pass
+              } else {
+                cp = ldcg(D.corr_prev + (long)st * D.nc + sk);
+              }
+            }
+            if (bwd) cn = correction(D, s, next_side(D), sk, aprev, X);
+            cpx[k] = cp;
+            cnx[k] = cn;
+          }
+          cbar(ncons);
+        }
+        // g_k = b_{s_k} (+ corrections) - U_{h_k}^T y_k[hi] - U_{s_k} y_{k+1}[lo] (reducer step (b)), into yseg
+        cplx* g = yseg;
+        const cplx* ybp = D.yb + par * exs;
+        for (int e = tid; e < K * w; e += ncons) {
+          const int k = e / w, q = e % w;
+          const int hk = D.seg_hi[k], sk = hk + 1;
+          cplx v = __ldg(D.R + node_of(D, a, sk, q));
+          if (st > 0 && q == qp) v = cadd(v, cpx[k]);
+          if (bwd && q == qn) v = cadd(v, cnx[k]);
+          const cplx* yh = ybp + (long)k * 2 * D.wmax + D.wmax;     // y_k[hi]
+          const cplx* yl = ybp + (long)(k + 1) * 2 * D.wmax;        // y_{k+1}[lo]
+          cplx t = cmul(__ldg(cband + (long)hk * D.wmax + q), ldcg(yh + q));
+          if (q >= 1) cfma(t, __ldg(nband + (long)hk * D.wmax + q - 1), ldcg(yh + q - 1));
+          cfma(t, __ldg(cband + (long)sk * D.wmax + q), ldcg(yl + q));
+          if (q + 1 < w) cfma(t, __ldg(nband + (long)sk * D.wmax + q), ldcg(yl + q + 1));
+          g[e] = csub(v, t);
+        }
+        cbar(ncons);
+        // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
+        const int cw = tid >> 5, ncw = ncons >> 5, lane = tid & 31;
+        if (p < D.P - 1) {
+          for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
+            const cplx* Xr[4];
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              ok[u] = rb + u < w;
+              Xr[u] = D.xinv + D.xinv_off[s] + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
+            }
+            cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+            for (long jj = lane; jj < Kw; jj += 128) {
+              cplx xv[4][4], gv[4];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const bool in = jj + 32 * v < Kw;
+                gv[v] = in ? g[jj + 32 * v] : cmk(0, 0);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ldcg(Xr[u] + jj + 32 * v) : cmk(0, 0);
+              }
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+#pragma unroll
+              for (int off = 16; off > 0; off >>= 1) {
+                acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
+                acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+              }
+              if (lane == 0 && ok[u]) xhi[rb + u] = acc[u];
+            }
+          }
+        }
+        for (int e = tid; e < D.wmax; e += ncons) {
+          if (p == 0) xlo[e] = cmk(0, 0);
+          if (p == D.P - 1) xhi[e] = cmk(0, 0);
+        }
+        cbar(ncons);
+        // publish x_p (gather row and the next solve's corrections), take x_{p-1}
+        if (p < D.P - 1) {
+          for (int e = tid; e < w; e += ncons) D.xs[par * xss + (long)p * D.wmax + e] = xhi[e];
+          if (writes_Z(D, i)) {
+            const int olo = D.own_lo[s], ohi = D.own_hi[s];
+            for (int q = olo + tid; q <= ohi; q += ncons) D.Z[node_of(D, a, hi + 1, q)] = xhi[q];
+          }
+          cbar(ncons);
+          if (tid == 0) {
+            __threadfence();
+            st_release(&D.flag[p], (unsigned)(i + 1));
+          }
+        }
+        if (p > 0) {
+          long long cw1 = clock64();
+          if (tid == 0) {
+            while (ld_relaxed(&D.flag[p - 1]) < (unsigned)(i + 1)) __nanosleep(20);
+            (void)ld_acquire(&D.flag[p - 1]);
+          }
+          cbar(ncons);
+          pf.xwait += clock64() - cw1;
+          for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D.xs + par * xss + (long)(p - 1) * D.wmax + e);
+        }
+        cbar(ncons);
+      }
+      if (D.P > 1) {
         for (int q = tid; q < w; q += ncons) {
           if (p > 0) {
             const cplx* crr = crow(lo - 1);
@@ -481,7 +628,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         }
       }
       if (D.P > 1) {
-        cplx* xb = D.xb + (long)p * 2 * D.wmax;
+        cplx* xb = D.xb + par * exs + (long)p * 2 * D.wmax;
         for (int e = tid; e < w; e += ncons) {
           xb[e] = yseg[e];
           xb[D.wmax + e] = yseg[(m - 1) * w + e];
@@ -731,7 +878,7 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   int nsolve_max = 1;
   for (int d = 0; d < t; ++d) nsolve_max = std::max(nsolve_max, dirs[d]->is_double ? 2 * dirs[d]->N - 1 : dirs[d]->N);
   nsolve_max = (nsolve_max + 1) & ~1;  // keeps the vector areas after the table 16-byte aligned
-  const long tail = sizeof(cplx) * (7L * wmax + pmax + 8) + 24L * nsolve_max + 32;
+  const long tail = sizeof(cplx) * (7L * wmax + 2L * pmax + 8) + 24L * nsolve_max + 32;
   const long stage_bytes = sizeof(cplx) * stage_elems;
   int vec_global = 0;
   long fixed = 256 + tail + sizeof(cplx) * 4 * vec_elems;
@@ -752,9 +899,9 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     off[d] = total;
-    total += al(sizeof(unsigned) * 2);
-    total += al(sizeof(cplx) * 2L * h->P * h->wmax) * 2;          // yb, xb
-    total += al(sizeof(cplx) * (long)std::max(h->P - 1, 1) * h->wmax);  // xs
+    total += al(sizeof(unsigned) * (2 + h->P));                     // counters, neighbour flags
+    total += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax) * 2;      // yb, xb (parity buffers)
+    total += al(sizeof(cplx) * 2L * h->P * h->wmax);              // xs (parity buffers)
     total += al(sizeof(cplx) * (long)h->N * h->nc);                // corr_prev
     total += al(sizeof(cplx) * (long)h->nc);                       // corr_next
   }
@@ -791,16 +938,21 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];
-    D.cnt = (unsigned*)q; q += al(sizeof(unsigned) * 2);
-    D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
-    D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
-    D.xs = (cplx*)q; q += al(sizeof(cplx) * (long)std::max(h->P - 1, 1) * h->wmax);
+    D.cnt = (unsigned*)q; D.flag = D.cnt + 2; q += al(sizeof(unsigned) * (2 + h->P));
+    D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
+    D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
+    D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
+    // explicit separator-inverse rows: the segments solve the separator system
+    // themselves (X path) unless HELM_GENERAL_REDUCER is set
+    static const bool force_reducer = getenv("HELM_GENERAL_REDUCER") != nullptr;
+    D.xinv = force_reducer ? nullptr : h->d_xinv;
+    D.xinv_off = h->d_xinv_off;
     D.corr_prev = (cplx*)q; q += al(sizeof(cplx) * (long)h->N * h->nc);
     D.corr_next = (cplx*)q;
     D.wmax = h->wmax;
     D.cta_base = base;
     base += h->P + (h->P > 1 ? 1 : 0);
-    e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * 2, st);
+    e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * (2 + h->P), st);
     if (e != cudaSuccess) break;
   }
   if (e == cudaSuccess)

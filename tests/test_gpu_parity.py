@@ -127,6 +127,28 @@ def test_short_segments(kernel, nseg, monkeypatch):
         assert rel(Zh[k], P.apply(R[k])) <= 1e-10, (kernel, nseg, names[k])
 
 
+@pytest.mark.parametrize("wide_xinv", [False, True])
+def test_wide_strips(wide_xinv, monkeypatch):
+    """Block rows wider than 36 nodes (x-strips of 83 nodes): the general kernel,
+    with the explicit separator-inverse rows formed in global memory (default)
+    or with the reducer CTA's separator solve (HELM_NO_WIDE_XINV) -- vs the oracle."""
+    if not wide_xinv:
+        monkeypatch.setenv("HELM_NO_WIDE_XINV", "1")
+    cfg = small_problem(160, 48, 12.0, seed=31, variable_c=True, n_strips=2, overlap=1)
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=2, overlap=1, n_segments=4) for nm in names]
+    assert dirs[0].info().wmax > 36
+    R = random_vector(cfg.n, 19, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    assert hs.sweep_kernel_name() == "k_sweep_apply"
+    Zh = Z.cpu().numpy()
+    for k, P in enumerate(_oracle_precs(cfg, A, names, n_strips=2, overlap=1)):
+        assert rel(Zh[k], P.apply(R[k])) <= 1e-10, (wide_xinv, names[k], rel(Zh[k], P.apply(R[k])))
+
+
 @pytest.mark.parametrize("kernel", ["dual", "warp", "fast", "general"])
 @pytest.mark.parametrize("name", ["var", "C2", "C5s"])
 def test_sweep_kernels_parity(kernel, name, monkeypatch):
