@@ -543,7 +543,8 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
               Xr[u] = D.xinv + D.xinv_off[s] + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
             }
             cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-            for (long jj = lane; jj < Kw; jj += 128) {
+#pragma unroll 2
+            for (long jj = lane; jj < Kw; jj += 128) {   // two iterations' loads in flight
               cplx xv[4][4], gv[4];
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
