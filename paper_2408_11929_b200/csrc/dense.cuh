@@ -196,16 +196,22 @@ __device__ inline int gj_invert(cplx* A, int w, int* piv, cplx* col, double* red
       A[k * w + j] = cmul(v, dinv);
     }
     __syncthreads();
-    // eliminate column k from all other rows
-    for (int e = tid; e < w * w; e += blockDim.x) {
-      int i = e / w, j = e % w;
-      if (i == k) continue;
-      cplx f = col[i];
-      cplx a = (j == k) ? cmk(0.0, 0.0) : A[e];
-      cplx r = A[k * w + j];
-      a.x -= f.x * r.x - f.y * r.y;
-      a.y -= f.x * r.y + f.y * r.x;
-      A[e] = a;
+    // eliminate column k from all other rows: a warp per row, lanes along the
+    // row (no index division, contiguous shared-memory access)
+    {
+      const int lane = tid & 31, nwarp = (int)(blockDim.x >> 5);
+      for (int i = tid >> 5; i < w; i += nwarp) {
+        if (i == k) continue;
+        const cplx f = col[i];
+        for (int j = lane; j < w; j += 32) {
+          const long e = (long)i * w + j;
+          cplx a = (j == k) ? cmk(0.0, 0.0) : A[e];
+          const cplx r = A[k * w + j];
+          a.x -= f.x * r.x - f.y * r.y;
+          a.y -= f.x * r.y + f.y * r.x;
+          A[e] = a;
+        }
+      }
     }
     __syncthreads();
   }

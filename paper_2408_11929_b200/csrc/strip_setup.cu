@@ -168,7 +168,7 @@ __global__ void k_factor_segments(FacArgs fa) {
   for (int c = hi - 1; c >= lo; --c) {
     // tmp = U_c Y_{c+1}  (into XLH as scratch), then nxt = -Sinv_c tmp
     blk_lxr(XLH, cur, Ub(c, BD_U), NONE, w, 1.0, false);
-    blk_matmul(nxt, fac + (long)c * w2, false, XLH, w, -1.0, false);
+    blk_mm_tiled(nxt, w, fac + (long)c * w2, w, false, XLH, w, w, -1.0, false);
     cplx* t = cur; cur = nxt; nxt = t;
   }
   blk_copy(XLH, cur, w);
@@ -640,7 +640,7 @@ __global__ void k_reduced_generic(RedArgs ra) {
     blk_lxr(S, scr(k + 1) + 2 * w2, Ub(sk, BD_U), Ub(sk, BD_UT), w, -1.0, true);
     if (k >= 1) {
       // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
-      blk_matmul(S, Rprev, true, red + (long)(k - 1) * 3 * w2 + 2 * w2, w, -1.0, true);
+      blk_mm_tiled(S, w, Rprev, w, true, red + (long)(k - 1) * 3 * w2 + 2 * w2, w, w, -1.0, true);
     }
     if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
       if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
@@ -654,12 +654,12 @@ __global__ void k_reduced_generic(RedArgs ra) {
         Tmp[e] = Rprev[q * w + p];
       }
       __syncthreads();
-      blk_matmul(G, Rinv, false, Tmp, w, 1.0, false);
+      blk_mm_tiled(G, w, Rinv, w, false, Tmp, w, w, 1.0, false);
     }
     if (k <= P - 3) {
       // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1}
       blk_lxr(Rprev, scr(k + 1) + 3 * w2, Ub(sk, BD_U), Ub(hk1, BD_U), w, -1.0, false);
-      blk_matmul(F, Rinv, false, Rprev, w, 1.0, false);
+      blk_mm_tiled(F, w, Rinv, w, false, Rprev, w, w, 1.0, false);
     }
   }
 }
