@@ -707,10 +707,17 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
       cp_async16(d + e, &blkX(k, r, c));
     }
   };
-  // forward: rows k < j are zero; k = j: Rinv_j; k > j: Z_k = -G_k Z_{k-1}
+  // X = R^{-1} is complex symmetric (R is): this CTA forms the blocks (k, j),
+  // k >= j, of its column block and mirrors them into (j, k), so the backward
+  // recurrence stops at k = j (a third less work than the full column block)
+  auto mirror = [&](int k, const cplx* blk) {   // block (j, k) = block(k, j)^T
+    for (int e = threadIdx.x; e < w2; e += NT) {
+      const int r = rowof(e), c = e - r * w;
+      X[((long)j * w + c) * ld + (long)k * w + r] = blk[e];
+    }
+  };
+  // forward: k = j: Rinv_j; k > j: Z_k = -G_k Z_{k-1}
   if (j + 1 < K) { stage_M(j + 1, 1); cp_async_commit(); }
-  for (int k = 0; k < j; ++k)
-    for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = cmk(0, 0); }
   int ic = 0;
   for (int e = threadIdx.x; e < w2; e += NT) {
     const cplx v = red[(long)j * 3 * w2 + e];
@@ -727,16 +734,18 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
     for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = nx[e]; }
     ic = (ic + 1) % 3;
   }
-  // backward: vb[ic] holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}
+  // backward: vb[ic] holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}, k >= j
+  if (K - 1 > j) mirror(K - 1, vb[ic]);
   __syncthreads();   // every thread's forward stores precede the read-back
-  if (K >= 2) { stage_M(K - 2, 2); stage_Z(K - 2, vb[(ic + 1) % 3]); cp_async_commit(); }
-  for (int k = K - 2; k >= 0; --k) {
+  if (K - 2 >= j) { stage_M(K - 2, 2); stage_Z(K - 2, vb[(ic + 1) % 3]); cp_async_commit(); }
+  for (int k = K - 2; k >= j; --k) {
     cp_async_wait_all();
     __syncthreads();
     cplx* z = vb[(ic + 1) % 3];
-    if (k >= 1) { stage_M(k - 1, 2); stage_Z(k - 1, vb[(ic + 2) % 3]); cp_async_commit(); }
+    if (k - 1 >= j) { stage_M(k - 1, 2); stage_Z(k - 1, vb[(ic + 2) % 3]); cp_async_commit(); }
     mm(z, Mb + (k & 1) * w2, vb[ic], true);
     for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = z[e]; }
+    if (k > j) mirror(k, z);
     ic = (ic + 1) % 3;
   }
 }
@@ -757,14 +766,24 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
   cplx* X = xinv + xinv_off[s];
   const long ld = x_ld(K, w);
   auto blk = [&](int k) { return X + (long)k * w * ld + (long)j * w; };   // block (k, j), row stride ld
-  for (int k = 0; k < j; ++k)
-    for (long e = threadIdx.x; e < w2; e += blockDim.x) blk(k)[(e / w) * ld + e % w] = cmk(0, 0);
+  // blocks (k, j), k >= j, mirrored into (j, k) (X is symmetric; see k_reduced_inverse)
+  auto mirror = [&](int k) {
+    __syncthreads();
+    const cplx* b = blk(k);
+    for (long e = threadIdx.x; e < w2; e += blockDim.x) {
+      const long r = e / w, c = e % w;
+      X[((long)j * w + c) * ld + (long)k * w + r] = b[r * ld + c];
+    }
+  };
   for (long e = threadIdx.x; e < w2; e += blockDim.x) blk(j)[(e / w) * ld + e % w] = red[(long)j * 3 * w2 + e];
   __syncthreads();
   for (int k = j + 1; k < K; ++k)
     blk_mm_tiled(blk(k), (int)ld, red + ((long)k * 3 + 1) * w2, w, false, blk(k - 1), (int)ld, w, -1.0, false);
-  for (int k = K - 2; k >= 0; --k)
+  if (K - 1 > j) mirror(K - 1);
+  for (int k = K - 2; k >= j; --k) {
     blk_mm_tiled(blk(k), (int)ld, red + ((long)k * 3 + 2) * w2, w, false, blk(k + 1), (int)ld, w, -1.0, true);
+    if (k > j) mirror(k);
+  }
 }
 
 // ------------------------------------------------------------------ host
