@@ -315,6 +315,36 @@ def test_host_buffers_end_to_end():
     assert np.linalg.norm(p1.load_vector(cfg) - A @ x) / np.linalg.norm(b) <= 1e-5
 
 
+def test_status_paths():
+    """Error and early-exit paths of the ABI: directions of another problem size
+    (HELM_EDIM), more than 8 directions (HELM_EINVAL), maxit reached
+    (HELM_ENOCONV with the last iterate), and b = 0 (x = 0, no iteration)."""
+    cfg = CFGS["C1"]()
+    prob = gpu_problem(cfg)
+    other = hs.Problem.from_config(CFGS["var"]())
+    d1 = hs.Sweep(prob, "LRL", n_strips=4, overlap=0)
+    d2 = hs.Sweep(other, "LRL", n_strips=5, overlap=1)
+    r = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    Z = torch.zeros((2, cfg.n), dtype=torch.complex128, device=DEV)
+    with pytest.raises(hs.HelmError) as ei:
+        hs.sweep_apply([d1, d2], r, Z, ldr=0)
+    assert ei.value.code == 2
+    Z9 = torch.zeros((9, cfg.n), dtype=torch.complex128, device=DEV)
+    with pytest.raises(hs.HelmError) as ei:
+        hs.sweep_apply([d1] * 9, r, Z9, ldr=0)
+    assert ei.value.code == 1
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    prob.load_vector(to_dev(cfg.f.ravel()), b)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st = hs.mpgmres_solve(prob, [d1], b, x, tol=1e-12, maxit=3)
+    assert st["status"] == "HELM_ENOCONV" and st["iterations"] == 3 and len(st["history"]) == 3
+    assert st["true_rel_res"] < 1.0 and torch.linalg.norm(x).item() > 0
+    z0 = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    x0 = torch.ones(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st0 = hs.mpgmres_solve(prob, [d1], z0, x0, tol=1e-6)
+    assert st0["iterations"] == 0 and torch.count_nonzero(x0).item() == 0
+
+
 def test_invalid_arguments_raise():
     cfg = CFGS["C1"]()
     prob = gpu_problem(cfg)
