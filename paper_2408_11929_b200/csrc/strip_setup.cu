@@ -787,14 +787,16 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
 }
 
 // ------------------------------------------------------------------ host
-// Segments per strip: start at 33 (C5, t = 4, 128-byte aligned separator-inverse
-// rows: P = 29..37 measured 4.35, 4.32, 4.11, 4.19, 4.05, 4.20, 4.13, 4.12,
-// 4.11 ms per apply -- P = 33 is the best; 4 directions x 33 segments =
-// 132 CTAs fit the 148 SMs), halved until segments have >= 8 rows.
+// Segments per strip: the largest P <= 33 whose segments have >= 8 cross rows
+// (C5, t = 4, 128-byte aligned separator-inverse rows: P = 29..37 measured 4.35,
+// 4.32, 4.11, 4.19, 4.05, 4.20, 4.13, 4.12, 4.11 ms per apply -- 33 is the best,
+// and 4 directions x 33 segments = 132 CTAs fit the 148 SMs; C2: 16 / 24 / 32
+// segments 0.56 / 0.50 / 0.53 ms -- more, shorter segments pay while the
+// separator system stays small).
 static int choose_segments(int nc, int requested) {
   if (requested > 0) return requested;
   int P = 33;
-  while (P > 1 && (nc - (P - 1)) / P < 8) P /= 2;
+  while (P > 1 && (nc - (P - 1)) / P < 8) --P;
   return P;
 }
 

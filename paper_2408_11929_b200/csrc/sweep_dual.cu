@@ -133,6 +133,10 @@ __device__ __forceinline__ void chain_row(int g, int e, int m, int lo, int hi, i
   high = up ? 0 : 1;                       // lo -> hi steps need o[r-1]: low mapping
 }
 
+// GSEP: the separator RHS g has its own shared-memory area (more separators
+// than segment rows, e.g. C2 with 32 segments); else it aliases xa.  A template
+// parameter, not a runtime choice: the kernel is at its register cap.
+template <bool GSEP>
 __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_constant__ DualArgs A) {
   using namespace dualk;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -169,7 +173,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* fb = xa + A.vec_elems;                      // chain B phase 3
   cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi (row stride wmax)
   cplx* bne = bcr + A.vec_elems;
-  cplx* gsm = xa;                                   // separator RHS g (K x w), dead before phase 3
+  cplx* gsm_own = bne + A.vec_elems + 7 * A.mmax;  // GSEP: after cs / cps / tcs
+  cplx* gsm = GSEP ? gsm_own : xa;                  // separator RHS g (K x w), xa is dead before phase 3
   cplx* cs = bne + A.vec_elems;                     // [mmax] corrections formed by the last epilogue (next RHS)
   cplx* cps = cs + A.mmax;                          // [mmax] forward-pass corr_prev rows (backward RHS), staged
   cplx* tcs = cps + A.mmax;                         // [5 mmax] transmission coefficients of the next epilogue, staged
@@ -879,7 +884,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   const int nw = (wmax + OWN - 1) / OWN;
   const int threads = 2 * nw * 32 + 64;   // two chain groups + two TMA producer warps
   if (threads > MAXT) return -1;
-  long vec_elems = 0;
+  long vec_elems = 0, gsm_elems = 0;
   int ctas = 0, mmax_all = 1;
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
@@ -887,14 +892,16 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     for (int p = 0; p < h->P; ++p) mmax = std::max(mmax, h->seg_hi[p] - h->seg_lo[p] + 1);
     vec_elems = std::max(vec_elems, (long)(mmax + 1) * h->wmax);
     mmax_all = std::max(mmax_all, mmax);
-    vec_elems = std::max(vec_elems, (long)(h->P - 1) * h->wmax);
+    gsm_elems = std::max(gsm_elems, (long)(h->P - 1) * h->wmax);
     ctas += h->P;
   }
   vec_elems = (vec_elems + 7) / 8 * 8;
   const long stage_elems = pk_size(wmax) + 8;   // padded packed block + a zero entry, 128-byte multiple
   size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * (4 * NST + 4) +
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * (WM + pmax) + 256;
-  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + 7L * mmax_all);
+  const bool gsep = gsm_elems > vec_elems;
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + 7L * mmax_all + (gsep ? gsm_elems : 0));
+  const void* kfun = gsep ? (const void*)k_sweep_dual<true> : (const void*)k_sweep_dual<false>;
   if (smem > (size_t)kDualSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
   std::vector<size_t> off(t);
@@ -951,18 +958,18 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     base += h->P;
     if (e == cudaSuccess) e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * (2 + h->P), st);
   }
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_sweep_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 0, occ = 0;
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_dual, threads, smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, threads, smem);
   if (e == cudaSuccess && occ * nsm < ctas) {
     cudaFreeAsync(scratch, st);
     return -1;   // not co-resident: the caller falls back to the single-chain kernel
   }
   if (e == cudaSuccess) {
     void* args[] = {(void*)&A};
-    e = cudaLaunchCooperativeKernel((void*)k_sweep_dual, dim3(ctas), dim3(threads), args, smem, st);
+    e = cudaLaunchCooperativeKernel(kfun, dim3(ctas), dim3(threads), args, smem, st);
     g_helm_launches++;
   }
   cudaFreeAsync(scratch, st);
