@@ -40,7 +40,8 @@ enum {
   HELM_ECUDA = 4,       /* CUDA runtime error or no device */
   HELM_ENOMEM = 5,      /* device allocation failed */
   HELM_ENOCONV = 6,     /* maxit reached; x holds the last iterate */
-  HELM_EEXHAUSTED = 7   /* every new column of a block deflated (search space exhausted) */
+  HELM_EEXHAUSTED = 7,  /* every new column of a block deflated (search space exhausted) */
+  HELM_ENONFINITE = 8   /* a NaN / Inf reached the Krylov block (failure detection) */
 };
 
 typedef struct helm_problem_s* helm_problem_t;  /* device matrix (4 symmetric diagonals) + geometry + c */
@@ -73,7 +74,10 @@ int helm_get_diagonals(helm_problem_t p, double* out, void* stream);
  * times the nodal complex source f.  [dev|host] f (n complex), b (n complex). */
 int helm_load_vector(helm_problem_t p, const double* f, double* b, void* stream);
 
-/* helm_spmv -- Y = A X for ncols columns (col-major, ld = n).  [dev|host]. */
+/* helm_spmv -- Y = A X for ncols columns (col-major, ld = n), with A the
+ * matrix of helm_assemble: the "t matrix-vector products" of each MPGMRES
+ * iteration (step 3 of D10).  [dev|host] X, Y (n x ncols complex).
+ * 1 <= ncols <= 8.  Errors: HELM_EINVAL, HELM_ECUDA. */
 int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols, void* stream);
 
 /* sweep_setup -- build and factor one directional sweep preconditioner
@@ -85,8 +89,9 @@ int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols, void* str
  *   is_double  1 = double sweep (2N-1 local solves), 0 = forward sweep only
  *   gather     0 = "recent" (P:L93 literal rule), 1 = "core" ownership (A16)
  *   n_segments P >= 1 cross-row segments per strip for the partitioned
- *              (separator) strip solve; 0 = choose automatically (33, halved
- *              until every segment has >= 8 cross rows)
+ *              (separator) strip solve; 0 = choose automatically (the
+ *              largest P <= 33 whose segments have >= 8 cross rows;
+ *              DESIGN.md §5)
  * Each strip's local block-tridiagonal matrix is factored once on the device
  * (block-Thomas per segment plus the separator Schur complement).
  * Errors: HELM_EINVAL, HELM_ESINGULAR, HELM_ENOMEM, HELM_ECUDA.  Synchronous. */
@@ -137,8 +142,12 @@ typedef struct {
  * Householder QR on the host.  x0 = 0; stops when rho_k <= tol.
  *   b [dev|host] n complex; x [dev|host] n complex (output).
  * Host-synchronous (one small device->host copy per iteration).
+ * One problem handle may be reused for solves with different t: its cached
+ * workspace is sized in columns and for the largest t seen.
  * Errors: HELM_EINVAL (tol not in (0,1), t not in [1,8], maxit < 1),
- *         HELM_ENOCONV, HELM_EEXHAUSTED, HELM_ENOMEM, HELM_ECUDA. */
+ *         HELM_ENOCONV, HELM_EEXHAUSTED, HELM_ENONFINITE (NaN / Inf in the
+ *         Gram diagonal, the BCGS2 coefficients or the new norms),
+ *         HELM_ENOMEM, HELM_ECUDA. */
 int mpgmres_solve(helm_problem_t p, const helm_sweep_t* dirs, int t,
                   const double* b, double* x, double tol, int maxit,
                   mpgmres_stats* stats, void* stream);
@@ -152,10 +161,28 @@ const char* helm_last_error(void);
 long helm_kernel_launches(void);
 
 /* Name of the sweep kernel the last sweep_apply / mpgmres_solve iteration of
- * this process launched ("k_sweep_dual", "k_sweep_warp", "k_sweep_fast",
- * "k_sweep_apply"; "" before the first apply).  Diagnostics: the choice
- * depends on the strip width, the segment count and HELM_SWEEP_KERNEL. */
+ * this process launched ("k_sweep_dual", "k_sweep_fast", "k_sweep_apply"; ""
+ * before the first apply).  Diagnostics: the choice depends on the strip
+ * width, the segment count and the sweep_kernel knob. */
 const char* helm_sweep_kernel_name(void);
+
+/* helm_set_knob -- diagnostics / testing controls, process-wide, all 0 (the
+ * product choice) by default; the library reads no environment variable.
+ *   "sweep_kernel"     0 auto (two-chain k_sweep_dual where it applies),
+ *                      2 start at the single-chain k_sweep_fast,
+ *                      3 the general TMA-ring k_sweep_apply
+ *   "general_reducer"  1: k_sweep_apply solves the separator system with its
+ *                      reducer CTA instead of the explicit inverse rows
+ *   "no_wide_xinv"     1: sweep_setup forms no explicit separator-inverse rows
+ *                      for strips wider than 36 nodes
+ *   "factor_generic"   1: sweep_setup uses the generic factorisation kernel
+ *   "orth_unfused"     1: multi-launch BCGS2 instead of the fused k_orth
+ *   "setup_timing"     1: sweep_setup prints its phase times to stderr
+ *   "orth_prof"        1: k_orth prints phase clock stamps to stderr
+ * Every knob selects a different, parity-tested kernel or schedule for the same
+ * arithmetic.  Not synchronised with calls running on other host threads.
+ * Errors: HELM_EINVAL (unknown name or value). */
+int helm_set_knob(const char* name, int value);
 
 #ifdef __cplusplus
 }

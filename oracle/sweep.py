@@ -79,14 +79,21 @@ class SweepPreconditioner:
     LR, RL, BT, TB), built once ("factored once") and applied many times."""
 
     def __init__(self, cfg, A, axis, order, n_strips, overlap, double=True,
-                 gather="recent", exact_schur=False):
+                 gather="recent", exact_schur=False, solvers_from=None):
         self.cfg = cfg
         self.axis = axis
         self.order = order
         self.double = double
         self.gather = gather
         self.p, self.strips = st_mod.strips(cfg, axis, n_strips, overlap)
-        self.solvers = [StripSolver(cfg, axis, s, A, exact_schur) for s in self.strips]
+        if solvers_from is not None:
+            # the same strips factored once serve both orders (LRL / RLR): the
+            # strip solvers depend only on (axis, N, overlap), not on the order
+            assert (solvers_from.axis, len(solvers_from.strips)) == (axis, n_strips)
+            assert all(np.array_equal(a.nodes, b.nodes) for a, b in zip(solvers_from.strips, self.strips))
+            self.solvers = solvers_from.solvers
+        else:
+            self.solvers = [StripSolver(cfg, axis, s, A, exact_schur) for s in self.strips]
         N = n_strips
         self.sigma = list(range(N)) if order == 0 else list(range(N - 1, -1, -1))
         # "prev" interface of a strip = the side facing sigma's predecessor
@@ -170,9 +177,24 @@ DIRS = {"LRL": (0, 0, True), "RLR": (0, 1, True), "BTB": (1, 0, True), "TBT": (1
 
 
 def make_preconditioner(cfg, A, name, n_strips=None, overlap=None, gather="recent",
-                        exact_schur=False):
+                        exact_schur=False, solvers_from=None):
+    """``solvers_from``: an existing preconditioner on the same strips (same axis,
+    N, overlap) whose factored strip solvers are reused -- no arithmetic change."""
     axis, order, double = DIRS[name]
     return SweepPreconditioner(cfg, A, axis, order,
                                cfg.n_strips if n_strips is None else n_strips,
                                cfg.overlap if overlap is None else overlap,
-                               double=double, gather=gather, exact_schur=exact_schur)
+                               double=double, gather=gather, exact_schur=exact_schur,
+                               solvers_from=solvers_from)
+
+
+def make_preconditioners(cfg, A, names, **kw):
+    """make_preconditioner for several directions, factoring each set of strips
+    (axis) once."""
+    out, by_axis = [], {}
+    for nm in names:
+        ax = DIRS[nm][0]
+        P = make_preconditioner(cfg, A, nm, solvers_from=by_axis.get(ax), **kw)
+        by_axis.setdefault(ax, P)
+        out.append(P)
+    return out

@@ -22,14 +22,15 @@ LIB_PATH = os.environ.get("HELM_LIB") or os.path.join(_HERE, "libhelmsweep.so")
 
 HELM_OK = 0
 STATUS = {0: "HELM_OK", 1: "HELM_EINVAL", 2: "HELM_EDIM", 3: "HELM_ESINGULAR", 4: "HELM_ECUDA",
-          5: "HELM_ENOMEM", 6: "HELM_ENOCONV", 7: "HELM_EEXHAUSTED"}
+          5: "HELM_ENOMEM", 6: "HELM_ENOCONV", 7: "HELM_EEXHAUSTED", 8: "HELM_ENONFINITE"}
 
 DIRECTIONS = {"LRL": (0, 0, 1), "RLR": (0, 1, 1), "BTB": (1, 0, 1), "TBT": (1, 1, 1),
               "LR": (0, 0, 0), "RL": (0, 1, 0), "BT": (1, 0, 0), "TB": (1, 1, 0)}
 
 EXPORTS = ["helm_assemble", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
            "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve", "helm_problem_destroy",
-           "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches", "helm_sweep_kernel_name"]
+           "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches", "helm_sweep_kernel_name",
+           "helm_set_knob"]
 
 
 class HelmError(RuntimeError):
@@ -87,6 +88,8 @@ def load():
     L.helm_kernel_launches.restype = l
     L.helm_sweep_kernel_name.argtypes = []
     L.helm_sweep_kernel_name.restype = ctypes.c_char_p
+    L.helm_set_knob.argtypes = [ctypes.c_char_p, i]
+    L.helm_set_knob.restype = i
     for name in ["helm_assemble", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
                  "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve"]:
         getattr(L, name).restype = i
@@ -107,6 +110,11 @@ def sweep_kernel_name() -> str:
     return load().helm_sweep_kernel_name().decode()
 
 
+def set_knob(name: str, value: int) -> None:
+    """helm_set_knob: diagnostics / testing controls (0 = the product choice)."""
+    _check(load().helm_set_knob(name.encode(), int(value)), "helm_set_knob")
+
+
 def _check(code, where):
     if code != HELM_OK:
         raise HelmError(code, where)
@@ -121,18 +129,39 @@ def _stream(stream):
     return ctypes.c_void_p(0)
 
 
-def _ptr(a, dtype=None):
-    """Raw pointer of a torch tensor (device) or numpy array (host); keeps the
-    array contiguous.  Returns (pointer, keepalive)."""
+_TORCH_DTYPES = {np.dtype(np.complex128): "complex128", np.dtype(np.float64): "float64"}
+
+
+def _ptr(a, dtype, count=None, out=False):
+    """Raw pointer of a torch tensor (device or host) or numpy array (host) of
+    `dtype` (complex128 or float64) holding at least `count` elements.  Inputs
+    given as numpy arrays of another dtype are converted (a copy); outputs and
+    torch tensors must already have the right dtype, be contiguous and large
+    enough -- the C ABI would otherwise read or write outside the buffer.
+    Returns (pointer, keepalive)."""
+    want = np.dtype(dtype)
     try:
         import torch
         if isinstance(a, torch.Tensor):
+            if a.dtype != getattr(torch, _TORCH_DTYPES[want]):
+                raise ValueError(f"tensor dtype {a.dtype}, expected torch.{_TORCH_DTYPES[want]}")
             if not a.is_contiguous():
                 raise ValueError("tensor must be contiguous")
+            if a.device.type not in ("cuda", "cpu"):
+                raise ValueError(f"tensor on unsupported device {a.device}")
+            if count is not None and a.numel() < count:
+                raise ValueError(f"tensor has {a.numel()} elements, need {count}")
             return ctypes.c_void_p(a.data_ptr()), a
     except ImportError:
         pass
-    arr = np.ascontiguousarray(a, dtype=dtype)
+    if out:
+        if not isinstance(a, np.ndarray) or a.dtype != want or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"output must be a contiguous {want} numpy array or torch tensor")
+        arr = a
+    else:
+        arr = np.ascontiguousarray(a, dtype=want)
+    if count is not None and arr.size < count:
+        raise ValueError(f"array has {arr.size} elements, need {count}")
     return ctypes.c_void_p(arr.ctypes.data), arr
 
 
@@ -144,7 +173,7 @@ class Problem:
         self._keep = []
         cp = ctypes.c_void_p(0)
         if c is not None:
-            cp, keep = _ptr(c, np.float64)
+            cp, keep = _ptr(c, np.float64, (nx + 1) * (ny + 1))
             self._keep.append(keep)
         desc = _GridDesc(nx, ny, h, omega, cp)
         handle = ctypes.c_void_p()
@@ -158,19 +187,19 @@ class Problem:
         return cls(cfg.nx, cfg.ny, cfg.h, cfg.omega, np.ascontiguousarray(cfg.c.ravel()), stream)
 
     def diagonals(self, out, stream=None):
-        p, keep = _ptr(out)
+        p, keep = _ptr(out, np.complex128, 4 * self.n, out=True)
         _check(load().helm_get_diagonals(self.handle, p, _stream(stream)), "helm_get_diagonals")
         return keep
 
     def load_vector(self, f, b, stream=None):
-        fp, k1 = _ptr(f, np.complex128)
-        bp, k2 = _ptr(b)
+        fp, k1 = _ptr(f, np.complex128, self.n)
+        bp, k2 = _ptr(b, np.complex128, self.n, out=True)
         _check(load().helm_load_vector(self.handle, fp, bp, _stream(stream)), "helm_load_vector")
         return k2
 
     def spmv(self, X, Y, ncols=1, stream=None):
-        xp, k1 = _ptr(X, np.complex128)
-        yp, k2 = _ptr(Y)
+        xp, k1 = _ptr(X, np.complex128, self.n * ncols)
+        yp, k2 = _ptr(Y, np.complex128, self.n * ncols, out=True)
         _check(load().helm_spmv(self.handle, xp, yp, ncols, _stream(stream)), "helm_spmv")
         return k2
 
@@ -284,8 +313,8 @@ def sweep_apply(dirs, R, Z, ldr=None, ldz=None, stream=None):
         ldr = 0 if (hasattr(R, "ndim") and R.ndim == 1) else n
     if ldz is None:
         ldz = n
-    rp, k1 = _ptr(R, np.complex128)
-    zp, k2 = _ptr(Z)
+    rp, k1 = _ptr(R, np.complex128, n if ldr == 0 else (t - 1) * ldr + n)
+    zp, k2 = _ptr(Z, np.complex128, (t - 1) * ldz + n, out=True)
     _check(load().sweep_apply(_dir_array(dirs), t, rp, ldr, zp, ldz, _stream(stream)), "sweep_apply")
     return k2
 
@@ -296,8 +325,9 @@ def mpgmres_solve(problem, dirs, b, x, tol=1e-6, maxit=200, stream=None, raise_o
     st = MPGMRESStats()
     st.history = ctypes.cast(hist, ctypes.POINTER(ctypes.c_double))
     st.history_cap = maxit
-    bp, k1 = _ptr(b, np.complex128)
-    xp, k2 = _ptr(x)
+    n = problem.n
+    bp, k1 = _ptr(b, np.complex128, n)
+    xp, k2 = _ptr(x, np.complex128, n, out=True)
     code = load().mpgmres_solve(problem.handle, _dir_array(dirs), len(dirs), bp, xp, tol, maxit,
                                 ctypes.byref(st), _stream(stream))
     if code not in (HELM_OK, 6, 7) or (raise_on_noconv and code != HELM_OK):

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhelmsweep.so")
-SOURCES = ["assemble.cu", "strip_setup.cu", "sweep_apply.cu", "sweep_fast.cu", "sweep_dual.cu", "sweep_warp.cu", "krylov.cu"]
+SOURCES = ["assemble.cu", "strip_setup.cu", "sweep_apply.cu", "sweep_fast.cu", "sweep_dual.cu", "krylov.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -35,10 +35,16 @@ def build(force=False, verbose=False, prof=False):
              "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
     if prof:
         flags.append("-DHELM_DUAL_PROF")
-    for src in SOURCES:
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", "_prof.o" if prof else ".o"))
         cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + flags
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")

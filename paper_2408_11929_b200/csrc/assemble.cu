@@ -21,6 +21,23 @@ void helm_set_error(const char* fmt, ...) {
 extern "C" const char* helm_last_error(void) { return g_err; }
 extern "C" long helm_kernel_launches(void) { return g_helm_launches.load(); }
 
+static std::atomic<int> g_knobs[KNOB_COUNT];
+int helm_knob(int id) { return (id >= 0 && id < KNOB_COUNT) ? g_knobs[id].load() : 0; }
+
+extern "C" int helm_set_knob(const char* name, int value) {
+  static const char* names[KNOB_COUNT] = {"sweep_kernel", "general_reducer", "no_wide_xinv", "factor_generic",
+                                          "orth_unfused", "setup_timing", "orth_prof"};
+  if (!name) return HELM_EINVAL;
+  for (int k = 0; k < KNOB_COUNT; ++k)
+    if (strcmp(name, names[k]) == 0) {
+      if (k == KNOB_SWEEP_KERNEL && value != 0 && value != 2 && value != 3) break;
+      g_knobs[k] = value;
+      return HELM_OK;
+    }
+  helm_set_error("helm_set_knob: unknown knob or value (%s = %d)", name, value);
+  return HELM_EINVAL;
+}
+
 extern "C" const char* helm_strerror(int code) {
   switch (code) {
     case HELM_OK: return "ok";
@@ -31,6 +48,7 @@ extern "C" const char* helm_strerror(int code) {
     case HELM_ENOMEM: return "out of device memory";
     case HELM_ENOCONV: return "maxit reached without convergence";
     case HELM_EEXHAUSTED: return "search space exhausted (block fully deflated)";
+    case HELM_ENONFINITE: return "non-finite values in the Krylov block";
     default: return "unknown status";
   }
 }

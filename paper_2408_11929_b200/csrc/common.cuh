@@ -40,6 +40,21 @@ __host__ __device__ __forceinline__ cplx cinv(cplx a) {
   return cmk(a.x * d, -a.y * d);
 }
 
+// ------------------------------------------------------------------ knobs
+// Diagnostics / testing controls set through helm_set_knob (helmsweep.h); all 0
+// by default (= the product choice).  The library reads no environment variable.
+enum HelmKnob {
+  KNOB_SWEEP_KERNEL = 0,    // 0 auto, 2 single-chain k_sweep_fast first, 3 general k_sweep_apply
+  KNOB_GENERAL_REDUCER,     // 1: the general kernel solves the separators with its reducer CTA
+  KNOB_NO_WIDE_XINV,        // 1: no explicit separator-inverse rows for w > 36
+  KNOB_FACTOR_GENERIC,      // 1: generic shared-memory factorisation (no packed / bottom-up factors)
+  KNOB_ORTH_UNFUSED,        // 1: multi-launch BCGS2 instead of the fused cooperative k_orth
+  KNOB_SETUP_TIMING,        // 1: sweep_setup prints its phase times to stderr
+  KNOB_ORTH_PROF,           // 1: k_orth phase clock stamps to stderr
+  KNOB_COUNT
+};
+int helm_knob(int id);
+
 // ------------------------------------------------------------------ errors
 void helm_set_error(const char* fmt, ...);
 extern std::atomic<long> g_helm_launches;   // host counter of this library's launches (thread-safe)

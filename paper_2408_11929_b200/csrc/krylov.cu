@@ -152,7 +152,7 @@ struct OrthArgs {
   cplx* part;       // nblk x S partial sums, S = (m + 1) * t
   cplx* out;        // [C1 m*t][C2 m*t][gram t*t][cv 2*t*t][nn t]  (host copy, one D2H)
   long rows;        // rows per block
-  long long* prof;  // optional phase clock stamps of block 0 (diagnostics, HELM_ORTH_PROF)
+  long long* prof;  // optional phase clock stamps of block 0 (diagnostics, orth_prof knob)
   cplx* ipart;      // [2][nblk][kIntraNV] intra-block partials, alternating per pass
 };
 
@@ -751,7 +751,9 @@ __global__ void k_scale_dev(long n, const cplx* __restrict__ x, const double* __
 // dot partials and pinned host mirrors.  No per-solve allocation.
 struct KrylovWS {
   long n = 0;
-  int icap = 0, tcap = 0;
+  int tcap = 0;              // largest t the t-sized buffers (W, Rsrc) hold
+  long vcap = 0, zcap = 0;   // V / Z capacities in columns
+  int small_t = 0;           // t the small per-iteration buffers (dC1, dC2, dsm, partial) are sized for
   cplx *V = nullptr, *Z = nullptr, *W = nullptr, *Rsrc = nullptr, *tmp = nullptr, *partial = nullptr;
   cplx *dC1 = nullptr, *dC2 = nullptr, *dsm = nullptr, *dy = nullptr;
   double* dscal = nullptr;
@@ -790,7 +792,9 @@ void helm_problem_free_ws(helm_problem_s* p) {
 }
 
 // ensure capacity for `iters` iterations of t columns; preserves the first
-// `keepV` V columns and `keepZ` Z columns
+// `keepV` V columns and `keepZ` Z columns.  Capacities are tracked in columns
+// (vcap, zcap) and the small per-iteration buffers are sized for the largest t
+// seen (tcap), so one problem handle can be reused with any t in [1, 8].
 static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keepZ, cudaStream_t st) {
   KrylovWS* w = reinterpret_cast<KrylovWS*>(p->ws);
   if (!w) { w = new KrylovWS(); p->ws = w; w->n = p->n; }
@@ -803,11 +807,11 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->Rsrc, sizeof(cplx) * n * t);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->tmp, sizeof(cplx) * n);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dscal, sizeof(double) * 16);
-    w->tcap = t;
-    w->icap = 0;   // column capacities depend on t
+    if (e == cudaSuccess) w->tcap = t;
   }
-  if (e == cudaSuccess && (long)iters * t > (long)w->icap * w->tcap) {
-    const long vc = 1 + (long)iters * t, zc = (long)iters * t;
+  const long need_v = 1 + (long)iters * t, need_z = (long)iters * t;
+  if (e == cudaSuccess && (need_v > w->vcap || need_z > w->zcap)) {
+    const long vc = std::max(need_v, w->vcap), zc = std::max(need_z, w->zcap);
     cplx *V2 = nullptr, *Z2 = nullptr;
     e = helm_dev_alloc((void**)&V2, sizeof(cplx) * n * vc);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&Z2, sizeof(cplx) * n * zc);
@@ -821,13 +825,19 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
     }
     helm_dev_free(w->V); helm_dev_free(w->Z);
     w->V = V2; w->Z = Z2;
+    w->vcap = vc; w->zcap = zc;
+    w->small_t = 0;   // the small buffers depend on vcap / zcap: resize below
+  }
+  if (e == cudaSuccess && w->small_t < w->tcap) {
+    // sized for vcap V columns and tcap new columns (the largest t any solve of this handle uses)
+    const long vc = w->vcap, zc = w->zcap, tc = w->tcap;
     helm_dev_free(w->dC1); helm_dev_free(w->dC2); helm_dev_free(w->dsm); helm_dev_free(w->dy); helm_dev_free(w->partial);
     w->dC1 = w->dC2 = w->dsm = w->dy = w->partial = nullptr;
     w->hsmall = nullptr;
-    w->partial_cap = std::max(((n + kDotChunk - 1) / kDotChunk) * kMaxT * vc * t, 148L * 4 * (vc + 1) * t);
-    w->small_cap = 4 * vc * t + 64;
-    e = helm_dev_alloc((void**)&w->dC1, sizeof(cplx) * vc * t);
-    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dC2, sizeof(cplx) * vc * t);
+    w->partial_cap = std::max(((n + kDotChunk - 1) / kDotChunk) * kMaxT * vc * tc, 148L * 4 * (vc + 1) * tc);
+    w->small_cap = 4 * vc * tc + 64;
+    e = helm_dev_alloc((void**)&w->dC1, sizeof(cplx) * vc * tc);
+    if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dC2, sizeof(cplx) * vc * tc);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dsm, sizeof(cplx) * w->small_cap);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->dy, sizeof(cplx) * zc);
     if (e == cudaSuccess) e = helm_dev_alloc((void**)&w->partial, sizeof(cplx) * (w->partial_cap + 2 * kIntraMaxBlk * kIntraNV));
@@ -835,7 +845,7 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
       w->hsmall = pinned_small(w->small_cap);
       if (!w->hsmall) e = cudaErrorMemoryAllocation;
     }
-    w->icap = (int)(zc / t);
+    if (e == cudaSuccess) w->small_t = w->tcap;
   }
   if (e != cudaSuccess) {
     helm_set_error("mpgmres_solve: workspace: %s", cudaGetErrorString(e));
@@ -848,7 +858,7 @@ static int ws_reserve(helm_problem_s* p, int t, int iters, long keepV, long keep
 // ran, 0 when the shapes exceed its shared-memory plan (the caller then uses
 // the multi-launch sequence), -1 on a CUDA error (message set).
 static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cudaStream_t st) {
-  if (getenv("HELM_ORTH_UNFUSED")) return 0;
+  if (helm_knob(KNOB_ORTH_UNFUSED)) return 0;
   const size_t smem = sizeof(cplx) * ((size_t)kOrthTile * t + (size_t)m * t + (size_t)(m + 1) * t + 9 * kIntraNV);
   if (smem > 200 * 1024) return 0;
   static int nsm = 0;
@@ -874,7 +884,7 @@ static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cuda
   a.ipart = ws->partial + ws->partial_cap;   // the tail region of the partial buffer
   if (nblk > kIntraMaxBlk) return 0;
   static long long* prof = nullptr;
-  if (getenv("HELM_ORTH_PROF") && !prof) cudaMallocManaged((void**)&prof, 16 * sizeof(long long));
+  if (helm_knob(KNOB_ORTH_PROF) && !prof) cudaMallocManaged((void**)&prof, 16 * sizeof(long long));
   a.prof = prof;
   if (prof) {
     static int calls = 0;
@@ -967,8 +977,8 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
     }
   }
   for (int k = 1; rc == HELM_OK && !converged && k <= maxit; ++k) {
-    if (k > ws->icap) {
-      rc = ws_reserve(prob, t, std::min(maxit, 2 * ws->icap), mV, nz, st);
+    if (1 + (long)k * t > ws->vcap || (long)k * t > ws->zcap) {
+      rc = ws_reserve(prob, t, std::min(maxit, 2 * k), mV, nz, st);
       if (rc != HELM_OK) break;
       wk.partial = ws->partial; wk.hsmall = pinned_small(ws->small_cap); wk.small_cap = ws->small_cap;
       d_gram = ws->dsm; d_cv = d_gram + t * t; d_nn = d_cv + 2 * t * t;
@@ -1059,16 +1069,33 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
       if ((rc = to_host(wk, ws->dC1, (size_t)m * t, h1)) != HELM_OK) break;
       if ((rc = to_host(wk, ws->dC2, (size_t)m * t, h2)) != HELM_OK) break;
       if ((rc = to_host(wk, d_gram, (size_t)(3 * t * t + t), small)) != HELM_OK) break;
-      HELM_CUDA_TRY(cudaMemcpyAsync(nrm.data(), d_nrm, sizeof(double) * t, cudaMemcpyDeviceToHost, st));
+      e = cudaMemcpyAsync(nrm.data(), d_nrm, sizeof(double) * t, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) { helm_set_error("mpgmres_solve: %s", cudaGetErrorString(e)); rc = HELM_ECUDA; break; }
     }
     inner += 2L * m * t;
-    HELM_CUDA_TRY(cudaStreamSynchronize(st));
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { helm_set_error("mpgmres_solve: %s", cudaGetErrorString(e)); rc = HELM_ECUDA; break; }
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[0], ev[1]); sweep_ms += ms;
     cudaEventElapsedTime(&ms, ev[1], ev[2]); spmv_ms += ms;
     cudaEventElapsedTime(&ms, ev[2], ev[3]); orth_ms += ms;
     const C* gram = small.data();
     const C* cv = gram + t * t;
+    // failure detection: a non-finite Gram diagonal, projection or norm (a NaN / Inf
+    // reached the new columns, e.g. from a singular strip solve) would otherwise be
+    // "deflated" silently by the 1e-10 rule; stop with its own status instead
+    {
+      bool finite = true;
+      for (int i = 0; i < t; ++i) finite = finite && std::isfinite(nrm[i]) && std::isfinite(gram[i * t + i].real());
+      for (size_t j = 0; j < h1.size() && finite; ++j)
+        finite = std::isfinite(h1[j].real()) && std::isfinite(h1[j].imag()) && std::isfinite(h2[j].real()) &&
+                 std::isfinite(h2[j].imag());
+      if (!finite) {
+        helm_set_error("mpgmres_solve: non-finite values in the new block at iteration %d", k);
+        rc = HELM_ENONFINITE;
+        break;
+      }
+    }
     std::vector<int> kept;
     std::vector<std::vector<C>> Rb(t, std::vector<C>(t, C(0)));
     for (int i = 0; i < t; ++i) {

@@ -503,7 +503,7 @@ struct RedArgs {
 // separator block-Thomas is a chain).  Block inverses use the register-row
 // Gauss-Jordan of k_factor_rows; products use register-tiled smem matmuls.
 // Shared memory: RowSmem (static) + S, T1 (R_{k,k+1}), T2 (F_k) (dynamic).
-__device__ long long g_red_prof[8];   // diagnostics (HELM_SETUP_TIMING): block 0 sub-phase cycles
+__device__ long long g_red_prof[8];   // diagnostics (setup_timing knob): block 0 sub-phase cycles
 
 // 384 threads: the register-row Gauss-Jordan uses the first 96 (the others only
 // join its barriers); the products, stencil applications and copies use all.
@@ -878,11 +878,11 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   // wide strips (w > 36): explicit separator-inverse rows too (formed in global
   // memory), used by the general kernel's segments instead of its reducer CTA's
   // sequential separator solve (C4: 19.1 -> 12.5 ms per t = 4 apply for +24 ms of
-  // setup per axis); HELM_NO_WIDE_XINV keeps the reducer path
-  const bool wide_xinv = wmax > kXinvMaxW && getenv("HELM_NO_WIDE_XINV") == nullptr;
+  // setup per axis); the no_wide_xinv knob keeps the reducer path
+  const bool wide_xinv = wmax > kXinvMaxW && !helm_knob(KNOB_NO_WIDE_XINV);
   const bool want_xinv = P > 1 && (wmax <= kXinvMaxW || wide_xinv);
   // bottom-up inverses for the two-chain kernel (sweep_dual.cu): row factorisation only
-  const bool want_fac2 = want_xinv && wmax <= kRowW && !getenv("HELM_FACTOR_GENERIC");
+  const bool want_fac2 = want_xinv && wmax <= kRowW && !helm_knob(KNOB_FACTOR_GENERIC);
   (void)wide_xinv;
   long pfac_total = 0;
   h->pfac_off.resize(n_strips);
@@ -977,7 +977,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   }
   GridView g{prob->nx, prob->ny, prob->h, prob->omega, prob->c};
   StripGeo sg{h->d_a, h->d_w, n_strips, nc, wmax, axis};
-  const bool timing = getenv("HELM_SETUP_TIMING") != nullptr;
+  const bool timing = helm_knob(KNOB_SETUP_TIMING) != 0;
   cudaEvent_t tev[6];
   if (timing) {
     for (auto& x : tev) cudaEventCreate(&x);
@@ -1012,7 +1012,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   FacArgs fa{h->d_w, h->d_fac_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr, h->d_ne,
              nc, wmax, P, h->d_fac, scratch, sstride, d_status, h->d_fac2, h->d_facp, h->d_pfac_off};
   if (timing) cudaEventRecord(tev[1], st);
-  if (wmax <= kRowW && !getenv("HELM_FACTOR_GENERIC"))
+  if (wmax <= kRowW && !helm_knob(KNOB_FACTOR_GENERIC))
     k_factor_rows<<<dim3(P, n_strips, 2), kRowThreads, 0, st>>>(fa);
   else
     k_factor_segments<<<dim3(P, n_strips), threads, smem, st>>>(fa);
@@ -1037,7 +1037,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       const long tot = xinv_total;
       if (e == cudaSuccess) {
         size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
-        static const int ri_nt = getenv("HELM_RI_NT") ? atoi(getenv("HELM_RI_NT")) : 128;
+        const int ri_nt = 128;   // 256 threads measured slower (round 1)
         if (wmax > kXinvMaxW) {
           k_reduced_inverse_glb<<<dim3(P - 1, n_strips), 256, 0, st>>>(ra, h->d_xinv, h->d_xinv_off);
         } else if (ri_nt >= 256) {
@@ -1058,7 +1058,12 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   // issued while the stream is busy blocks inside the driver and serialises
   // setups running concurrently on other streams / host threads
   int status = 0;
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  {
+    // always drain this setup's stream before the scratch buffers are freed below,
+    // also after a launch error (kernels queued earlier may still use them)
+    const cudaError_t es = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = es;
+  }
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (timing && e == cudaSuccess) {

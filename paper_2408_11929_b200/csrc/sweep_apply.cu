@@ -762,8 +762,6 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
                      cudaStream_t st);
 int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                      cudaStream_t st);
-int sweep_apply_warp(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
-                     cudaStream_t st);
 
 int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr, cplx* Zdev, long ldz,
                     cudaStream_t st);
@@ -829,20 +827,10 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   // kernel choice: the two-chain block kernel (sweep_dual.cu) where it applies
   // (w <= 36, P > 1), else the single-chain register-streaming kernel
   // (sweep_fast.cu, w <= 36), else the general TMA-ring kernel.
-  // HELM_SWEEP_KERNEL=fast|general starts lower, =warp selects the experimental
-  // warp-chain kernel (sweep_warp.cu) first (diagnostics, parity tests of every
-  // kernel); read per call.
-  const char* ev = getenv("HELM_SWEEP_KERNEL");
-  const int level = !ev ? 1
-                        : strcmp(ev, "general") == 0 ? 3
-                        : strcmp(ev, "fast") == 0    ? 2
-                        : strcmp(ev, "warp") == 0    ? 0
-                                                     : 1;
-  if (level == 0) {
-    g_sweep_kernel = "k_sweep_warp";
-    int rc = sweep_apply_warp(dirs, t, Rdev, ldr, Zdev, ldz, st);
-    if (rc != -1) return rc;
-  }
+  // The sweep_kernel knob (helm_set_knob: 2 = fast, 3 = general) starts lower
+  // (parity tests of every kernel); read per call.
+  const int kn = helm_knob(KNOB_SWEEP_KERNEL);
+  const int level = kn == 2 || kn == 3 ? kn : 1;
   if (level <= 1) {
     g_sweep_kernel = "k_sweep_dual";
     int rc = sweep_apply_dual(dirs, t, Rdev, ldr, Zdev, ldz, st);
@@ -944,8 +932,8 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
     D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
     // explicit separator-inverse rows: the segments solve the separator system
-    // themselves (X path) unless HELM_GENERAL_REDUCER is set
-    static const bool force_reducer = getenv("HELM_GENERAL_REDUCER") != nullptr;
+    // themselves (X path) unless the general_reducer knob is set
+    const bool force_reducer = helm_knob(KNOB_GENERAL_REDUCER) != 0;
     D.xinv = force_reducer ? nullptr : h->d_xinv;
     D.xinv_off = h->d_xinv_off;
     D.corr_prev = (cplx*)q; q += al(sizeof(cplx) * (long)h->N * h->nc);

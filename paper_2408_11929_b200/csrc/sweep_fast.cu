@@ -629,12 +629,9 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   int nsx = room > 0 ? (int)std::min<long>(8, room / (long)(sizeof(cplx) * xrow)) : 0;
   if (pmax > 1 && nsx < 2) nsx = 0;
   if (pmax == 1) nsx = 0;
-  {
-    // The TMA ring for the separator-inverse rows is experimental: it hangs with
-    // >= ~96 co-resident CTAs (cause not yet understood), so it is opt-in.
-    const char* ev = getenv("HELM_XRING");
-    if (!(ev && ev[0] == '1')) nsx = 0;
-  }
+  // (A TMA ring for the separator-inverse rows was tried in round 1 and hung
+  // with >= ~96 co-resident CTAs; it is disabled: the rows are read from L2.)
+  nsx = 0;
   smem += ring_fixed + (size_t)nsx * xrow * sizeof(cplx);
   if (smem > (size_t)kFastSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections

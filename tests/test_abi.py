@@ -64,3 +64,36 @@ def test_no_device_fails_loudly(lib):
     with pytest.raises(pkg.HelmError) as ei:
         pkg.Problem(8, 8, 1.0 / 8, 5.0)
     assert ei.value.code == 4   # HELM_ECUDA
+
+
+def test_knobs_are_explicit_calls(lib):
+    """Kernel / path choices are explicit helm_set_knob calls (no environment
+    variable is read by the library); unknown names and values are rejected."""
+    import paper_2408_11929_b200 as pkg
+    pkg.set_knob("sweep_kernel", 3)
+    pkg.set_knob("sweep_kernel", 0)
+    with pytest.raises(pkg.HelmError) as ei:
+        pkg.set_knob("sweep_kernel", 1)
+    assert ei.value.code == 1
+    with pytest.raises(pkg.HelmError):
+        pkg.set_knob("no_such_knob", 1)
+    so = open(build_mod.LIB, "rb").read()
+    assert b"getenv" not in so
+
+
+def test_binding_rejects_wrong_buffers():
+    """The binding checks dtype, contiguity and size before handing a pointer to
+    the C ABI (a complex64 or short tensor would be read / written out of bounds)."""
+    import numpy as np
+    import torch
+    import paper_2408_11929_b200 as pkg
+    with pytest.raises(ValueError):
+        pkg._ptr(torch.zeros(8, dtype=torch.complex64), np.complex128, 8)
+    with pytest.raises(ValueError):
+        pkg._ptr(torch.zeros(7, dtype=torch.complex128), np.complex128, 8)
+    with pytest.raises(ValueError):
+        pkg._ptr(torch.zeros(16, dtype=torch.complex128)[::2], np.complex128, 8)
+    with pytest.raises(ValueError):
+        pkg._ptr(np.zeros(8, dtype=np.complex64), np.complex128, 8, out=True)
+    p, keep = pkg._ptr(np.zeros(8, dtype=np.float32), np.complex128, 8)   # inputs are converted
+    assert keep.dtype == np.complex128

@@ -21,6 +21,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 import paper_2408_11929_b200 as hs
 from helm_inputs import make_config, random_vector
+from oracle import p1, sweep
 
 DEV = torch.device("cuda:0")
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -88,3 +89,24 @@ def test_fullsize_repeatable_c5():
     hs.sweep_apply(dirs, r, Z1, ldr=0)
     hs.sweep_apply(dirs, r, Z2, ldr=0)
     assert torch.equal(Z1, Z2)
+
+
+@pytest.mark.parametrize("num", [4, 5])
+def test_fullsize_full_vector(num):
+    """The production configuration compared over the WHOLE vector: C4 (x-strips
+    99 nodes wide: the general kernel) and C5 (P = 33, m = 30-31, w = 35: the
+    two-chain kernel as bench.py launches it), all four directions batched in
+    one launch, against the oracle computed here (splu strip factors, one set
+    per axis): max |dz| <= 1e-10 ||z||_inf and the relative 2-norm <= 1e-10."""
+    cfg, prob, dirs = setup(num)
+    A = p1.assemble(cfg)
+    precs = sweep.make_preconditioners(cfg, A, cfg.dirs)
+    r = random_vector(cfg.n, 41)
+    Z = torch.zeros((len(dirs), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, torch.tensor(r, device=DEV), Z, ldr=0)
+    Zh = Z.cpu().numpy()
+    for k, P in enumerate(precs):
+        z = P.apply(r)
+        err_inf = float(np.max(np.abs(Zh[k] - z)) / np.max(np.abs(z)))
+        assert err_inf <= 1e-10, (cfg.name, cfg.dirs[k], err_inf)
+        assert rel(Zh[k], z) <= 1e-10, (cfg.name, cfg.dirs[k], rel(Zh[k], z))

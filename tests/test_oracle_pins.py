@@ -64,6 +64,65 @@ def test_pin1_closed_form_rows(k):
         np.testing.assert_allclose(row, expected, rtol=0, atol=1e-14, err_msg=name)
 
 
+def test_pin1b_variable_c_closed_form_rows():
+    """Pin-1b (A5 / D3, variable wave speed): on a 2 x 2-cell grid with nine
+    nodal c values (non-linear in i, j), the assembled rows equal the rows
+    derived by hand in tests/golden/p1_variable_c_closed_form.txt, where every
+    k_T = omega / mean(c at the triangle's vertices) and k_e = omega / mean(c at
+    the edge's ends) was worked out as a fraction.  A centroid, harmonic-mean,
+    nodal-k or wrong-triangle reading changes these numbers."""
+    from helm_inputs import HelmConfig
+    c = np.array([[1.0, 3.0, 2.0], [4.0, 1.0, 5.0], [2.0, 6.0, 3.0]])     # [j][i]
+    cfg = HelmConfig("pin1b", 2, 2, 1.0, 1.0, 6.0, c, np.zeros((3, 3), np.complex128), 1, 0, ["LRL"])
+    A = p1.assemble(cfg).tocsr()
+    rows = {}
+    with open(os.path.join(GOLDEN, "p1_variable_c_closed_form.txt")) as fh:
+        for line in fh:
+            line = line.split("#")[0].strip()
+            if not line:
+                continue
+            i, j, di, dj, re_expr, im_expr = line.split()
+            rows.setdefault((int(i), int(j)), []).append((int(di), int(dj), eval(re_expr), eval(im_expr)))
+    assert len(rows) == 4
+    for (i, j), entries in rows.items():
+        row = A.getrow(p1.node(cfg, i, j)).toarray().ravel()
+        expected = np.zeros(cfg.n, dtype=np.complex128)
+        for di, dj, re, im in entries:
+            expected[p1.node(cfg, i + di, j + dj)] = re + 1j * im
+        np.testing.assert_allclose(row, expected, rtol=0, atol=1e-14, err_msg=str((i, j)))
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+@pytest.mark.parametrize("overlap", [0, 1])
+def test_pin_d7_strip_is_its_own_impedance_problem(axis, overlap):
+    """D7 interface term (Eq. 4): the transmission operator on an
+    interface is B = d/dn - i k, the operator of the physical boundary condition
+    Eq. 1b.  So each local matrix A_s must equal the D4 assembly of the
+    strip's rectangle posed as its OWN impedance problem (all of its boundary
+    edges impedance edges, with k_e from the same nodal c), which Pin-1 / Pin-1b
+    / Pin-4 fix independently.  A wrong sign or scale of the interface term
+    i k_e B_e, or a missing / extra interface edge, fails here.  Every strip of a
+    16 x 12 variable-c grid, both axes, overlap 0 and 1."""
+    from helm_inputs import HelmConfig
+    cfg = small_problem(16, 12, 9.0, seed=21, variable_c=True, n_strips=4, overlap=overlap)
+    _, sts = strips.strips(cfg, axis, 4, overlap)
+    for st in sts:
+        As = strips.restrict(strips.local_matrix_global(cfg, axis, st), st.nodes).toarray()
+        if axis == 0:
+            c_sub = cfg.c[:, st.a:st.b + 1]
+            sub = HelmConfig("sub", st.b - st.a, cfg.ny, (st.b - st.a) * cfg.h, cfg.Ly, cfg.omega,
+                             np.ascontiguousarray(c_sub), np.zeros_like(c_sub, np.complex128), 1, 0, ["LRL"])
+        else:
+            c_sub = cfg.c[st.a:st.b + 1, :]
+            sub = HelmConfig("sub", cfg.nx, st.b - st.a, cfg.Lx, (st.b - st.a) * cfg.h, cfg.omega,
+                             np.ascontiguousarray(c_sub), np.zeros_like(c_sub, np.complex128), 1, 0, ["LRL"])
+        assert abs(sub.h - cfg.h) < 1e-15
+        Asub = p1.assemble(sub).toarray()
+        assert As.shape == Asub.shape
+        scale = np.abs(Asub).max()
+        assert np.abs(As - Asub).max() <= 1e-14 * scale, (axis, overlap, st.s)
+
+
 def test_pin2_complex_symmetric_not_hermitian():
     cfg = small_problem(10, 7, 6.0, seed=3, variable_c=True)
     A = p1.assemble(cfg)
@@ -426,3 +485,17 @@ def test_duplicate_preconditioner_deflates_to_gmres():
     assert d.deflations == d.iterations
     assert d.iterations == g.iterations
     np.testing.assert_allclose(d.history, g.history, rtol=1e-6)
+
+
+def test_shared_strip_solvers_are_identical():
+    """make_preconditioners factors each axis once and reuses the strip solvers
+    for the other order (test / bench infrastructure): the applies are bit for
+    bit those of independently built preconditioners."""
+    cfg = small_problem(20, 16, 8.0, seed=4, variable_c=True, n_strips=3, overlap=1)
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    shared = sweep.make_preconditioners(cfg, A, names)
+    assert shared[0].solvers is shared[1].solvers and shared[2].solvers is shared[3].solvers
+    r = np.random.default_rng(3).standard_normal(cfg.n) + 0j
+    for nm, P in zip(names, shared):
+        assert np.array_equal(P.apply(r), sweep.make_preconditioner(cfg, A, nm).apply(r)), nm
