@@ -8,14 +8,16 @@ one batched 4-direction sweep_apply launch, SpMM, BCGS2 + block QR, host LSQ)
 -> x.  `value` = sweep-preconditioner applies per second over the whole step
 (t x iterations / step time, setup included); ms_per_step is the
 time-to-solution.  Inputs (c, f) are resident in HBM when the timed region
-starts; the factor set (5.2 GB) is larger than L2, so no explicit flush.
+starts; the two factor sets (one per strip axis, shared by LRL/RLR and
+BTB/TBT) are GBs, far larger than the 126 MB L2, so no explicit flush.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5]
 
 N > 1 (torchrun): independent replicas per rank ("replicas only", DESIGN.md
 §8; scaling weak), timed by CUDA events, max over ranks.
---impl reference: the CPU oracle (oracle/) timed on this host on a bounded
-sample of the same workload, extrapolated to the same metric.
+--impl reference: the CPU oracle (oracle/) timed on this host; one step =
+one batched t = 4 sweep apply of the same C5 workload (measured, no
+extrapolation; factor sets built before timing).
 """
 from __future__ import annotations
 
@@ -42,6 +44,7 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true")
     return ap.parse_args()
 
 
@@ -234,7 +237,8 @@ def run_ours(args):
                                f"t={t} ({'+'.join(names)}), MPGMRES tol {cfg.tol:g}, x0=0; step = assemble + "
                                "4 sweep setups + solve",
                    "n_unknowns": cfg.n, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2_policy": "no flush: factor set %.2f GB >> 126 MB L2" % (sum(i.factor_bytes for i in last["dirs_info"]) / 1e9)},
+                   "l2_policy": "no flush: two factor sets (x / y strips) of %.2f GB in all >> 126 MB L2" % (
+                       sum({i.axis: i.factor_bytes for i in last["dirs_info"]}.values()) / 1e9)},
         "time_to_solution_ms": round(ms_step, 3),
         "iterations": its[-1],
         "setup_ms_avg": round(setup_s / args.steps * 1e3, 3),
@@ -250,10 +254,17 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    if not args.no_e2e and ws == 1:
-        out["e2e"] = run_e2e(args, cfg, names)
+    if not args.no_north_star:
+        out["north_star"] = north_star_kernels(cfg, names, peak)
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, names)
+        # replicas: the job's end-to-end time is the max over ranks, its work the sum
+        e_ms, e_app = reduce_over_ranks(e2e.pop("_ms_total"), e2e.pop("_applies"), pg, dev)
+        e2e["value"] = round(e_app / (e_ms / 1e3), 3)
+        e2e["ms_per_step"] = round(e_ms / args.steps, 3)
+        out["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline and ws == 1:
-        out["cpu_baseline"] = oracle_baseline(cfg, names, its[-1], sample_solves=3)
+        out["cpu_baseline"] = oracle_baseline(cfg, names)
     if rank == 0:
         print(json.dumps(out))
     if pg:
@@ -263,8 +274,9 @@ def run_ours(args):
 
 def run_e2e(args, cfg, names):
     """Same metric through the C ABI with HOST buffers: pinned host c and f are
-    copied in, x is copied back, every step, inside the timed region."""
-    import numpy as np
+    copied in, x is copied back, every step, inside the timed region.  Same
+    --warmup / --steps as the device arm; timed with CUDA events on the
+    launching stream, synchronised on both sides (x is on the host at the end)."""
     import torch
 
     import paper_2408_11929_b200 as hs
@@ -274,7 +286,7 @@ def run_e2e(args, cfg, names):
     f_h = torch.tensor(cfg.f.ravel(), dtype=torch.complex128).pin_memory()
     x_h = torch.zeros(cfg.n, dtype=torch.complex128).pin_memory()
     b_d = torch.zeros(cfg.n, dtype=torch.complex128, device="cuda")
-
+    stream = torch.cuda.current_stream()
     setup_streams = {0: torch.cuda.Stream().cuda_stream, 1: torch.cuda.Stream().cuda_stream}
 
     def step():
@@ -284,93 +296,229 @@ def run_e2e(args, cfg, names):
         _, st = hs.mpgmres_solve(prob, dirs, b_d, x_h.numpy(), tol=cfg.tol, maxit=cfg.maxit)
         return st["iterations"]
 
-    step()
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    its = [step() for _ in range(max(1, min(args.steps, 3)))]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    its = [step() for _ in range(args.steps)]
+    e1.record(stream)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    return {"value": round(sum(its) * t / dt, 3), "unit": "applies/s",
+    wall = time.perf_counter() - w0
+    ms = e0.elapsed_time(e1)
+    return {"_ms_total": ms, "_applies": sum(its) * t, "unit": "applies/s",
             "h2d_bytes_per_step": 8 * cfg.n + 16 * cfg.n, "d2h_bytes_per_step": 16 * cfg.n,
-            "ms_per_step": round(dt / len(its) * 1e3, 3),
+            "host_wall_ms_per_step": round(wall / len(its) * 1e3, 3),
+            "steps": len(its), "warmup": args.warmup,
             "path": "helm_assemble(host c) + sweep_setup x4 + helm_load_vector(host f) + mpgmres_solve(x to host)"}
 
 
-def oracle_baseline(cfg, names, iterations, sample_solves=3):
-    """The CPU oracle as it stands, timed on this host on a bounded sample of
-    the same workload: factor (splu) and solve a few C5 strips, extrapolate
-    to the metric (setup of all strips + iterations x t double sweeps of
-    2N-1 strip solves each)."""
-    import numpy as np
+def north_star_kernels(cfg, names, peak):
+    """The north star's per-kernel numbers on this config, measured with CUDA
+    events on the launching stream (warm, 2 warm-up + 10 timed launches each):
+    SpMV (1 column) and SpMM (t = 4) against the SURVEY 8(d) byte model
+    16 nnz + 2 t 16 n, and the batched sweep apply at t = 1 (LRL), 2 (+BTB),
+    4 (+RLR, TBT) as applies/s and model GB/s.  Inputs exceed L2 (factor sets
+    of GBs; the SpMM's 252 MB > 126 MB)."""
+    import torch
 
+    import paper_2408_11929_b200 as hs
+    from helm_inputs import random_vector
+
+    dev = torch.device("cuda")
+    stream = torch.cuda.current_stream()
+    prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev))
+    dirs = dict(zip(names, hs.make_sweeps(prob, names, n_strips=cfg.n_strips, overlap=cfg.overlap)))
+    # assembled nonzeros of the 7-point P1 stencil on the grid (SURVEY 8(a): 7,346,177 for C5)
+    nx, ny = cfg.nx, cfg.ny
+    nnz = (nx + 1) * (ny + 1) + 2 * (nx * (ny + 1) + (nx + 1) * ny + nx * ny)
+
+    def timed(fn, reps=10, warm=2):
+        for _ in range(warm):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {"nnz": nnz}
+    for ncol in (1, 4):
+        X = torch.tensor(random_vector(cfg.n, 5, ncol), device=dev)
+        Y = torch.zeros_like(X)
+        ms = timed(lambda: prob.spmv(X, Y, ncol), reps=50)
+        model = 16 * nnz + 2 * ncol * 16 * cfg.n
+        out["spmv" if ncol == 1 else "spmm_t4"] = {
+            "ms": round(ms, 5), "model_bytes": model, "achieved_gbs": round(model / (ms / 1e3) / 1e9, 1),
+            "frac_of_peak": round(model / (ms / 1e3) / 1e9 / peak, 4)}
+    r = torch.tensor(random_vector(cfg.n, 6), device=dev)
+    for combo in (["LRL"], ["LRL", "BTB"], ["LRL", "RLR", "BTB", "TBT"]):
+        ds = [dirs[nm] for nm in combo]
+        Z = torch.zeros((len(ds), cfg.n), dtype=torch.complex128, device=dev)
+        ms = timed(lambda: hs.sweep_apply(ds, r, Z, ldr=0), reps=10)
+        model = sum(d.info().model_bytes_per_apply for d in ds)
+        out[f"sweep_apply_t{len(ds)}"] = {
+            "dirs": "+".join(combo), "ms": round(ms, 4), "applies_per_s": round(len(ds) / (ms / 1e3), 1),
+            "model_bytes": model, "achieved_gbs": round(model / (ms / 1e3) / 1e9, 1),
+            "frac_of_peak": round(model / (ms / 1e3) / 1e9 / peak, 4), "kernel": hs.sweep_kernel_name()}
+    return out
+
+
+def host_info():
+    """Host description for the CPU numbers."""
+    info = {"os_cpu_count": os.cpu_count()}
+    try:
+        info["nproc"] = len(os.sched_getaffinity(0))
+    except Exception:
+        info["nproc"] = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{k: d.get(k) for k in ("internal_api", "num_threads")} for d in threadpool_info()]
+    except Exception:
+        info["blas"] = None
+    info["OMP_NUM_THREADS"] = os.environ.get("OMP_NUM_THREADS")
+    return info
+
+
+def oracle_baseline(cfg, names):
+    """The CPU oracle as it stands, timed on this host on a bounded sample of
+    the same workload, measured (not extrapolated): the C5 assembly, the
+    splu factor set of the x strips (LRL's 32 strips), and one full LRL double
+    sweep (2N - 1 = 63 strip solves).  `value` is the oracle's measured apply
+    rate (applies/s, factor set built); its setup times are reported beside it."""
     from helm_inputs import random_vector
     from oracle import p1, sweep
-    from oracle import strips as st_mod
 
     t0 = time.perf_counter()
     A = p1.assemble(cfg)
     t_asm = time.perf_counter() - t0
-    _, strips_x = st_mod.strips(cfg, 0, cfg.n_strips, cfg.overlap)
-    mid = cfg.n_strips // 2
-    picks = [strips_x[mid + k] for k in range(2)]
-    fac_t, sol_t = [], []
+    t1 = time.perf_counter()
+    P = sweep.make_preconditioner(cfg, A, names[0])
+    t_fac = time.perf_counter() - t1
     r = random_vector(cfg.n, 77)
-    for stp in picks:
-        t1 = time.perf_counter()
-        S = sweep.StripSolver(cfg, 0, stp, A)
-        fac_t.append(time.perf_counter() - t1)
-        rl = r[stp.nodes]
-        for _ in range(sample_solves):
-            t2 = time.perf_counter()
-            S.solve(rl)
-            sol_t.append(time.perf_counter() - t2)
-    N = cfg.n_strips
-    t = len(names)
-    setup = t_asm + 2 * N * float(np.mean(fac_t))       # both axes (LRL/RLR, BTB/TBT share strips)
-    apply_s = (2 * N - 1) * float(np.mean(sol_t))
-    total = setup + iterations * t * apply_s
+    t2 = time.perf_counter()
+    c2 = time.process_time()
+    P.apply(r)
+    t_apply = time.perf_counter() - t2
+    cores = (time.process_time() - c2) / t_apply   # threads actually busy (process CPU time / wall)
     sample_s = time.perf_counter() - t0
-    return {"value": round(iterations * t / total, 6), "unit": "applies/s", "cores": 1, "kind": "oracle",
-            "sample": f"oracle assembly of {cfg.name} + splu factor of 2 interior x-strips + "
-                      f"{sample_solves} solves each ({sample_s:.1f} s of CPU work), extrapolated to "
-                      f"setup of 2N={2*N} strips + {iterations} iterations x t={t} x (2N-1)={2*N-1} strip solves",
-            "oracle_apply_s": round(apply_s, 3), "oracle_setup_s": round(setup, 3),
-            "oracle_time_to_solution_s": round(total, 3)}
+    return {"value": round(1.0 / t_apply, 4), "unit": "applies/s", "cores": round(cores, 2), "kind": "oracle",
+            "sample": f"{cfg.name}: oracle assembly ({t_asm:.1f} s) + splu of the {cfg.n_strips} x-strips "
+                      f"({t_fac:.1f} s) + one {names[0]} double sweep of {2 * cfg.n_strips - 1} strip solves "
+                      f"({t_apply:.2f} s); {sample_s:.1f} s of CPU work in all, single process",
+            "oracle_apply_s": round(t_apply, 3), "oracle_assembly_s": round(t_asm, 3),
+            "oracle_factor_one_axis_s": round(t_fac, 3), "host": host_info()}
+
+
+def _ref_worker_init(cfg_num, name):
+    global _REF_P, _REF_R
+    from helm_inputs import make_config, random_vector
+    from oracle import p1, sweep
+    cfg = make_config(cfg_num)
+    A = p1.assemble(cfg)
+    _REF_P = sweep.make_preconditioner(cfg, A, name)
+    _REF_R = random_vector(cfg.n, 78)
+
+
+def _ref_worker_apply(_):
+    t0 = time.perf_counter()
+    _REF_P.apply(_REF_R)
+    return time.perf_counter() - t0
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle (oracle/, numpy/scipy splu) as it
+    stands, on this host, on the same config / metric / unit.  Untimed
+    preparation: assembly and the splu factor sets of both strip axes.  One
+    step = one batched t = 4 sweep apply (LRL, RLR, BTB, TBT, each 2N - 1
+    strip solves), applied one after another as in the paper's serial MATLAB
+    runs.  value = t / step time (applies/s).  Also measured: the
+    t-process mode (a pool of t worker processes, one direction each, "applied
+    in parallel", P:L142).  Under torchrun only rank 0 runs."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from helm_inputs import make_config
+    from helm_inputs import make_config, random_vector
+    from oracle import p1, sweep
     cfg = make_config(args.config)
     names = cfg.dirs
-    # the oracle's own iteration count for this config (tests/golden, written by
-    # tools/make_golden.py from oracle/ only); the full oracle solve is not rerun here
-    iters_assumed = 13
-    gp = os.path.join(ROOT, "tests", "golden", f"oracle_C{args.config}.npz")
-    if os.path.exists(gp):
-        import numpy as np
-        iters_assumed = int(np.load(gp)["iterations"])
-    vals = []
-    t_all = time.perf_counter()
-    for k in range(args.warmup + args.steps):
-        b = oracle_baseline(cfg, names, iters_assumed, sample_solves=1)
-        if k >= args.warmup:
-            vals.append(b)
-    dt = time.perf_counter() - t_all
-    v = sum(x["value"] for x in vals) / len(vals)
-    out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "applies/s", "n_gpus": ws,
-           "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": round(1e3 * sum(x["oracle_time_to_solution_s"] for x in vals) / len(vals), 1),
+    t = len(names)
+    tp0 = time.perf_counter()
+    A = p1.assemble(cfg)
+    t_asm = time.perf_counter() - tp0
+    tf0 = time.perf_counter()
+    precs = sweep.make_preconditioners(cfg, A, names)
+    t_fac = time.perf_counter() - tf0
+    r = random_vector(cfg.n, 78)
+
+    def step():
+        for P in precs:
+            P.apply(r)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    cpu0 = time.process_time()
+    for _ in range(args.steps):
+        s0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - s0)
+    cores = (time.process_time() - cpu0) / sum(times)   # threads actually busy (process CPU time / wall)
+    ms = 1e3 * sum(times) / len(times)
+    value = t / (ms / 1e3)
+    del precs
+    # t-process mode: one worker per direction, the t applies run concurrently
+    par = None
+    try:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        ctx = mp.get_context("fork")
+        pools = [ProcessPoolExecutor(1, mp_context=ctx, initializer=_ref_worker_init, initargs=(args.config, nm))
+                 for nm in names]
+        w0 = time.perf_counter()
+        for f in [pl.submit(_ref_worker_apply, 0) for pl in pools]:
+            f.result()          # first call includes each worker's setup
+        t_par_setup = time.perf_counter() - w0
+        pt = []
+        for _ in range(args.steps):
+            s0 = time.perf_counter()
+            for f in [pl.submit(_ref_worker_apply, 0) for pl in pools]:
+                f.result()
+            pt.append(time.perf_counter() - s0)
+        for pl in pools:
+            pl.shutdown()
+        par = {"value": round(t / (sum(pt) / len(pt)), 4), "unit": "applies/s", "processes": t,
+               "ms_per_step": round(1e3 * sum(pt) / len(pt), 1), "setup_plus_first_apply_s": round(t_par_setup, 1)}
+    except Exception as e:  # pragma: no cover - host without fork / memory
+        par = {"unavailable": str(e)[:200]}
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "applies/s", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 complex)",
            "data": "synthetic (helm_inputs seeded recipe of " + cfg.name + ")",
-           "config": {"workload": f"{cfg.name}: same workload as the GPU arm; CPU oracle (numpy/scipy splu)",
+           "config": {"workload": f"{cfg.name}: P1 {cfg.nx}x{cfg.ny} k={cfg.omega:g}, N={cfg.n_strips} strips "
+                                  f"l={cfg.overlap}, t={t} ({'+'.join(names)}); CPU oracle (numpy/scipy splu); "
+                                  "step = one batched t-direction sweep apply, factor sets built before timing",
                       "n_unknowns": cfg.n},
-           "cpu_baseline": {"value": round(v, 6), "unit": "applies/s", "cores": 1, "kind": "oracle",
-                            "sample": vals[-1]["sample"] + f"; assumes {iters_assumed} iterations"},
-           "e2e": {"value": round(v, 6), "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "wall_s": round(dt, 1)}
+           "cpu_baseline": {"value": round(value, 5), "unit": "applies/s", "cores": round(cores, 2), "kind": "oracle",
+                            "sample": f"per step: {t} double sweeps x {2 * cfg.n_strips - 1} strip solves on the full "
+                                      f"{cfg.name} grid, serial (paper-like, P:L241); untimed preparation: assembly "
+                                      f"{t_asm:.1f} s + splu factor sets of both axes {t_fac:.1f} s",
+                            "host": host_info()},
+           "t_process_mode": par,
+           "oracle_setup_s": {"assembly": round(t_asm, 2), "factor_both_axes": round(t_fac, 2)},
+           "e2e": {"value": round(value, 5), "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
 

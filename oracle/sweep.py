@@ -31,6 +31,7 @@ import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
+from . import fd5
 from . import p1
 from . import strips as st_mod
 
@@ -39,11 +40,14 @@ class StripSolver:
     """One strip's local operator: either SuperLU of A_s (D7) or, in exact-Schur
     mode, a dense LU of the exact Schur complement (D12)."""
 
-    def __init__(self, cfg, axis, strip, A, exact_schur=False):
+    def __init__(self, cfg, axis, strip, A, exact_schur=False, disc="p1"):
         self.strip = strip
         nodes = strip.nodes
         if not exact_schur:
-            Atilde = st_mod.local_matrix_global(cfg, axis, strip)
+            if disc == "fd5":    # five-point rows, ghost-point Robin interface rows (oracle/fd5.py)
+                Atilde = fd5.local_matrix_global(cfg, axis, strip, A)
+            else:                # P1 strip assembly with interface impedance edges (D7)
+                Atilde = st_mod.local_matrix_global(cfg, axis, strip)
             self.Atilde = Atilde
             self.As = st_mod.restrict(Atilde, nodes)
             self.lu = spla.splu(self.As.tocsc())
@@ -79,7 +83,7 @@ class SweepPreconditioner:
     LR, RL, BT, TB), built once ("factored once") and applied many times."""
 
     def __init__(self, cfg, A, axis, order, n_strips, overlap, double=True,
-                 gather="recent", exact_schur=False, solvers_from=None):
+                 gather="recent", exact_schur=False, solvers_from=None, disc="p1"):
         self.cfg = cfg
         self.axis = axis
         self.order = order
@@ -93,7 +97,7 @@ class SweepPreconditioner:
             assert all(np.array_equal(a.nodes, b.nodes) for a, b in zip(solvers_from.strips, self.strips))
             self.solvers = solvers_from.solvers
         else:
-            self.solvers = [StripSolver(cfg, axis, s, A, exact_schur) for s in self.strips]
+            self.solvers = [StripSolver(cfg, axis, s, A, exact_schur, disc) for s in self.strips]
         N = n_strips
         self.sigma = list(range(N)) if order == 0 else list(range(N - 1, -1, -1))
         # "prev" interface of a strip = the side facing sigma's predecessor
@@ -177,15 +181,17 @@ DIRS = {"LRL": (0, 0, True), "RLR": (0, 1, True), "BTB": (1, 0, True), "TBT": (1
 
 
 def make_preconditioner(cfg, A, name, n_strips=None, overlap=None, gather="recent",
-                        exact_schur=False, solvers_from=None):
+                        exact_schur=False, solvers_from=None, disc="p1"):
     """``solvers_from``: an existing preconditioner on the same strips (same axis,
-    N, overlap) whose factored strip solvers are reused -- no arithmetic change."""
+    N, overlap) whose factored strip solvers are reused -- no arithmetic change.
+    ``disc``: "p1" (the hot path, D4/D7) or "fd5" (the paper's five-point
+    scheme, oracle/fd5.py; A must then be fd5.assemble(cfg))."""
     axis, order, double = DIRS[name]
     return SweepPreconditioner(cfg, A, axis, order,
                                cfg.n_strips if n_strips is None else n_strips,
                                cfg.overlap if overlap is None else overlap,
                                double=double, gather=gather, exact_schur=exact_schur,
-                               solvers_from=solvers_from)
+                               solvers_from=solvers_from, disc=disc)
 
 
 def make_preconditioners(cfg, A, names, **kw):
