@@ -42,6 +42,15 @@
 #ifndef HELM_DUAL_SNPOS
 #define HELM_DUAL_SNPOS 1   // where the next block's entries are read (see step(); 1 = interleaved with the FMAs)
 #endif
+#ifndef HELM_DUAL_XSYM
+#define HELM_DUAL_XSYM 0    // 1: read only the upper block triangle of X (each block by its two users)
+#endif
+#ifndef HELM_DUAL_XCH
+#define HELM_DUAL_XCH 4     // 32-column chunks per row in flight in the X mat-vec (4 rows per warp)
+#endif
+#ifndef HELM_DUAL_XTU
+#define HELM_DUAL_XTU 4     // rows in flight per lane in the transposed X part (XSYM)
+#endif
 #ifndef HELM_DUAL_RHS_TMA
 #define HELM_DUAL_RHS_TMA 0   // stage the next RHS by bulk copies (1) or per-element cp.async (0)
 #endif
@@ -53,6 +62,7 @@ constexpr int WM = 40;    // vector stride
 constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
 constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA producer warps
 }  // namespace dualk
+constexpr int kXpartElems = 10 * dualk::WM;   // <= 10 consumer warps
 
 // per-CTA cycle counters (tools/prof_sweep.py) only in the -DHELM_DUAL_PROF build
 // (python -m paper_2408_11929_b200.build --prof); the per-step sub-phase counters
@@ -173,7 +183,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* fb = xa + A.vec_elems;                      // chain B phase 3
   cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi (row stride wmax)
   cplx* bne = bcr + A.vec_elems;
-  cplx* gsm_own = bne + A.vec_elems + 7 * A.mmax;  // GSEP: after cs / cps / tcs
+  cplx* xpart = bne + A.vec_elems + 7 * A.mmax;    // [consumer warps][WM] partial sums of the transposed X part
+  cplx* gsm_own = xpart + kXpartElems;              // GSEP: after cs / cps / tcs / xpart
   cplx* gsm = GSEP ? gsm_own : xa;                  // separator RHS g (K x w), xa is dead before phase 3
   cplx* cs = bne + A.vec_elems;                     // [mmax] corrections formed by the last epilogue (next RHS)
   cplx* cps = cs + A.mmax;                          // [mmax] forward-pass corr_prev rows (backward RHS), staged
@@ -443,13 +454,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     if (p < P - 1 && tid < 32) {
-      // stream this CTA's rows of the separator inverse (w rows of stride x_ld,
-      // contiguous) into L2 while the all-gather completes; the mat-vec reads L2
+      // stream this CTA's part of the UPPER block triangle of the separator inverse
+      // (row r of block row p, columns p w .. K w) into L2 while the all-gather
+      // completes; the mat-vec reads it from L2, and so does CTA k > p, which uses
+      // block (p, k) transposed (X = R^{-1} is complex symmetric)
       const long ld = x_ld(K, w);
-      const char* xp = reinterpret_cast<const char*>(tab[i].xinv + (long)p * w * ld);
-      const long bytes = (long)w * ld * (long)sizeof(cplx);
-      for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
-        dprefetch_l2(xp + o, (uint32_t)(bytes - o < 32768L ? bytes - o : 32768L), pol_first);
+      const int kc = HELM_DUAL_XSYM ? p : 0;   // first column block read from block row p
+      const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(cplx));
+      for (int r = tid; r < w; r += 32)
+        dprefetch_l2(tab[i].xinv + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
     }
     // publish this segment's contributions to its two separator right-hand sides:
     //   yb[0..w)   = U_{lo-1} x0_lo   (enters g_{p-1}),  yb[wmax..) = U_hi^T x0_hi  (enters g_p)
@@ -540,7 +553,11 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       }
     }
     cbar();
-    // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
+    // x_p = X_p g with X = R^{-1} complex symmetric: only the upper block triangle
+    // is read, each of its blocks by its two users in the same stage (the second
+    // read hits L2), so the separator-inverse HBM stream is halved:
+    //   normal part      sum_{k >= p} X[p][r][k w + j] g_k[j]   (row r of block row p)
+    //   transposed part  sum_{k <  p} X[k][i][p w + r] g_k[i]   (= X[p][r][k w + i])
     const long long cx0 = pclk();
     pacc(14, cx0 - cg0);
     const long Kw = (long)K * w, xld = x_ld(K, w);
@@ -550,6 +567,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #else
     if (p < P - 1) {
 #endif
+      const long c0 = HELM_DUAL_XSYM ? (long)p * w : 0;
+      constexpr int XCH = HELM_DUAL_XCH;
+      // normal part: 4 rows per warp, lanes over the columns, 4 XCH loads in flight per lane
       for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
         const cplx* Xr[4];
         bool ok[4];
@@ -559,17 +579,17 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
         }
         cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-        for (long jj = lane; jj < Kw; jj += 128) {
-          cplx xv[4][4], gv[4];
+        for (long jj = c0 + lane; jj < Kw; jj += 32 * XCH) {
+          cplx xv[4][XCH], gv[XCH];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
+          for (int v = 0; v < XCH; ++v) {
             const bool in = jj + 32 * v < Kw;
             gv[v] = in ? gsm[jj + 32 * v] : cmk(0, 0);
 #pragma unroll
             for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ld_cg_hint(Xr[u] + jj + 32 * v, pol_first) : cmk(0, 0);
           }
 #pragma unroll
-          for (int v = 0; v < 4; ++v)
+          for (int v = 0; v < XCH; ++v)
 #pragma unroll
             for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
         }
@@ -583,7 +603,40 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           if (lane == 0 && ok[u]) xhi[rb + u] = acc[u];
         }
       }
+      // transposed part: rows (k, i), k < p, of the blocks (k, p), lanes over r;
+      // 4 rows in flight per lane, per-warp partial sums combined in a fixed order
+      constexpr int XTU = HELM_DUAL_XTU;
+      cplx t0 = cmk(0, 0), t1 = cmk(0, 0);
+      const int nrow = HELM_DUAL_XSYM ? p * w : 0;
+      for (int e0 = cw; e0 < nrow; e0 += XTU * ncw) {
+        cplx xa0[XTU], xa1[XTU], gv[XTU];
+#pragma unroll
+        for (int u = 0; u < XTU; ++u) {
+          const int e = e0 + u * ncw;
+          const bool ok = e < nrow;
+          const cplx* row = tab[i].xinv + (long)(ok ? e : 0) * xld + c0;   // row (k, i) = global row e = k w + i
+          xa0[u] = (ok && lane < w) ? ld_cg_hint(row + lane, pol_first) : cmk(0, 0);
+          xa1[u] = (ok && lane + 32 < w) ? ld_cg_hint(row + lane + 32, pol_first) : cmk(0, 0);
+          gv[u] = ok ? gsm[e] : cmk(0, 0);                                   // g_k[i] = gsm[k w + i]
+        }
+#pragma unroll
+        for (int u = 0; u < XTU; ++u) {
+          cfma(t0, xa0[u], gv[u]);
+          cfma(t1, xa1[u], gv[u]);
+        }
+      }
+      if (HELM_DUAL_XSYM) {
+        xpart[cw * WM + lane] = t0;
+        if (lane + 32 < WM) xpart[cw * WM + lane + 32] = t1;
+      }
     }
+    cbar();
+    if (HELM_DUAL_XSYM && p < P - 1)
+      for (int r = tid; r < w; r += ncons) {
+        cplx acc = xhi[r];
+        for (int v = 0; v < ncw; ++v) acc = cadd(acc, xpart[v * WM + r]);
+        xhi[r] = acc;
+      }
     for (int e = tid; e < WM; e += ncons) {
       if (p == 0) xlo[e] = cmk(0, 0);
       if (p == P - 1) xhi[e] = cmk(0, 0);
@@ -704,6 +757,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         if (G == 1 && PH == 0) wb = bseg[(ci - 1) * bsc + row * bsq];
       }
       if (sub && act) ysub = yseg[ci * w + row];
+#ifdef HELM_DUAL_ABL_NOWOPS
+      wc = cmk(1e-3, 0); wn = cmk(1e-4, 0); wb = cmk(1e-5, 0); ysub = cmk(0, 0);   // ablation: no writer operand loads
+#endif
       cplx vv[KPL];
 #pragma unroll
       for (int c = 0; c < KPL; ++c) {
@@ -900,7 +956,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * (4 * NST + 4) +
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * (WM + pmax) + 256;
   const bool gsep = gsm_elems > vec_elems;
-  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + 7L * mmax_all + (gsep ? gsm_elems : 0));
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + 7L * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
   const void* kfun = gsep ? (const void*)k_sweep_dual<true> : (const void*)k_sweep_dual<false>;
   if (smem > (size_t)kDualSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections

@@ -1,0 +1,141 @@
+"""Pins of the oracle's five-point (FD5) paper-calibration mode (oracle/fd5.py,
+SURVEY §8(f) NEXT #1) against what the paper and the mathematics fix.  CPU only.
+
+* hand-derived ghost-point rows (SPEC helmholtz_fd examples, h = 1/4, k = 2);
+* O(h^2) convergence to a plane wave with matching impedance data (Eq. 1b);
+* the interface term of Eq. 4 (B = d/dn - i k) on a field whose
+  centred-difference derivative is known in closed form;
+* the diagonal similarity D A = (D A)^T that makes the scheme complex symmetric
+  up to row scaling (used by the DESIGN.md FD5 reading);
+* the PAPER'S OWN NUMBERS: MPGMRES iteration counts of LRL+BTB (and LRL) at
+  h = 2^-9 / 2^-8, k = 50, N = 8 (Table 1; Table 4).
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from helm_inputs import HelmConfig
+from oracle import fd5, krylov, p1, strips, sweep
+
+
+def fd5_cfg(n, k, N=8, overlap=1):
+    c = np.ones((n + 1, n + 1))
+    return HelmConfig(f"fd5_{n}_{k}", n, n, 1.0, 1.0, k, c, np.zeros_like(c, np.complex128), N, overlap,
+                      ["LRL", "BTB"])
+
+
+def row_dict(A, cfg, i, j):
+    r = A.getrow(p1.node(cfg, i, j))
+    return {int(c): complex(v) for c, v in zip(r.indices, r.data)}
+
+
+def test_fd5_closed_form_rows():
+    """h = 1/4, k = 2 (1/h^2 = 16): interior row 16 x 4, diagonal -64 + 4 = -60;
+    left edge (ghost u_-1 = u_1 + 2 i k h u_0): right 32, up / down 16,
+    diagonal -60 + 16i; corner (0, 0): right 32, up 32, diagonal -60 + 32i
+    (hand algebra, SPEC helmholtz_fd examples)."""
+    cfg = fd5_cfg(4, 2.0, N=1)
+    A = fd5.assemble(cfg)
+    nd = lambda i, j: int(p1.node(cfg, i, j))
+    assert row_dict(A, cfg, 2, 2) == {nd(2, 2): -60, nd(1, 2): 16, nd(3, 2): 16, nd(2, 1): 16, nd(2, 3): 16}
+    assert row_dict(A, cfg, 0, 2) == {nd(0, 2): -60 + 16j, nd(1, 2): 32, nd(0, 1): 16, nd(0, 3): 16}
+    assert row_dict(A, cfg, 0, 0) == {nd(0, 0): -60 + 32j, nd(1, 0): 32, nd(0, 1): 32}
+    assert row_dict(A, cfg, 4, 4) == {nd(4, 4): -60 + 32j, nd(3, 4): 32, nd(4, 3): 32}
+
+
+def test_fd5_plane_wave_second_order():
+    """u* = exp(i k (x cos 0.3 + y sin 0.3)), f = 0, impedance data
+    g = du*/dn - i k u* entering the ghost-eliminated rows as -(2/h) g (twice at
+    corners): the max-norm error decreases at order >= 1.9 (h = 2^-4 .. 2^-6, k = 10)."""
+    k, th = 10.0, 0.3
+    errs = []
+    for n in (16, 32, 64):
+        cfg = fd5_cfg(n, k, N=1)
+        A = fd5.assemble(cfg)
+        x, y = p1.node_xy(cfg)
+        u = np.exp(1j * k * (x * math.cos(th) + y * math.sin(th)))
+        ux, uy = 1j * k * math.cos(th) * u, 1j * k * math.sin(th) * u
+        b = np.zeros(cfg.n, dtype=np.complex128)
+        for mask, dn in ((np.isclose(x, 0), -ux), (np.isclose(x, 1), ux), (np.isclose(y, 0), -uy), (np.isclose(y, 1), uy)):
+            b[mask] += -(2.0 / cfg.h) * (dn[mask] - 1j * k * u[mask])
+        uh = spla.spsolve(A.tocsc(), b)
+        errs.append(np.max(np.abs(uh - u)))
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert min(orders) >= 1.9, (errs, orders)
+
+
+def test_fd5_interface_term_is_the_robin_operator():
+    """Eq. 4 on an interface: (Atilde_s - A) w on the interface rows equals
+    -(2/h) B(w), B(w) = dw/dn - i k w with the centred difference across the
+    interface line.  For w = exp(i k x) at a low (left) interface, outward normal
+    -x: B(w) = e^{i k x_a} (-i sin(k h) / h - i k) (closed form; SPEC trace_rhs)."""
+    cfg = fd5_cfg(16, 7.0, N=2)
+    A = fd5.assemble(cfg)
+    _, sts = strips.strips(cfg, 0, 2, 1)
+    st = sts[1]                               # its low interface line a = 7
+    At = fd5.local_matrix_global(cfg, 0, st, A)
+    x, y = p1.node_xy(cfg)
+    k, h = cfg.omega, cfg.h
+    w = np.exp(1j * k * x)
+    corr = (At - A) @ w
+    line = np.isclose(x, st.a * h) & (y > 0.5 * h) & (y < 1 - 0.5 * h)   # interface nodes off the physical boundary
+    B = np.exp(1j * k * st.a * h) * (-1j * math.sin(k * h) / h - 1j * k)
+    np.testing.assert_allclose(corr[line], -(2.0 / h) * B, rtol=1e-12)
+    # a constant field: B(1) = -i k
+    np.testing.assert_allclose(((At - A) @ np.ones(cfg.n))[line], -(2.0 / h) * (-1j * k), rtol=1e-12)
+
+
+@pytest.mark.parametrize("N", [1, 3])
+def test_fd5_diagonal_similarity_is_symmetric(N):
+    """D A = (D A)^T with D = 1 inside, 1/2 on boundary lines, 1/4 at corners
+    (the ghost rows couple inward with 2/h^2, the inward rows back with 1/h^2);
+    the same holds for every strip matrix with its interface lines counted as
+    boundary lines."""
+    cfg = fd5_cfg(12, 6.0, N=N)
+    A = fd5.assemble(cfg)
+    x, y = p1.node_xy(cfg)
+    d = np.where(np.isclose(x, 0) | np.isclose(x, 1), 0.5, 1.0) * np.where(np.isclose(y, 0) | np.isclose(y, 1), 0.5, 1.0)
+    S = (A.T.multiply(d)).T.tocsr()
+    assert abs(S - S.T).max() < 1e-9
+    _, sts = strips.strips(cfg, 0, N, 1)
+    for st in sts:
+        At = strips.restrict(fd5.local_matrix_global(cfg, 0, st, A), st.nodes)
+        xs = x[st.nodes]
+        ds = np.where(np.isclose(xs, st.a * cfg.h) | np.isclose(xs, st.b * cfg.h), 0.5, 1.0) * \
+             np.where(np.isclose(y[st.nodes], 0) | np.isclose(y[st.nodes], 1), 0.5, 1.0)
+        Ss = (At.T.multiply(ds)).T.tocsr()
+        assert abs(Ss - Ss.T).max() < 1e-9
+
+
+def _iters(cfg, names, gather):
+    A = fd5.assemble(cfg)
+    b = fd5.source(cfg)
+    precs = sweep.make_preconditioners(cfg, A, names, gather=gather, disc="fd5")
+    _, st = krylov.mpgmres(A, [P.apply for P in precs], b, tol=1e-6, maxit=60)
+    assert st.converged
+    return st.iterations
+
+
+@pytest.mark.parametrize("gather", ["recent", "core"])
+def test_fd5_paper_table4_h8(gather):
+    """Table 4, h = 2^-8, k = 50, N = 8: LRL+BTB takes 8 iterations."""
+    assert abs(_iters(fd5_cfg(256, 50.0), ["LRL", "BTB"], gather) - 8) <= 1
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("gather", ["recent", "core"])
+def test_fd5_paper_table1_k50(gather):
+    """Table 1 / Table 2 / Table 5, h = 2^-9
+    (513^2 = 263,169 unknowns), k = 50, N = 8, the paper's source
+    3e4 exp(-200 k |x - c|^2): LRL+BTB takes 9 iterations (oracle: 8 recent, 9 core)."""
+    assert abs(_iters(fd5_cfg(512, 50.0), ["LRL", "BTB"], gather) - 9) <= 1
+
+
+@pytest.mark.slow
+def test_fd5_paper_table1_lrl_core():
+    """Table 1, LRL alone at h = 2^-9, k = 50, N = 8: paper 20 iterations; the
+    oracle with the "core" gather takes 17 (the literal "recent" gather
+    stagnates, 87: DESIGN.md §3, reading A16)."""
+    assert abs(_iters(fd5_cfg(512, 50.0), ["LRL"], "core") - 20) <= 3

@@ -51,8 +51,8 @@ constexpr int NBLK = 256;   // blocks per chain stream (cycled): 256 x 12 KB x c
 
 // NCH chains per warp; NST ring stages per group; each stage holds NCH blocks.
 // MODE 0: next blocks' entries read between the FMAs (k_sweep_dual), MODE 1: just in time.
-template <int NCH, int NST, int MODE>
-__global__ void __launch_bounds__(2 * NW * 32 + 64, 1) k_step(int steps, const cplx* __restrict__ F, int pks,
+template <int NCH, int NST, int MODE, int NG = 2>
+__global__ void __launch_bounds__(NG * NW * 32 + 32 * NG, 1) k_step(int steps, const cplx* __restrict__ F, int pks,
                                                               long long* cyc, cplx* out) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int stage_elems = NCH * (pks + 8);
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(2 * NW * 32 + 64, 1) k_step(int steps, const c
   uint64_t* empty = full + 2 * NST;
   cplx* vbuf = (cplx*)(empty + 2 * NST);                  // [2 groups][NCH][2][WM]
   int* pkst = (int*)(vbuf + 2 * NCH * 2 * WM);
-  const int tid = threadIdx.x, gsz = NW * 32, ncons = 2 * gsz;
+  const int tid = threadIdx.x, gsz = NW * 32, ncons = NG * gsz;
   for (int r = tid; r < W; r += blockDim.x) pkst[r] = pk_start(r, W);
   for (int e = tid; e < 2 * NCH * 2 * WM; e += blockDim.x) vbuf[e] = make_double2(1e-3 * (e % 37), 1e-4);
   for (int e = tid; e < 2 * NST * NCH; e += blockDim.x) ring[(long)e * (pks + 8) + pks + 7] = make_double2(0, 0);
@@ -208,18 +208,18 @@ __global__ void __launch_bounds__(2 * NW * 32 + 64, 1) k_step(int steps, const c
   if (owned) out[(long)blockIdx.x * 512 + tid] = acc_out;
 }
 
-template <int NCH, int NST, int MODE>
+template <int NCH, int NST, int MODE, int NG = 2>
 void run(const char* name, int ctas, const cplx* F, int pks, long long* dcyc, cplx* dout) {
   const int steps = 2048;
   const int stage_elems = NCH * (pks + 8);
   size_t smem = 16ul * 2 * NST * stage_elems + 8 * 4 * NST + 16ul * 2 * NCH * 2 * WM + 4 * 64 + 256;
-  cudaFuncSetAttribute(k_step<NCH, NST, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_step<NCH, NST, MODE, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  k_step<NCH, NST, MODE><<<ctas, 2 * NW * 32 + 64, smem>>>(steps, F, pks, dcyc, dout);
+  k_step<NCH, NST, MODE, NG><<<ctas, NG * NW * 32 + 32 * NG, smem>>>(steps, F, pks, dcyc, dout);
   cudaEventRecord(e0);
-  k_step<NCH, NST, MODE><<<ctas, 2 * NW * 32 + 64, smem>>>(steps, F, pks, dcyc, dout);
+  k_step<NCH, NST, MODE, NG><<<ctas, NG * NW * 32 + 32 * NG, smem>>>(steps, F, pks, dcyc, dout);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -229,7 +229,7 @@ void run(const char* name, int ctas, const cplx* F, int pks, long long* dcyc, cp
   double avg = 0;
   for (int i = 0; i < ctas; ++i) avg += h[i];
   avg /= ctas;
-  const double bytes = (double)ctas * 2 * NCH * steps * pks * 16.0;
+  const double bytes = (double)ctas * NG * NCH * steps * pks * 16.0;
   printf("%-34s ctas=%3d  %6.0f cycles/step  %5.0f cycles/(chain-step per group)  %6.3f ms  %6.0f GB/s  err=%s\n", name,
          ctas, avg / steps, avg / steps / NCH, ms, bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
 }
@@ -247,13 +247,12 @@ int main() {
   cudaMalloc(&dcyc, 8 * 1024);
   cudaMalloc(&dout, 16L * 160 * 512);
   printf("pk_size(35) = %d entries (%d bytes)\n", pks, pks * 16);
-  for (int ctas : {1, 132, nsm}) {
-    run<1, 4, 0>("1 chain/warp NST4 prefetch", ctas, F, pks, dcyc, dout);
-    run<1, 4, 1>("1 chain/warp NST4 just-in-time", ctas, F, pks, dcyc, dout);
-    run<2, 2, 0>("2 chains/warp NST2 prefetch", ctas, F, pks, dcyc, dout);
-    run<2, 3, 0>("2 chains/warp NST3 prefetch", ctas, F, pks, dcyc, dout);
-    run<2, 3, 1>("2 chains/warp NST3 just-in-time", ctas, F, pks, dcyc, dout);
-    run<2, 4, 1>("2 chains/warp NST4 just-in-time", ctas, F, pks, dcyc, dout);
+  for (int ctas : {1, 136, nsm}) {
+    run<1, 4, 0>("2 groups x 1 chain NST4 prefetch", ctas, F, pks, dcyc, dout);
+    run<1, 4, 0, 1>("1 group x 1 chain NST4 prefetch", ctas, F, pks, dcyc, dout);
+    run<1, 6, 0, 1>("1 group x 1 chain NST6 prefetch", ctas, F, pks, dcyc, dout);
+    run<1, 4, 1, 1>("1 group x 1 chain NST4 just-in-time", ctas, F, pks, dcyc, dout);
+    run<2, 4, 1, 1>("1 group x 2 chains NST4 just-in-time", ctas, F, pks, dcyc, dout);
   }
   return 0;
 }
