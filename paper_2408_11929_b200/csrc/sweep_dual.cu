@@ -42,6 +42,9 @@
 #ifndef HELM_DUAL_SNPOS
 #define HELM_DUAL_SNPOS 1   // where the next block's entries are read (see step(); 1 = interleaved with the FMAs)
 #endif
+#ifndef HELM_DUAL_WOPS_LATE
+#define HELM_DUAL_WOPS_LATE 1   // 1: writer operands read after the FMAs (not before the input-vector loads)
+#endif
 #ifndef HELM_DUAL_XSYM
 #define HELM_DUAL_XSYM 0    // 1: read only the upper block triangle of X (each block by its two users)
 #endif
@@ -737,17 +740,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     // one block step with this block's entries in Sc; the next block's entries are
     // read into Sn while the reductions, the writer and the barrier of this step
     // run, so only the input-vector loads sit on the dependent path
-    auto step = [&](int js, cplx (&Sc)[KPL], cplx (&Sn)[KPL]) {
-      long long q0 = 0;
-      if (kProfStep && A.prof && tid == 0) q0 = pclk();
-      const int st = cseq % NST;
-      const int ci = up ? js : m - 1 - js;   // local block row
-      const bool last = js == m - 1;
-      const cplx* vin = myv + cur * WM;
-      // writer operands (independent of this step's result): couplings of the
-      // next input and, for the sweeps that subtract, the source row
-      constexpr bool cplus = (G == 0 && PH == 0) || (G == 1 && PH == 1);   // A1, B3: row ci+1 of the staged bands
-      cplx wc = cmk(0, 0), wn = cmk(0, 0), wb = cmk(0, 0), ysub = cmk(0, 0);
+    // writer operands (independent of this step's result): couplings of the
+    // next input and, for the sweeps that subtract, the source row
+    auto load_wops = [&](int ci, bool last, cplx& wc, cplx& wn, cplx& wb, cplx& ysub) {
+      constexpr bool cplus = (G == 0 && PH == 0) || (G == 1 && PH == 1);
       if (owned && !last) {
         const int crow = cplus ? ci + 1 : ci;
         wc = bcr[crow * bw + row];
@@ -759,6 +755,18 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (sub && act) ysub = yseg[ci * w + row];
 #ifdef HELM_DUAL_ABL_NOWOPS
       wc = cmk(1e-3, 0); wn = cmk(1e-4, 0); wb = cmk(1e-5, 0); ysub = cmk(0, 0);   // ablation: no writer operand loads
+#endif
+    };
+    auto step = [&](int js, cplx (&Sc)[KPL], cplx (&Sn)[KPL]) {
+      long long q0 = 0;
+      if (kProfStep && A.prof && tid == 0) q0 = pclk();
+      const int st = cseq % NST;
+      const int ci = up ? js : m - 1 - js;   // local block row
+      const bool last = js == m - 1;
+      const cplx* vin = myv + cur * WM;
+      cplx wc = cmk(0, 0), wn = cmk(0, 0), wb = cmk(0, 0), ysub = cmk(0, 0);
+#if !HELM_DUAL_WOPS_LATE
+      load_wops(ci, last, wc, wn, wb, ysub);
 #endif
       cplx vv[KPL];
 #pragma unroll
@@ -794,6 +802,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
       }
       cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
+#if HELM_DUAL_WOPS_LATE
+      load_wops(ci, last, wc, wn, wb, ysub);   // behind the input-vector loads in the LSU queue
+#endif
 #if HELM_DUAL_SNPOS == 0
       if (!last) load_S(Sn, cseq + 1);   // Sc is dead: Sn can take its registers
 #endif
