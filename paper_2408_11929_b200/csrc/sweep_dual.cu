@@ -45,6 +45,9 @@
 #ifndef HELM_DUAL_WOPS_LATE
 #define HELM_DUAL_WOPS_LATE 1   // 1: writer operands read after the FMAs (not before the input-vector loads)
 #endif
+#ifndef HELM_DUAL_GSRC
+#define HELM_DUAL_GSRC 1   // 1: the separator-row source is staged into the g area at the pre-actions
+#endif
 #ifndef HELM_DUAL_XSYM
 #define HELM_DUAL_XSYM 0    // 1: read only the upper block triangle of X (each block by its two users)
 #endif
@@ -525,6 +528,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
       (void)ld_acquire(&D_.cnt[0]);
     }
+#if HELM_DUAL_GSRC
+    cp_async_wait_all();   // the separator-row source staged at the pre-actions
+#endif
     cbar();
     pacc(4, pclk() - cw0);
     pacc(12, pclk() - cw0);
@@ -542,7 +548,11 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         const int k = ok ? e / w : 0, qq = ok ? e - k * w : 0;
         th[u] = ok ? ldcg(ybp + (long)k * 2 * D_.wmax + D_.wmax + qq) : cmk(0, 0);
         tl[u] = ok ? ldcg(ybp + (long)(k + 1) * 2 * D_.wmax + qq) : cmk(0, 0);
+#if HELM_DUAL_GSRC
+        gs[u] = ok ? gsm[e] : cmk(0, 0);                                    // source at the separator rows (staged)
+#else
         gs[u] = ok ? ldcg(D_.R + node_of(D_, a, sepr[k], qq)) : cmk(0, 0);   // source at the separator rows
+#endif
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -886,6 +896,18 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       mbar_wait(&sbar[1], i & 1);
       cbar();
       seg_rhs(i);
+#if HELM_DUAL_GSRC
+      {
+        // the source at the separator rows is constant during the solve: copy it into
+        // the g area now (free until the separator stage), off the stage's critical path
+        const int a = tab[i].a;
+        for (int e = tid; e < K * w; e += ncons) {
+          const int k = e / w, qq = e - k * w;
+          cp_async16(gsm + e, D_.R + node_of(D_, a, sepr[k], qq));
+        }
+        cp_async_commit();
+      }
+#endif
       cbar();
       for (int e = tid; e < w; e += ncons) {
         const int bsc = D_.axis == 0 ? w : 1;
