@@ -63,6 +63,21 @@ typedef struct {
  * Errors: HELM_EINVAL (nx, ny < 2, h <= 0), HELM_ENOMEM, HELM_ECUDA. */
 int helm_assemble(const helm_grid_desc* grid, void* stream, helm_problem_t* out);
 
+/* helm_assemble_fd5 -- the paper's own discretisation (paper-calibration
+ * mode): "the standard five-point finite difference
+ * approximation on a regular Cartesian grid" (§4) of Eq. 1a-1b,
+ *   A = Delta_h + k^2  (interior row (u_E + u_W + u_N + u_S - 4u)/h^2 + k^2 u),
+ * impedance rows by ghost-point elimination of the centred normal derivative
+ * through Eq. 1b (inward neighbour 2/h^2, + 2ik/h on the diagonal per boundary
+ * line; reading DESIGN.md §3 FD5).  Constant k = omega: c_nodes must be NULL.
+ * Stored as the complex-symmetric S = D A (D = 1/2 per boundary line the node
+ * lies on), whose diagonals helm_get_diagonals returns (NE = 0); helm_spmv
+ * applies A = D^{-1} S; helm_load_vector returns b = f; sweep_setup factors the
+ * strip matrices D_s A_s (interface lines eliminated like boundary lines,
+ * Eq. 4) and needs overlap >= 1.
+ * Errors: HELM_EINVAL (c_nodes given, nx, ny < 2, h <= 0), HELM_ENOMEM, HELM_ECUDA. */
+int helm_assemble_fd5(const helm_grid_desc* grid, void* stream, helm_problem_t* out);
+
 /* n = (nx+1)(ny+1), nx, ny of a problem.  Host-only query. */
 int helm_problem_info(helm_problem_t p, long* n, int* nx, int* ny);
 

@@ -27,7 +27,7 @@ STATUS = {0: "HELM_OK", 1: "HELM_EINVAL", 2: "HELM_EDIM", 3: "HELM_ESINGULAR", 4
 DIRECTIONS = {"LRL": (0, 0, 1), "RLR": (0, 1, 1), "BTB": (1, 0, 1), "TBT": (1, 1, 1),
               "LR": (0, 0, 0), "RL": (0, 1, 0), "BT": (1, 0, 0), "TB": (1, 1, 0)}
 
-EXPORTS = ["helm_assemble", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
+EXPORTS = ["helm_assemble", "helm_assemble_fd5", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
            "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve", "helm_problem_destroy",
            "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches", "helm_sweep_kernel_name",
            "helm_set_knob"]
@@ -68,6 +68,7 @@ def load():
     L = ctypes.CDLL(LIB_PATH)
     vp, i, d, l = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_long
     L.helm_assemble.argtypes = [ctypes.POINTER(_GridDesc), vp, ctypes.POINTER(vp)]
+    L.helm_assemble_fd5.argtypes = [ctypes.POINTER(_GridDesc), vp, ctypes.POINTER(vp)]
     L.helm_problem_info.argtypes = [vp, ctypes.POINTER(l), ctypes.POINTER(i), ctypes.POINTER(i)]
     L.helm_get_diagonals.argtypes = [vp, vp, vp]
     L.helm_load_vector.argtypes = [vp, vp, vp, vp]
@@ -90,7 +91,7 @@ def load():
     L.helm_sweep_kernel_name.restype = ctypes.c_char_p
     L.helm_set_knob.argtypes = [ctypes.c_char_p, i]
     L.helm_set_knob.restype = i
-    for name in ["helm_assemble", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
+    for name in ["helm_assemble", "helm_assemble_fd5", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
                  "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve"]:
         getattr(L, name).restype = i
     _lib = L
@@ -166,9 +167,10 @@ def _ptr(a, dtype, count=None, out=False):
 
 
 class Problem:
-    """helm_assemble: the P1 matrix of Eq. 1a-1b on the '/' mesh (device)."""
+    """helm_assemble: the P1 matrix of Eq. 1a-1b on the '/' mesh (device);
+    disc="fd5": helm_assemble_fd5, the paper's five-point scheme (c = 1)."""
 
-    def __init__(self, nx, ny, h, omega, c=None, stream=None):
+    def __init__(self, nx, ny, h, omega, c=None, stream=None, disc="p1"):
         L = load()
         self._keep = []
         cp = ctypes.c_void_p(0)
@@ -177,7 +179,11 @@ class Problem:
             self._keep.append(keep)
         desc = _GridDesc(nx, ny, h, omega, cp)
         handle = ctypes.c_void_p()
-        _check(L.helm_assemble(ctypes.byref(desc), _stream(stream), ctypes.byref(handle)), "helm_assemble")
+        if disc not in ("p1", "fd5"):
+            raise ValueError(f"unknown discretisation {disc!r}")
+        fn = L.helm_assemble_fd5 if disc == "fd5" else L.helm_assemble
+        _check(fn(ctypes.byref(desc), _stream(stream), ctypes.byref(handle)), fn.__name__)
+        self.disc = disc
         self.handle = handle
         self.nx, self.ny, self.h, self.omega = nx, ny, h, omega
         self.n = (nx + 1) * (ny + 1)

@@ -143,6 +143,24 @@ __global__ void k_assemble(GridView g, cplx* dC, cplx* dE, cplx* dN, cplx* dNE) 
   }
 }
 
+// Five-point scheme (the paper's own; DESIGN.md §3 FD5), constant k =
+// omega: A = Delta_h + k^2 with ghost-point impedance rows (Eq. 1b).  Stored as
+// the complex-symmetric S = D A (common.cuh fd5_d on the global grid) in the
+// same 4 diagonals (NE = 0); k_spmm applies A = D^{-1} S.
+__global__ void k_assemble_fd5(int nx, int ny, double h, double k, cplx* dC, cplx* dE, cplx* dN, cplx* dNE) {
+  const long n = (long)(nx + 1) * (ny + 1);
+  const double ih2 = 1.0 / (h * h);
+  for (long gi = blockIdx.x * (long)blockDim.x + threadIdx.x; gi < n; gi += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(gi % (nx + 1)), j = (int)(gi / (nx + 1));
+    const bool ie = i == 0 || i == nx, je = j == 0 || j == ny;
+    const double di = ie ? 0.5 : 1.0, dj = je ? 0.5 : 1.0;
+    dC[gi] = cmk(di * dj * (-4.0 * ih2 + k * k), di * dj * (2.0 * k / h) * ((ie ? 1 : 0) + (je ? 1 : 0)));
+    dE[gi] = i < nx ? cmk(dj * ih2, 0.0) : cmk(0, 0);
+    dN[gi] = j < ny ? cmk(di * ih2, 0.0) : cmk(0, 0);
+    dNE[gi] = cmk(0, 0);
+  }
+}
+
 // b = M1 f (D5): sum over the 6 triangles around node g of
 // (h^2/24) (2 f_g + f_o1 + f_o2)  (consistent P1 mass, unit coefficient).
 __global__ void k_load_vector(int nx, int ny, double h, const cplx* __restrict__ f, cplx* __restrict__ b) {
@@ -172,12 +190,14 @@ __global__ void k_load_vector(int nx, int ny, double h, const cplx* __restrict__
 // Y = A X for ncols columns; A complex symmetric stored as 4 upper diagonals.
 // One thread per row; the row's 4 stored coefficients (+3 mirrored) are read
 // once and applied to every column (SpMM: one matrix read serves t columns).
+// FD5 problems store S = D A: the row result is scaled by D^{-1} (fd5 = 1).
 template <int NC>
 __global__ void __launch_bounds__(256) k_spmm(long n, int nxp1, const cplx* __restrict__ dC,
                                               const cplx* __restrict__ dE, const cplx* __restrict__ dN,
                                               const cplx* __restrict__ dNE, const cplx* __restrict__ X,
-                                              cplx* __restrict__ Y, int ncols, long ld) {
+                                              cplx* __restrict__ Y, int ncols, long ld, int fd5) {
   const long s = nxp1;
+  const long nyl = n / nxp1 - 1;
   for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < n; g += (long)gridDim.x * blockDim.x) {
     cplx c0 = __ldg(dC + g);
     cplx e = __ldg(dE + g);
@@ -187,6 +207,11 @@ __global__ void __launch_bounds__(256) k_spmm(long n, int nxp1, const cplx* __re
     cplx so = g >= s ? __ldg(dN + g - s) : cmk(0, 0);
     cplx sw = g >= s + 1 ? __ldg(dNE + g - s - 1) : cmk(0, 0);
     const int nc = NC > 0 ? NC : ncols;
+    double dinv = 1.0;
+    if (fd5) {
+      const long i = g % s, j = g / s;
+      dinv = ((i == 0 || i == s - 1) ? 2.0 : 1.0) * ((j == 0 || j == nyl) ? 2.0 : 1.0);
+    }
 #pragma unroll
     for (int col = 0; col < (NC > 0 ? NC : 8); ++col) {
       if (col >= nc) break;
@@ -198,12 +223,13 @@ __global__ void __launch_bounds__(256) k_spmm(long n, int nxp1, const cplx* __re
       if (g >= 1) cfma(acc, w, __ldg(x + g - 1));
       if (g >= s) cfma(acc, so, __ldg(x + g - s));
       if (g >= s + 1) cfma(acc, sw, __ldg(x + g - s - 1));
-      Y[col * ld + g] = acc;
+      Y[col * ld + g] = fd5 ? cscale(acc, dinv) : acc;
     }
   }
 }
 
 int helm_spmm_dev(const helm_problem_s* p, const cplx* X, cplx* Y, int ncols, long ld, cudaStream_t st) {
+  const int fd5 = p->disc == HELM_DISC_FD5 ? 1 : 0;
   int threads = 256;
   long blocks = (p->n + threads - 1) / threads;
   if (blocks > 148L * 16) blocks = 148L * 16;
@@ -212,10 +238,10 @@ int helm_spmm_dev(const helm_problem_s* p, const cplx* X, cplx* Y, int ncols, lo
     const cplx* x = X + (long)c0 * ld;
     cplx* y = Y + (long)c0 * ld;
     switch (nc) {
-      case 1: k_spmm<1><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld); break;
-      case 2: k_spmm<2><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld); break;
-      case 4: k_spmm<4><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld); break;
-      default: k_spmm<0><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld); break;
+      case 1: k_spmm<1><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld, fd5); break;
+      case 2: k_spmm<2><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld, fd5); break;
+      case 4: k_spmm<4><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld, fd5); break;
+      default: k_spmm<0><<<blocks, threads, 0, st>>>(p->n, p->nx + 1, p->dC, p->dE, p->dN, p->dNE, x, y, nc, ld, fd5); break;
     }
     HELM_LAUNCH_CHECK();
   }
@@ -223,7 +249,22 @@ int helm_spmm_dev(const helm_problem_s* p, const cplx* X, cplx* Y, int ncols, lo
 }
 
 // ------------------------------------------------------------------ C ABI
+static int assemble_impl(const helm_grid_desc* gd, int disc, void* stream, helm_problem_t* out);
+
 extern "C" int helm_assemble(const helm_grid_desc* gd, void* stream, helm_problem_t* out) {
+  return assemble_impl(gd, HELM_DISC_P1, stream, out);
+}
+
+extern "C" int helm_assemble_fd5(const helm_grid_desc* gd, void* stream, helm_problem_t* out) {
+  if (gd && gd->c_nodes) {
+    helm_set_error("helm_assemble_fd5: the five-point mode has constant k = omega (c_nodes must be NULL)");
+    if (out) *out = nullptr;
+    return HELM_EINVAL;
+  }
+  return assemble_impl(gd, HELM_DISC_FD5, stream, out);
+}
+
+static int assemble_impl(const helm_grid_desc* gd, int disc, void* stream, helm_problem_t* out) {
   if (!gd || !out) { helm_set_error("null argument"); return HELM_EINVAL; }
   *out = nullptr;
   if (gd->nx < 2 || gd->ny < 2 || !(gd->h > 0.0) || !(gd->omega > 0.0)) {
@@ -237,9 +278,10 @@ extern "C" int helm_assemble(const helm_grid_desc* gd, void* stream, helm_proble
     return HELM_ECUDA;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  static long next_uid = 1;
+  static std::atomic<long> next_uid{1};
   helm_problem_s* p = new helm_problem_s();
   p->uid = next_uid++;
+  p->disc = disc;
   p->nx = gd->nx; p->ny = gd->ny; p->h = gd->h; p->omega = gd->omega;
   p->n = (long)(gd->nx + 1) * (gd->ny + 1);
   size_t vb = sizeof(cplx) * p->n;
@@ -271,7 +313,10 @@ extern "C" int helm_assemble(const helm_grid_desc* gd, void* stream, helm_proble
   GridView g{p->nx, p->ny, p->h, p->omega, p->c};
   long blocks = (p->n + 255) / 256;
   if (blocks > 148L * 8) blocks = 148L * 8;
-  k_assemble<<<blocks, 256, 0, st>>>(g, p->dC, p->dE, p->dN, p->dNE);
+  if (disc == HELM_DISC_FD5)
+    k_assemble_fd5<<<blocks, 256, 0, st>>>(p->nx, p->ny, p->h, p->omega, p->dC, p->dE, p->dN, p->dNE);
+  else
+    k_assemble<<<blocks, 256, 0, st>>>(g, p->dC, p->dE, p->dN, p->dNE);
   g_helm_launches++;
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -314,8 +359,13 @@ extern "C" int helm_load_vector(helm_problem_t p, const double* f, double* b, vo
   HELM_TRY(helm_stage_in(b, vb, false, st, sb));
   long blocks = (p->n + 255) / 256;
   if (blocks > 148L * 8) blocks = 148L * 8;
-  k_load_vector<<<blocks, 256, 0, st>>>(p->nx, p->ny, p->h, (const cplx*)sf.dev, (cplx*)sb.dev);
-  HELM_LAUNCH_CHECK();
+  if (p->disc == HELM_DISC_FD5) {
+    // five-point scheme: b = f at every node (the ghost-eliminated rows keep their source)
+    HELM_CUDA_TRY(cudaMemcpyAsync(sb.dev, sf.dev, vb, cudaMemcpyDeviceToDevice, st));
+  } else {
+    k_load_vector<<<blocks, 256, 0, st>>>(p->nx, p->ny, p->h, (const cplx*)sf.dev, (cplx*)sb.dev);
+    HELM_LAUNCH_CHECK();
+  }
   helm_stage_free(sf, st);
   HELM_TRY(helm_stage_out(sb, st));
   return HELM_OK;

@@ -120,6 +120,20 @@ __host__ __device__ inline int pk_index(int r, int k, int w) {
   return k >= r ? pk_start(r, w) + (k - r) : pk_start(k, w) + (r - k);
 }
 
+// ------------------------------------------------------------------ discretisations
+enum { HELM_DISC_P1 = 0, HELM_DISC_FD5 = 1 };
+// Transmission-correction stencil (D8) per interface node: kTcW coefficients on
+// the source solution at (c-1, qi), (c, qi), (c+1, qi), (c, qo), (c+dd, qo),
+// (c, qin): interface line qi, outer line qo, inner line qin of the destination
+// strip (the last one is zero for P1; FD5's centred normal derivative uses it).
+constexpr int kTcW = 6;
+// FD5 row scaling of a strip (or of the global) matrix: S = D A is complex
+// symmetric with d = 1/2 on each boundary line (physical or interface) the node
+// lies on (ghost rows couple inward with 2/h^2, the inward rows back with 1/h^2).
+__host__ __device__ __forceinline__ double fd5_d(int q, int w, int c, int nc) {
+  return ((q == 0 || q == w - 1) ? 0.5 : 1.0) * ((c == 0 || c == nc - 1) ? 0.5 : 1.0);
+}
+
 // ------------------------------------------------------------------ handles
 struct helm_problem_s {
   int nx, ny;
@@ -130,6 +144,7 @@ struct helm_problem_s {
   cplx* dE;
   cplx* dN;
   cplx* dNE;
+  int disc = 0;        // HELM_DISC_P1 (D4) or HELM_DISC_FD5 (five-point, the paper's own scheme)
   void* ws = nullptr;  // cached MPGMRES workspace (krylov.cu), grown on demand
   long uid = 0;        // unique id (factor-set sharing key; addresses can be reused)
 };
@@ -139,6 +154,7 @@ void helm_problem_free_ws(helm_problem_s* p);
 struct helm_sweep_s {
   helm_problem_s* prob;
   int axis, order, N, overlap, is_double, gather;
+  int disc;        // discretisation of the problem (HELM_DISC_P1 / HELM_DISC_FD5)
   int nc;          // cross rows per strip (ny+1 for axis 0, nx+1 for axis 1)
   int wmax;        // max nodes per block row over strips
   int P;           // segments per strip

@@ -46,6 +46,47 @@ struct StripGeo {
   int N, nc, wmax, axis;
 };
 
+// Five-point scheme (the paper's; reading DESIGN.md §3 FD5): the strip
+// matrix A_s has the global rows (u_E + u_W + u_N + u_S - 4 u)/h^2 + k^2 u with
+// ghost-point Robin elimination (Eq. 1b / Eq. 4: inward neighbour 2/h^2,
+// + 2ik/h on the diagonal) on every boundary line of the strip, physical or
+// interface.  Stored: S_s = D_s A_s (complex symmetric), D_s = fd5_d:
+//   S(p,p) = d_p (-4/h^2 + k^2 + 2ik/h [q edge] + 2ik/h [c edge])
+//   S(p, along) = dc(c)/h^2,  S(p, cross) = dq(q)/h^2,  no diagonal coupling.
+// The correction (Atilde_s - A) v on an interface row is
+//   (1/h^2) v(inner line) + (2ik/h) v(interface line) - (1/h^2) v(outer line),
+// unscaled (the kernels scale source + corrections by D_s together).
+__global__ void k_strip_bands_fd5(GridView g, StripGeo sg, cplx* dg, cplx* al, cplx* cr, cplx* ne, cplx* tc) {
+  const int s = blockIdx.y;
+  const int w = sg.w[s];
+  const int nc = sg.nc;
+  const double ih2 = 1.0 / (g.h * g.h), k = g.omega;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nc * sg.wmax; e += gridDim.x * blockDim.x) {
+    int c = e / sg.wmax, q = e % sg.wmax;
+    long idx = ((long)s * nc + c) * sg.wmax + q;
+    if (q >= w) {
+      dg[idx] = al[idx] = cr[idx] = ne[idx] = cmk(0, 0);
+      continue;
+    }
+    const bool qe = q == 0 || q == w - 1, ce = c == 0 || c == nc - 1;
+    const double dq = qe ? 0.5 : 1.0, dc = ce ? 0.5 : 1.0;
+    dg[idx] = cmk(dq * dc * (-4.0 * ih2 + k * k), dq * dc * (2.0 * k / g.h) * ((qe ? 1 : 0) + (ce ? 1 : 0)));
+    al[idx] = (q + 1 < w) ? cmk(dc * ih2, 0.0) : cmk(0, 0);
+    cr[idx] = (c + 1 < nc) ? cmk(dq * ih2, 0.0) : cmk(0, 0);
+    ne[idx] = cmk(0, 0);
+  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nc; e += gridDim.x * blockDim.x) {
+    int side = e / nc, c = e % nc;
+    cplx* o = tc + (((long)s * 2 + side) * nc + c) * kTcW;
+    bool has = side == 0 ? (s > 0) : (s < sg.N - 1);
+    for (int kk = 0; kk < kTcW; ++kk) o[kk] = cmk(0, 0);
+    if (!has) continue;
+    o[1] = cmk(0.0, 2.0 * k / g.h);   // interface line
+    o[3] = cmk(-ih2, 0.0);            // outer line
+    o[5] = cmk(ih2, 0.0);             // inner line
+  }
+}
+
 __global__ void k_strip_bands(GridView g, StripGeo sg, cplx* dg, cplx* al, cplx* cr, cplx* ne, cplx* tc) {
   const int s = blockIdx.y;
   const int a = sg.a[s], w = sg.w[s], b = a + w - 1;
@@ -66,11 +107,13 @@ __global__ void k_strip_bands(GridView g, StripGeo sg, cplx* dg, cplx* al, cplx*
     ne[idx] = (c + 1 < nc && q + 1 < w) ? gen_ne(g, loc, sg.axis, pa, c) : cmk(0, 0);
   }
   // transmission-correction stencil (D8): (Atilde_s - A) on the interface rows.
-  // tc[((s*2 + side)*nc + c)*5 + k], k: 0 v(L,c-1), 1 v(L,c), 2 v(L,c+1), 3 v(O,c), 4 v(O,c+dd)
+  // tc[((s*2 + side)*nc + c)*kTcW + k], k: 0 v(L,c-1), 1 v(L,c), 2 v(L,c+1), 3 v(O,c),
+  // 4 v(O,c+dd), 5 v(I,c) (inner line: zero for P1)
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * nc; e += gridDim.x * blockDim.x) {
     int side = e / nc, c = e % nc;
-    cplx* o = tc + (((long)s * 2 + side) * nc + c) * 5;
+    cplx* o = tc + (((long)s * 2 + side) * nc + c) * kTcW;
     bool has = side == 0 ? (s > 0) : (s < sg.N - 1);
+    o[5] = cmk(0, 0);
     if (!has) {
       for (int k = 0; k < 5; ++k) o[k] = cmk(0, 0);
       continue;
@@ -822,10 +865,17 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     return HELM_EINVAL;
   }
   if (n_strips > n_axis) { helm_set_error("sweep_setup: more strips than cells"); return HELM_EINVAL; }
+  if (prob->disc == HELM_DISC_FD5 && n_strips > 1 && overlap < 1) {
+    // the FD5 transmission data use the centred difference across the interface
+    // line, i.e. the neighbour's values one line inside this strip
+    helm_set_error("sweep_setup: the five-point scheme needs overlap >= 1");
+    return HELM_EINVAL;
+  }
   helm_sweep_s* h = new helm_sweep_s();
   h->prob = prob;
   h->axis = axis; h->order = order; h->N = n_strips; h->overlap = overlap;
   h->is_double = is_double ? 1 : 0; h->gather = gather; h->nc = nc;
+  h->disc = prob->disc;
   h->a.resize(n_strips); h->b.resize(n_strips); h->w.resize(n_strips);
   h->own_lo.resize(n_strips); h->own_hi.resize(n_strips);
   int wmax = 0;
@@ -842,6 +892,16 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     }
   }
   h->wmax = wmax;
+  {
+    // the generic (w > 36) factorisation holds one w x w block in shared memory
+    const size_t need = sizeof(cplx) * ((size_t)wmax * wmax + wmax) + sizeof(int) * (wmax + 4) + 64;
+    if (wmax > kRowW && need > 227u * 1024u) {
+      helm_set_error("sweep_setup: strips of %d nodes exceed the factorisation's shared-memory block (max 119); "
+                     "use more strips", wmax);
+      delete h;
+      return HELM_EINVAL;
+    }
+  }
   int P = choose_segments(nc, n_segments);
   if (P < 1 || nc - (P - 1) < P) {
     helm_set_error("sweep_setup: %d segments do not fit %d cross rows", P, nc);
@@ -930,7 +990,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     alloc((void**)&h->d_al, sizeof(cplx) * bandN);
     alloc((void**)&h->d_cr, sizeof(cplx) * bandN);
     alloc((void**)&h->d_ne, sizeof(cplx) * bandN);
-    alloc((void**)&h->d_tc, sizeof(cplx) * n_strips * 2 * nc * 5);
+    alloc((void**)&h->d_tc, sizeof(cplx) * n_strips * 2 * nc * kTcW);
     alloc((void**)&h->d_fac, sizeof(cplx) * fac_total);
     alloc((void**)&h->d_red, sizeof(cplx) * std::max(red_total, 1L));
     if (want_xinv) alloc((void**)&h->d_xinv, sizeof(cplx) * xinv_total);
@@ -985,7 +1045,10 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   }
   {
     dim3 grid((nc * wmax + 255) / 256, n_strips);
-    k_strip_bands<<<grid, 256, 0, st>>>(g, sg, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc);
+    if (prob->disc == HELM_DISC_FD5)
+      k_strip_bands_fd5<<<grid, 256, 0, st>>>(g, sg, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc);
+    else
+      k_strip_bands<<<grid, 256, 0, st>>>(g, sg, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc);
     HELM_LAUNCH_CHECK();
   }
   // factorisation

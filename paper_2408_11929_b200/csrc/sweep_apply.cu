@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         cplx v = __ldg(D.R + node_of(D, a, c, q));
         if (has_prev && q == qp) v = cadd(v, D.corr_prev[(long)st * D.nc + c]);
         if (has_next && q == qn) v = cadd(v, D.corr_next[c]);
-        bseg[cl * w + q] = v;
+        bseg[cl * w + q] = cscale(v, rhs_scale(D, c, q, w));
       }
       for (int e = tid; e < (m + 1) * w; e += ncons) {
         int cl = e / w, q = e % w, c = lo - 1 + cl;
@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
           cplx v = __ldg(D.R + node_of(D, a, sk, q));
           if (st > 0 && q == qp) v = cadd(v, cpx[k]);
           if (bwd && q == qn) v = cadd(v, cnx[k]);
+          v = cscale(v, rhs_scale(D, sk, q, w));
           const cplx* yh = ybp + (long)k * 2 * D.wmax + D.wmax;     // y_k[hi]
           const cplx* yl = ybp + (long)(k + 1) * 2 * D.wmax;        // y_{k+1}[lo]
           cplx t = cmul(__ldg(cband + (long)hk * D.wmax + q), ldcg(yh + q));
@@ -700,6 +701,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         cplx v = __ldg(D.R + node_of(D, a, sk, q));
         if (st > 0 && q == qp) v = cadd(v, D.corr_prev[(long)st * D.nc + sk]);
         if (bwd && q == qn) v = cadd(v, cnx[k]);
+        v = cscale(v, rhs_scale(D, sk, q, w));
         const cplx* yh = D.yb + (long)k * 2 * D.wmax + D.wmax;     // y_k[hi]
         const cplx* yl = D.yb + (long)(k + 1) * 2 * D.wmax;        // y_{k+1}[lo]
         cplx t = cmul(__ldg(cband + (long)hk * D.wmax + q), ldcg(yh + q));
@@ -918,7 +920,7 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     DirArgs& D = A.d[d];
-    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc;
+    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc; D.disc = h->disc;
     D.nxp1 = prob->nx + 1; D.is_double = h->is_double; D.ntile_max = (h->wmax + R_t - 1) / R_t;
     D.a = h->d_a; D.w = h->d_w; D.own_lo = h->d_own_lo; D.own_hi = h->d_own_hi;
     D.seg_lo = h->d_seg_lo; D.seg_hi = h->d_seg_hi;

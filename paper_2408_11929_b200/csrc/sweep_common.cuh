@@ -8,6 +8,7 @@
 
 struct DirArgs {
   int axis, order, N, P, nc, nxp1, is_double, ntile_max;
+  int disc;              // HELM_DISC_P1 / HELM_DISC_FD5 (RHS row scaling of the FD5 strip systems)
   const int *a, *w, *own_lo, *own_hi, *seg_lo, *seg_hi;
   const cplx *cr, *ne;   // bands: U_c couplings, stride wmax per row, nc*wmax per strip
   const cplx* tc;        // transmission stencils [s][side][c][5]
@@ -145,11 +146,11 @@ __device__ __forceinline__ int next_side(const DirArgs& D) { return D.order == 0
 template <class XF>
 __device__ __forceinline__ cplx correction_aw(const DirArgs& D, int t, int at, int wt, int side, int c, int a_src,
                                               XF X) {
-  const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * 5;
+  const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * kTcW;
   const int bt = at + wt - 1;
-  int qi, qo, dd;
-  if (side == 0) { qi = at - a_src; qo = at - 1 - a_src; dd = -1; }
-  else { qi = bt - a_src; qo = bt + 1 - a_src; dd = 1; }
+  int qi, qo, qn, dd;
+  if (side == 0) { qi = at - a_src; qo = at - 1 - a_src; qn = at + 1 - a_src; dd = -1; }
+  else { qi = bt - a_src; qo = bt + 1 - a_src; qn = bt - 1 - a_src; dd = 1; }
   const cplx k0 = c >= 1 ? __ldg(k + 0) : cmk(0, 0);
   const cplx k1 = __ldg(k + 1);
   const cplx k2 = c + 1 < D.nc ? __ldg(k + 2) : cmk(0, 0);
@@ -165,21 +166,30 @@ __device__ __forceinline__ cplx correction_aw(const DirArgs& D, int t, int at, i
   cfma(acc, k0, x0);
   cfma(acc, k2, x2);
   cfma(acc, k4, x4);
+  if (D.disc == HELM_DISC_FD5) cfma(acc, __ldg(k + 5), X(c, qn));   // inner line (centred normal derivative)
   return acc;
 }
 
 template <class XF>
 __device__ __forceinline__ cplx correction(const DirArgs& D, int t, int side, int c, int a_src, XF X) {
-  const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * 5;
+  const cplx* k = D.tc + (((long)t * 2 + side) * D.nc + c) * kTcW;
   int at = D.a[t], bt = at + D.w[t] - 1;
-  int qi, qo, dd;
-  if (side == 0) { qi = at - a_src; qo = at - 1 - a_src; dd = -1; }
-  else { qi = bt - a_src; qo = bt + 1 - a_src; dd = 1; }
+  int qi, qo, qn, dd;
+  if (side == 0) { qi = at - a_src; qo = at - 1 - a_src; qn = at + 1 - a_src; dd = -1; }
+  else { qi = bt - a_src; qo = bt + 1 - a_src; qn = bt - 1 - a_src; dd = 1; }
   cplx acc = cmul(__ldg(k + 1), X(c, qi));
   cfma(acc, __ldg(k + 3), X(c, qo));
   if (c >= 1) cfma(acc, __ldg(k + 0), X(c - 1, qi));
   if (c + 1 < D.nc) cfma(acc, __ldg(k + 2), X(c + 1, qi));
   if (c + dd >= 0 && c + dd < D.nc) cfma(acc, __ldg(k + 4), X(c + dd, qo));
+  if (D.disc == HELM_DISC_FD5) cfma(acc, __ldg(k + 5), X(c, qn));
   return acc;
+}
+
+// RHS row scaling of the strip system actually factored: 1 for P1; for FD5 the
+// strip matrix is S_s = D_s A_s (complex symmetric), so A_s v = f is solved as
+// S_s v = D_s f (common.cuh fd5_d; the source and the corrections both scale)
+__device__ __forceinline__ double rhs_scale(const DirArgs& D, int c, int q, int w) {
+  return D.disc == HELM_DISC_FD5 ? fd5_d(q, w, c, D.nc) : 1.0;
 }
 

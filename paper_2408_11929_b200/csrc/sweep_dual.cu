@@ -189,12 +189,12 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* fb = xa + A.vec_elems;                      // chain B phase 3
   cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi (row stride wmax)
   cplx* bne = bcr + A.vec_elems;
-  cplx* xpart = bne + A.vec_elems + 7 * A.mmax;    // [consumer warps][WM] partial sums of the transposed X part
+  cplx* xpart = bne + A.vec_elems + (2 + kTcW) * A.mmax;   // [consumer warps][WM] partial sums of the transposed X part
   cplx* gsm_own = xpart + kXpartElems;              // GSEP: after cs / cps / tcs / xpart
   cplx* gsm = GSEP ? gsm_own : xa;                  // separator RHS g (K x w), xa is dead before phase 3
   cplx* cs = bne + A.vec_elems;                     // [mmax] corrections formed by the last epilogue (next RHS)
   cplx* cps = cs + A.mmax;                          // [mmax] forward-pass corr_prev rows (backward RHS), staged
-  cplx* tcs = cps + A.mmax;                         // [5 mmax] transmission coefficients of the next epilogue, staged
+  cplx* tcs = cps + A.mmax;                         // [kTcW mmax] transmission coefficients of the next epilogue, staged
 
   const int nsolve = n_solves(D_);
   for (int i = tid; i < nsolve; i += blockDim.x) {
@@ -337,16 +337,18 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       const int wt = i + 1 < nsolve ? tab[i + 1].w : D_.w[tdst];
       const int bt = at + wt - 1;
       const int qi = side == 0 ? at - a : bt - a, qo = side == 0 ? at - 1 - a : bt + 1 - a;
+      const int qin = side == 0 ? at + 1 - a : bt - 1 - a;
       const int dd = side == 0 ? -1 : 1;
       for (int c = lo + tid; c <= hi; c += ncons) {
         // D8 stencil with the coefficients staged in tcs (sweep_common.cuh correction_aw)
-        const cplx* kk = tcs + (c - lo) * 5;
+        const cplx* kk = tcs + (c - lo) * kTcW;
         const bool h4 = c + dd >= 0 && c + dd < D_.nc;
         cplx v = cmul(kk[1], X(c, qi));
         cfma(v, kk[3], X(c, qo));
         if (c >= 1) cfma(v, kk[0], X(c - 1, qi));
         if (c + 1 < D_.nc) cfma(v, kk[2], X(c + 1, qi));
         if (h4) cfma(v, kk[4], X(c + dd, qo));
+        if (D_.disc == HELM_DISC_FD5) cfma(v, kk[5], X(c, qin));
         target[c] = v;
         cs[c - lo] = v;
       }
@@ -417,9 +419,9 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     issue_copies(nr + 2, [&](int j, cplx*& dd, const cplx*& sr, uint32_t& by) {
       if (j < nr) { rhs_copy(i + 1, j, dd, sr, by); return; }
       dd = j == nr ? tcs : cps;
-      sr = j == nr ? D_.tc + (((long)(tdst < 0 ? 0 : tdst) * 2 + side) * D_.nc + lo) * 5
+      sr = j == nr ? D_.tc + (((long)(tdst < 0 ? 0 : tdst) * 2 + side) * D_.nc + lo) * kTcW
                    : D_.corr_prev + (long)step_of(D_, i + 1 < nsolve ? i + 1 : i) * D_.nc + lo;
-      by = j == nr ? (tdst >= 0 ? (uint32_t)(5 * m * sizeof(cplx)) : 0u) : (cpb ? (uint32_t)(m * sizeof(cplx)) : 0u);
+      by = j == nr ? (tdst >= 0 ? (uint32_t)(kTcW * m * sizeof(cplx)) : 0u) : (cpb ? (uint32_t)(m * sizeof(cplx)) : 0u);
     }, &sbar[0]);
   };
   auto stage_bands = [&](int i) {
@@ -448,6 +450,16 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       const int bsc = D_.axis == 0 ? w : 1;
       if (st > 0) bseg[cl * bsc + qp * bsq] = cadd(bseg[cl * bsc + qp * bsq], bwd ? cps[cl] : cs[cl]);
       if (bwd) bseg[cl * bsc + qn * bsq] = cadd(bseg[cl * bsc + qn * bsq], cs[cl]);
+      if (D_.disc == HELM_DISC_FD5) {
+        // FD5: the factored strip matrix is D_s A_s, so the RHS is D_s (source + corrections)
+        const int c = lo + cl;
+        if (c == 0 || c == D_.nc - 1) {
+          for (int qq = 0; qq < w; ++qq) bseg[cl * bsc + qq * bsq] = cscale(bseg[cl * bsc + qq * bsq], rhs_scale(D_, c, qq, w));
+        } else {
+          bseg[cl * bsc] = cscale(bseg[cl * bsc], 0.5);
+          bseg[cl * bsc + (w - 1) * bsq] = cscale(bseg[cl * bsc + (w - 1) * bsq], 0.5);
+        }
+      }
     }
   };
   // separator stage of solve i (after phase 1): all-gather of x0_lo / x0_hi, g,
@@ -562,6 +574,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         cplx v = gs[u];
         if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
         if (bwd && qq == qn) v = cadd(v, cnv[k]);
+        if (D_.disc == HELM_DISC_FD5) v = cscale(v, rhs_scale(D_, sepr[k], qq, w));
         gsm[e] = csub(csub(v, th[u]), tl[u]);
       }
     }
@@ -989,7 +1002,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * (4 * NST + 4) +
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * (WM + pmax) + 256;
   const bool gsep = gsm_elems > vec_elems;
-  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + 7L * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + (2L + kTcW) * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
   const void* kfun = gsep ? (const void*)k_sweep_dual<true> : (const void*)k_sweep_dual<false>;
   if (smem > (size_t)kDualSmemMax) return -1;
   // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
@@ -1026,7 +1039,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     DirArgs& D = A.d[d];
-    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc;
+    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc; D.disc = h->disc;
     D.nxp1 = prob->nx + 1; D.is_double = h->is_double; D.ntile_max = 1;
     D.a = h->d_a; D.w = h->d_w; D.own_lo = h->d_own_lo; D.own_hi = h->d_own_hi;
     D.seg_lo = h->d_seg_lo; D.seg_hi = h->d_seg_hi;

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant_
       cplx v = __ldg(D_.R + node_of(D_, a, c, qq));
       if (st > 0 && qq == qp) v = cadd(v, D_.corr_prev[(long)st * D_.nc + c]);
       if (bwd && qq == qn) v = cadd(v, D_.corr_next[c]);
-      bseg[cl * w + qq] = v;
+      bseg[cl * w + qq] = cscale(v, rhs_scale(D_, c, qq, w));
     }
     for (int e = tid; e < (m + 1) * w; e += ncons) {
       int cl = e / w, qq = e % w, c = lo - 1 + cl;
@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(32 * 8, 1) k_sweep_fast(const __grid_constant_
       cplx v = __ldg(D_.R + node_of(D_, a, sk, qq));
       if (st > 0 && qq == qp) v = cadd(v, cpv[k]);
       if (bwd && qq == qn) v = cadd(v, cnv[k]);
+      v = cscale(v, rhs_scale(D_, sk, qq, w));
       const cplx* yh = ybp + (long)k * 2 * D_.wmax + D_.wmax;
       const cplx* yl = ybp + (long)(k + 1) * 2 * D_.wmax;
       cplx tt = cmul(__ldg(cband + (long)hk * D_.wmax + qq), ldcg(yh + qq));
@@ -669,7 +670,7 @@ int sweep_apply_fast(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     DirArgs& D = A.d[d];
-    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc;
+    D.axis = h->axis; D.order = h->order; D.N = h->N; D.P = h->P; D.nc = h->nc; D.disc = h->disc;
     D.nxp1 = prob->nx + 1; D.is_double = h->is_double; D.ntile_max = 1;
     D.a = h->d_a; D.w = h->d_w; D.own_lo = h->d_own_lo; D.own_hi = h->d_own_hi;
     D.seg_lo = h->d_seg_lo; D.seg_hi = h->d_seg_hi;
