@@ -251,6 +251,12 @@ def run_ours(args):
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "model_bytes_per_launch": model_bytes,
                      "model": "SURVEY 8(d): sum over local solves of 16(2 n_c w^2 + 3 n_c w)"},
+        "setup_roofline": (lambda fl: {
+            "bound": "fp64", "achieved": round(fl / (setup_s / args.steps) / 1e12, 2), "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": round(fl / (setup_s / args.steps) / 1e12 / FP64_PEAK_TFLOPS, 4),
+            "flops_per_step": fl, "peak_source": "measured FP64 FMA throughput, tools/bench_fp64 (profiles/r02_fp64_peak.txt)",
+            "model": "both axes: sum over strips of 8 w^3 (3 n_c + 4 K + K (K-1)); setup wall time of the step's sweep_setup calls"})(
+            setup_flops(cfg, last["dirs_info"][0].n_segments)),
         "gpu_launches": launches,
         "clocks": clocks,
     }
@@ -270,6 +276,33 @@ def run_ours(args):
     if pg:
         pg.barrier()
         pg.destroy_process_group()
+
+
+FP64_PEAK_TFLOPS = 34.1   # measured: tools/bench_fp64 on this pool's B200 (profiles/r02_fp64_peak.txt)
+
+
+def setup_flops(cfg, n_segments):
+    """Algorithmic FP64 flops of the strip factorisations (sweep_setup) of BOTH
+    strip axes, complex multiply-add = 8 flops (DESIGN.md §5 "Setup"):
+      rows        n_c x (inverse S_c^-1, 8 w^3; bottom-up inverse, 8 w^3; the
+                  X[lo][hi] chain product, 8 w^3)                 = 24 w^3 n_c
+      separators  K x (Schur update, inverse, G_k, F_k: 4 x 8 w^3)  = 32 w^3 K
+      explicit R^-1 rows  K (K - 1) block products                 =  8 w^3 K (K - 1)
+    summed over the strips' widths w (interior strips cells + 2l + 1 nodes)."""
+    total = 0.0
+    for axis in (0, 1):
+        n_axis = cfg.nx if axis == 0 else cfg.ny
+        nc = (cfg.ny if axis == 0 else cfg.nx) + 1
+        base, extra = divmod(n_axis, cfg.n_strips)
+        p = [0]
+        for s in range(cfg.n_strips):
+            p.append(p[-1] + base + (1 if s < extra else 0))
+        K = n_segments - 1
+        for s in range(cfg.n_strips):
+            a, b = max(p[s] - cfg.overlap, 0), min(p[s + 1] + cfg.overlap, n_axis)
+            w = b - a + 1
+            total += 8.0 * w ** 3 * (3 * nc + 4 * K + K * (K - 1))
+    return total
 
 
 def run_e2e(args, cfg, names):

@@ -467,3 +467,22 @@ def test_binding_checks_tensor_dtype_and_size():
         prob.load_vector(to_dev(cfg.f.ravel()), torch.zeros(cfg.n, dtype=torch.complex64, device=DEV))
     with pytest.raises(ValueError):
         prob.load_vector(to_dev(cfg.f.ravel()), torch.zeros(cfg.n - 1, dtype=torch.complex128, device=DEV))
+
+
+@pytest.mark.parametrize("kernel", ["dual", "fast", "general"])
+def test_overlap2(kernel, knob):
+    """Overlap l = 2 (two extra mesh lines per internal boundary, SURVEY §8(f) #4,
+    P:L152 generalised): all four double sweeps vs the oracle on every kernel."""
+    knob("sweep_kernel", KERNEL_KNOB[kernel])
+    cfg = small_problem(60, 44, 18.0, seed=12, variable_c=True, n_strips=5, overlap=2)
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=5, overlap=2, n_segments=3) for nm in names]
+    R = random_vector(cfg.n, 29, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    Zh = Z.cpu().numpy()
+    for k, P in enumerate(_oracle_precs(cfg, A, names, n_strips=5, overlap=2)):
+        z = P.apply(R[k])
+        assert rel(Zh[k], z) <= 1e-10 and elementwise(Zh[k], z) <= 1e-10, (kernel, names[k])
