@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "directions"],
+                    help="N > 1: independent replicas per rank (default), or the direction-parallel "
+                         "solve (mpgmres_solve_dist: the t directions split over the ranks of a group, "
+                         "NCCL all-gather of the new columns each iteration)")
     return ap.parse_args()
 
 
@@ -155,6 +159,8 @@ def run_ours(args):
     cfg = make_config(args.config)
     names = cfg.dirs
     t = len(names)
+    dp = direction_groups(args, ws, rank, t, pg)       # None: replicas
+    my_names = names if dp is None else hs.partition_directions(names, dp["size"])[dp["rank"]]
     c_dev = torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev)
     f_dev = torch.tensor(cfg.f.ravel(), dtype=torch.complex128, device=dev)
     b = torch.zeros(cfg.n, dtype=torch.complex128, device=dev)
@@ -168,10 +174,14 @@ def run_ours(args):
     def step():
         prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, c_dev)
         t0 = time.perf_counter()
-        dirs = hs.make_sweeps(prob, names, n_strips=cfg.n_strips, overlap=cfg.overlap, streams=setup_streams)
+        dirs = hs.make_sweeps(prob, my_names, n_strips=cfg.n_strips, overlap=cfg.overlap, streams=setup_streams)
         t1 = time.perf_counter()
         prob.load_vector(f_dev, b)
-        _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol, maxit=cfg.maxit)
+        if dp is None:
+            _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol, maxit=cfg.maxit)
+        else:
+            _, st = hs.mpgmres_solve_dist(prob, dirs, dp["size"], dp["rank"], b, x, dp["cb"], tol=cfg.tol,
+                                          maxit=cfg.maxit)
         last.update(st=st, setup_s=t1 - t0, dirs_info=[d.info() for d in dirs])
         return st
 
@@ -203,7 +213,10 @@ def run_ours(args):
     sampler.mark(tw0, time.monotonic())
     launches = hs.kernel_launches() - l0
     clocks = sampler.stop()
-    total_ms, applies = reduce_over_ranks(ev0.elapsed_time(ev1), sum(its) * t, pg, dev)
+    # replicas: each rank's solve applies t preconditioners per iteration; direction-
+    # parallel: a group's solve applies t per iteration, t / size of them on each rank
+    local_t = t if dp is None else len(my_names)
+    total_ms, applies = reduce_over_ranks(ev0.elapsed_time(ev1), sum(its) * local_t, pg, dev)
     value = applies / (total_ms / 1e3)
     ms_step = total_ms / args.steps
     st = last["st"]
@@ -229,14 +242,17 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if (dp is not None and dp["size"] == ws) else "weak",
         "vs_baseline": None,
         "dtype": "c128 (f64 complex)",
         "data": "synthetic (helm_inputs seeded recipe of " + cfg.name + ")",
         "config": {"workload": f"{cfg.name}: P1 {cfg.nx}x{cfg.ny} k={cfg.omega:g}, N={cfg.n_strips} strips l={cfg.overlap}, "
                                f"t={t} ({'+'.join(names)}), MPGMRES tol {cfg.tol:g}, x0=0; step = assemble + "
                                "4 sweep setups + solve",
-                   "n_unknowns": cfg.n, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "n_unknowns": cfg.n,
+                   "parallelism": ("single GPU" if ws == 1 else f"replicas x{ws}" if dp is None else
+                                   f"direction-parallel: {ws // dp['size']} group(s) of {dp['size']} ranks "
+                                   f"x {t // dp['size']} direction(s), NCCL all-gather of Z and AZ per iteration"),
                    "l2_policy": "no flush: two factor sets (x / y strips) of %.2f GB in all >> 126 MB L2" % (
                        sum({i.axis: i.factor_bytes for i in last["dirs_info"]}.values()) / 1e9)},
         "time_to_solution_ms": round(ms_step, 3),
@@ -260,10 +276,10 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    if not args.no_north_star:
+    if not args.no_north_star and ws == 1:
         out["north_star"] = north_star_kernels(cfg, names, peak)
     if not args.no_e2e:
-        e2e = run_e2e(args, cfg, names)
+        e2e = run_e2e(args, cfg, names, my_names, dp)
         # replicas: the job's end-to-end time is the max over ranks, its work the sum
         e_ms, e_app = reduce_over_ranks(e2e.pop("_ms_total"), e2e.pop("_applies"), pg, dev)
         e2e["value"] = round(e_app / (e_ms / 1e3), 3)
@@ -305,7 +321,20 @@ def setup_flops(cfg, n_segments):
     return total
 
 
-def run_e2e(args, cfg, names):
+def direction_groups(args, ws, rank, t, pg):
+    """--mode directions: ranks form groups of `size` = the largest divisor of t
+    that divides ws (<= t); each group solves the problem with its directions
+    split over its ranks (mpgmres_solve_dist), the groups are replicas."""
+    if args.mode != "directions" or ws == 1:
+        return None
+    import paper_2408_11929_b200 as hs
+    size = max(d for d in range(1, t + 1) if t % d == 0 and ws % d == 0)
+    groups = [pg.new_group(ranks=list(range(g0, g0 + size))) for g0 in range(0, ws, size)]
+    grp = groups[rank // size]
+    return {"size": size, "rank": rank % size, "group": grp, "cb": hs.torch_allgather(grp)}
+
+
+def run_e2e(args, cfg, names, my_names=None, dp=None):
     """Same metric through the C ABI with HOST buffers: pinned host c and f are
     copied in, x is copied back, every step, inside the timed region.  Same
     --warmup / --steps as the device arm; timed with CUDA events on the
@@ -322,11 +351,17 @@ def run_e2e(args, cfg, names):
     stream = torch.cuda.current_stream()
     setup_streams = {0: torch.cuda.Stream().cuda_stream, 1: torch.cuda.Stream().cuda_stream}
 
+    my_names = my_names or names
+
     def step():
         prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, c_h.numpy())
-        dirs = hs.make_sweeps(prob, names, n_strips=cfg.n_strips, overlap=cfg.overlap, streams=setup_streams)
+        dirs = hs.make_sweeps(prob, my_names, n_strips=cfg.n_strips, overlap=cfg.overlap, streams=setup_streams)
         prob.load_vector(f_h.numpy(), b_d)
-        _, st = hs.mpgmres_solve(prob, dirs, b_d, x_h.numpy(), tol=cfg.tol, maxit=cfg.maxit)
+        if dp is None:
+            _, st = hs.mpgmres_solve(prob, dirs, b_d, x_h.numpy(), tol=cfg.tol, maxit=cfg.maxit)
+        else:
+            _, st = hs.mpgmres_solve_dist(prob, dirs, dp["size"], dp["rank"], b_d, x_h.numpy(), dp["cb"],
+                                          tol=cfg.tol, maxit=cfg.maxit)
         return st["iterations"]
 
     for _ in range(args.warmup):
@@ -340,7 +375,7 @@ def run_e2e(args, cfg, names):
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
     ms = e0.elapsed_time(e1)
-    return {"_ms_total": ms, "_applies": sum(its) * t, "unit": "applies/s",
+    return {"_ms_total": ms, "_applies": sum(its) * len(my_names), "unit": "applies/s",
             "h2d_bytes_per_step": 8 * cfg.n + 16 * cfg.n, "d2h_bytes_per_step": 16 * cfg.n,
             "host_wall_ms_per_step": round(wall / len(its) * 1e3, 3),
             "steps": len(its), "warmup": args.warmup,

@@ -167,6 +167,29 @@ int mpgmres_solve(helm_problem_t p, const helm_sweep_t* dirs, int t,
                   const double* b, double* x, double tol, int maxit,
                   mpgmres_stats* stats, void* stream);
 
+/* All-gather callback of the direction-parallel solve: every rank contributes
+ * `bytes` from `send` (device memory, on `stream`) and receives all ranks'
+ * contributions concatenated in rank order in `recv` (nranks * bytes; send ==
+ * recv + rank * bytes, i.e. in place).  Returns 0 on success.  The caller
+ * provides it (e.g. an NCCL all-gather over NVLink through torch.distributed);
+ * the library itself holds no communicator. */
+typedef int (*helm_allgather_fn)(void* ctx, const void* send, void* recv, long bytes, void* stream);
+
+/* mpgmres_solve_dist -- the direction-parallel MPGMRES of SURVEY §8(e): the
+ * t = nranks * t_local preconditioners are split over the ranks (one process
+ * per GPU), rank r applying global directions r*t_local .. r*t_local+t_local-1
+ * ("we can perform this part fully in parallel").  Per iteration each
+ * rank sweeps its directions and forms its columns of W = A Z, then the new Z
+ * and W columns are all-gathered (two callbacks); source selection, BCGS2 +
+ * block QR and the host least squares run replicated and deterministic, so all
+ * ranks hold the same x.  Every rank passes the same problem data, b, tol and
+ * maxit; local_dirs are this rank's sweep handles.  nranks == 1 is
+ * mpgmres_solve.  Errors: as mpgmres_solve, HELM_EINVAL for a bad rank /
+ * missing callback, HELM_ECUDA if the callback fails. */
+int mpgmres_solve_dist(helm_problem_t p, const helm_sweep_t* local_dirs, int t_local, int nranks, int rank,
+                       helm_allgather_fn allgather, void* ctx, const double* b, double* x,
+                       double tol, int maxit, mpgmres_stats* stats, void* stream);
+
 void helm_problem_destroy(helm_problem_t p);
 void sweep_destroy(helm_sweep_t s);
 const char* helm_strerror(int code);

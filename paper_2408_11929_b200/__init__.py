@@ -30,7 +30,7 @@ DIRECTIONS = {"LRL": (0, 0, 1), "RLR": (0, 1, 1), "BTB": (1, 0, 1), "TBT": (1, 1
 EXPORTS = ["helm_assemble", "helm_assemble_fd5", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
            "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve", "helm_problem_destroy",
            "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches", "helm_sweep_kernel_name",
-           "helm_set_knob"]
+           "helm_set_knob", "mpgmres_solve_dist"]
 
 
 class HelmError(RuntimeError):
@@ -55,6 +55,10 @@ class MPGMRESStats(ctypes.Structure):
 
 
 _lib = None
+
+# helm_allgather_fn (helmsweep.h): int (*)(void* ctx, const void* send, void* recv, long bytes, void* stream)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long,
+                                ctypes.c_void_p)
 
 
 def load():
@@ -91,6 +95,9 @@ def load():
     L.helm_sweep_kernel_name.restype = ctypes.c_char_p
     L.helm_set_knob.argtypes = [ctypes.c_char_p, i]
     L.helm_set_knob.restype = i
+    L.mpgmres_solve_dist.argtypes = [vp, ctypes.POINTER(vp), i, i, i, ALLGATHER_FN, vp, vp, vp, d, i,
+                                     ctypes.POINTER(MPGMRESStats), vp]
+    L.mpgmres_solve_dist.restype = i
     for name in ["helm_assemble", "helm_assemble_fd5", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
                  "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve"]:
         getattr(L, name).restype = i
@@ -338,6 +345,84 @@ def mpgmres_solve(problem, dirs, b, x, tol=1e-6, maxit=200, stream=None, raise_o
                                 ctypes.byref(st), _stream(stream))
     if code not in (HELM_OK, 6, 7) or (raise_on_noconv and code != HELM_OK):
         _check(code, "mpgmres_solve")
+    stats = {f: getattr(st, f) for f, _ in MPGMRESStats._fields_ if f != "history"}
+    stats["history"] = [hist[i] for i in range(st.iterations)]
+    stats["status"] = STATUS.get(code, code)
+    return k2, stats
+
+
+# ---------------------------------------------------------------- direction-parallel solve
+
+def partition_directions(names, nranks):
+    """Direction-parallel split: rank r owns the t / nranks
+    consecutive global directions r*t_local .. (r+1)*t_local - 1.  t must be a
+    multiple of nranks."""
+    t = len(names)
+    if nranks < 1 or t % nranks:
+        raise ValueError(f"{t} directions do not split over {nranks} ranks")
+    tl = t // nranks
+    return [list(names[r * tl:(r + 1) * tl]) for r in range(nranks)]
+
+
+class _Bytes:
+    """__cuda_array_interface__ / __array_interface__ view of raw bytes."""
+
+    def __init__(self, ptr, nbytes, device):
+        iface = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False), "version": 3}
+        if device:
+            iface["strides"] = None
+            iface["stream"] = None
+            self.__cuda_array_interface__ = iface
+        else:
+            self.__array_interface__ = iface
+
+
+def torch_allgather(group=None, device=True):
+    """An all-gather callback (helm_allgather_fn) over torch.distributed: NCCL
+    all_gather_into_tensor on the library's stream for device buffers (device
+    = True), or a gloo all_gather on host buffers (device = False, CPU tests).
+    Keep the returned object alive for the duration of the solve."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(ctx, send, recv, nbytes, stream):
+        try:
+            ws = dist.get_world_size(group)
+            if device:
+                s = torch.as_tensor(_Bytes(send, nbytes, True), device="cuda")
+                r = torch.as_tensor(_Bytes(recv, nbytes * ws, True), device="cuda")
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0))):
+                    dist.all_gather_into_tensor(r, s, group=group)
+            else:
+                s = torch.from_numpy(np.asarray(_Bytes(send, nbytes, False))).clone()
+                r = torch.from_numpy(np.asarray(_Bytes(recv, nbytes * ws, False)))
+                parts = [torch.empty_like(s) for _ in range(ws)]
+                dist.all_gather(parts, s, group=group)
+                r.copy_(torch.cat(parts))
+            return 0
+        except Exception:  # reported to the library as a failed collective
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    return ALLGATHER_FN(cb)
+
+
+def mpgmres_solve_dist(problem, local_dirs, nranks, rank, b, x, allgather, tol=1e-6, maxit=200, stream=None):
+    """mpgmres_solve_dist: this rank's directions local_dirs (global directions
+    rank*t_local ..), the new Z / W columns all-gathered by `allgather` (an
+    ALLGATHER_FN, e.g. torch_allgather()).  Returns (x, stats dict)."""
+    hist = (ctypes.c_double * maxit)()
+    st = MPGMRESStats()
+    st.history = ctypes.cast(hist, ctypes.POINTER(ctypes.c_double))
+    st.history_cap = maxit
+    n = problem.n
+    bp, k1 = _ptr(b, np.complex128, n)
+    xp, k2 = _ptr(x, np.complex128, n, out=True)
+    code = load().mpgmres_solve_dist(problem.handle, _dir_array(local_dirs), len(local_dirs), nranks, rank,
+                                     allgather, None, bp, xp, tol, maxit, ctypes.byref(st), _stream(stream))
+    if code not in (HELM_OK, 6, 7):
+        _check(code, "mpgmres_solve_dist")
     stats = {f: getattr(st, f) for f, _ in MPGMRESStats._fields_ if f != "history"}
     stats["history"] = [hist[i] for i in range(st.iterations)]
     stats["status"] = STATUS.get(code, code)

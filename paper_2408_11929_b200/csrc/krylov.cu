@@ -906,8 +906,16 @@ static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cuda
   return 1;
 }
 
-extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int t, const double* b_in,
-                             double* x_out, double tol, int maxit, mpgmres_stats* stats, void* stream) {
+// One MPGMRES solve.  Direction-parallel mode: this
+// rank applies only its t_local directions dirs[0..t_local) -- global directions
+// rank*t_local .. -- and the new Z and W = A Z columns of all ranks are
+// all-gathered through `gather` after the SpMM; everything else (source
+// selection, BCGS2 + block QR, the host least squares) runs replicated on every
+// rank from identical data, so every rank takes the same decisions.  gather ==
+// nullptr: single process (t_local == t).
+static int mpgmres_core(helm_problem_t prob, const helm_sweep_t* dirs, int t_local, int t, int rank,
+                        helm_allgather_fn gather, void* gctx, const double* b_in, double* x_out, double tol,
+                        int maxit, mpgmres_stats* stats, void* stream) {
   typedef std::complex<double> C;
   auto t0 = std::chrono::steady_clock::now();
   if (!prob || !dirs || !b_in || !x_out) { helm_set_error("mpgmres_solve: null argument"); return HELM_EINVAL; }
@@ -915,7 +923,7 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
     helm_set_error("mpgmres_solve: need 1 <= t <= 8, 0 < tol < 1, maxit >= 1");
     return HELM_EINVAL;
   }
-  for (int d = 0; d < t; ++d)
+  for (int d = 0; d < t_local; ++d)
     if (!dirs[d] || dirs[d]->prob->n != prob->n) { helm_set_error("mpgmres_solve: direction %d size mismatch", d); return HELM_EDIM; }
   cudaStream_t st = (cudaStream_t)stream;
   const long n = prob->n;
@@ -1014,15 +1022,25 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
       g_helm_launches++;
       src = Rsrc;
     }
-    // ---- a4: Z_k = [M_i^{-1} src_i], one batched launch
+    // ---- a4: Z_k = [M_i^{-1} src_i], one batched launch (this rank's directions)
     cplx* Zk = Z + nz * n;
+    const long off = (long)rank * t_local;   // first global direction of this rank
     cudaEventRecord(ev[0], st);
-    rc = sweep_apply_dev(dirs, t, src, ldr, Zk, n, st);
+    rc = sweep_apply_dev(dirs, t_local, ldr == 0 ? src : src + off * ldr, ldr, Zk + off * n, n, st);
     if (rc != HELM_OK) break;
     cudaEventRecord(ev[1], st);
-    // ---- a5: W = A Z_k
-    rc = helm_spmm_dev(prob, Zk, W, t, n, st);
+    // ---- a5: W = A Z_k (this rank's columns)
+    rc = helm_spmm_dev(prob, Zk + off * n, W + off * n, t_local, n, st);
     if (rc != HELM_OK) break;
+    if (gather) {
+      // direction-parallel: every rank receives all t new Z and W columns (in place)
+      const long bytes = (long)t_local * n * (long)sizeof(cplx);
+      if (gather(gctx, Zk + off * n, Zk, bytes, st) != 0 || gather(gctx, W + off * n, W, bytes, st) != 0) {
+        helm_set_error("mpgmres_solve_dist: all-gather callback failed at iteration %d", k);
+        rc = HELM_ECUDA;
+        break;
+      }
+    }
     cudaEventRecord(ev[2], st);
     // ---- a6: Gram diagonal of A Z_k (for ||A z_i||), BCGS2 against V_1..k, intra-block CGS2
     const int m = (int)mV;
@@ -1183,4 +1201,20 @@ extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int 
   if (exhausted) return HELM_EEXHAUSTED;
   if (!converged) return HELM_ENOCONV;
   return HELM_OK;
+}
+
+extern "C" int mpgmres_solve(helm_problem_t prob, const helm_sweep_t* dirs, int t, const double* b_in,
+                             double* x_out, double tol, int maxit, mpgmres_stats* stats, void* stream) {
+  return mpgmres_core(prob, dirs, t, t, 0, nullptr, nullptr, b_in, x_out, tol, maxit, stats, stream);
+}
+
+extern "C" int mpgmres_solve_dist(helm_problem_t prob, const helm_sweep_t* local_dirs, int t_local, int nranks,
+                                  int rank, helm_allgather_fn allgather, void* ctx, const double* b, double* x,
+                                  double tol, int maxit, mpgmres_stats* stats, void* stream) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || t_local < 1 || (nranks > 1 && !allgather)) {
+    helm_set_error("mpgmres_solve_dist: need 0 <= rank < nranks, t_local >= 1 and an all-gather callback");
+    return HELM_EINVAL;
+  }
+  return mpgmres_core(prob, local_dirs, t_local, t_local * nranks, rank, nranks > 1 ? allgather : nullptr, ctx, b, x,
+                      tol, maxit, stats, stream);
 }

@@ -234,6 +234,170 @@ void run(const char* name, int ctas, const cplx* F, int pks, long long* dcyc, cp
          ctas, avg / steps, avg / steps / NCH, ms, bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
 }
 
+
+// FP32 data path: factor blocks float2 (8 B per entry), input vector float2, FP32 FMAs
+__device__ __forceinline__ void cfmaf(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+template <int NST, int CONV>
+__global__ void __launch_bounds__(2 * NW * 32 + 64, 1) k_step32(int steps, const float2* __restrict__ F, int pks,
+                                                                long long* cyc, float2* out) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int stage_elems = pks + 8;
+  float2* ring = (float2*)sm;
+  uint64_t* full = (uint64_t*)(ring + 2 * NST * stage_elems);
+  uint64_t* empty = full + 2 * NST;
+  float2* vbuf = (float2*)(empty + 2 * NST);
+  double2* vbufd = (double2*)(vbuf + 2 * 2 * WM);
+  int* pkst = (int*)(vbufd + 2 * 2 * WM);
+  const int tid = threadIdx.x, gsz = NW * 32, ncons = 2 * gsz;
+  for (int r = tid; r < W; r += blockDim.x) pkst[r] = pk_start(r, W);
+  for (int e = tid; e < 2 * 2 * WM; e += blockDim.x) { vbuf[e] = make_float2(1e-3f * (e % 37), 1e-4f); vbufd[e] = make_double2(1e-3 * (e % 37), 1e-4); }
+  for (int e = tid; e < 2 * NST; e += blockDim.x) ring[(long)e * stage_elems + pks + 7] = make_float2(0, 0);
+  if (tid == 0) {
+    for (int e = 0; e < 2 * NST; ++e) { mbar_init(&full[e], 1); mbar_init(&empty[e], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= ncons) {
+    const int pg = (tid - ncons) >> 5;
+    if ((tid & 31) == 0) {
+      const uint32_t bytes = pks * sizeof(float2);
+      for (int f = 0; f < steps; ++f) {
+        const int st = f % NST;
+        if (f >= NST) mbar_wait(&empty[pg * NST + st], ((f / NST) - 1) & 1);
+        mbar_expect_tx(&full[pg * NST + st], bytes);
+        const float2* src = F + ((long)blockIdx.x * 2 + pg) * NBLK * pks + (long)(f % NBLK) * pks;
+        bulk_g2s(ring + ((long)pg * NST + st) * stage_elems, src, bytes, &full[pg * NST + st]);
+      }
+    }
+    return;
+  }
+  const int g = tid >= gsz ? 1 : 0, gtid = tid - g * gsz, wi = gtid >> 5, lane = tid & 31;
+  const int slot = lane & 7, q = lane >> 3;
+  const int row = 7 * wi + slot - 1;
+  const bool act = row >= 0 && row < W;
+  const bool owned = q == 0 && act && slot >= 1;
+  uint32_t off[KPL];
+#pragma unroll
+  for (int c = 0; c < KPL; ++c) {
+    const int k = q + 4 * c;
+    int idx = pks + 7;
+    if (act && k < W) idx = k >= row ? pkst[row] + (k - row) : pkst[k] + (row - k);
+    off[c] = idx * 8u;
+  }
+  const uint32_t rb = smem_u32(ring + (long)g * NST * stage_elems);
+  const uint32_t sbytes = stage_elems * 8u;
+  float2* myv = vbuf + g * 2 * WM;
+  double2* myvd = vbufd + g * 2 * WM;
+  int cur = 0;
+  long long t0 = clock64();
+  float accout = 0.f;
+  double accoutd = 0.0;
+  float2 S[2][KPL];
+  mbar_wait(&full[g * NST], 0);
+#pragma unroll
+  for (int c = 0; c < KPL; ++c) S[0][c] = lds64(rb + off[c]);
+  for (int s = 0; s < steps; s += 2) {
+#pragma unroll
+    for (int hb = 0; hb < 2; ++hb) {
+      const int ss = s + hb;
+      const int st = ss % NST;
+      const bool last = ss + 1 >= steps;
+      uint32_t sbn = 0;
+      if (!last) {
+        mbar_wait(&full[g * NST + (ss + 1) % NST], ((ss + 1) / NST) & 1);
+        sbn = rb + ((ss + 1) % NST) * sbytes;
+      }
+      if (CONV == 0) {
+        const float2* vin = myv + cur * WM;
+        float2 a0 = make_float2(0, 0), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) {
+          const float2 v = vin[q + 4 * c];
+          if ((c & 3) == 0) cfmaf(a0, S[hb][c], v);
+          else if ((c & 3) == 1) cfmaf(a1, S[hb][c], v);
+          else if ((c & 3) == 2) cfmaf(a2, S[hb][c], v);
+          else cfmaf(a3, S[hb][c], v);
+          if (!last) S[hb ^ 1][c] = lds64(sbn + off[c]);
+        }
+        float2 a = make_float2(a0.x + a1.x + a2.x + a3.x, a0.y + a1.y + a2.y + a3.y);
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, 16);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, 16);
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, 8);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, 8);
+        float2 nb;
+        nb.x = __shfl_up_sync(0xffffffffu, a.x, 1, 8);
+        nb.y = __shfl_up_sync(0xffffffffu, a.y, 1, 8);
+        if (owned) myv[(cur ^ 1) * WM + row] = make_float2(1e-2f * a.x - 1e-3f * nb.x, 1e-2f * a.y + 1e-3f * nb.y);
+        accout += a.x;
+      } else {
+        // fp32 factors, fp64 vector and accumulation (convert each entry)
+        const double2* vin = myvd + cur * WM;
+        double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+        for (int c = 0; c < KPL; ++c) {
+          const double2 v = vin[q + 4 * c];
+          const double2 sv = make_double2((double)S[hb][c].x, (double)S[hb][c].y);
+          if ((c & 3) == 0) cfma(a0, sv, v);
+          else if ((c & 3) == 1) cfma(a1, sv, v);
+          else if ((c & 3) == 2) cfma(a2, sv, v);
+          else cfma(a3, sv, v);
+          if (!last) S[hb ^ 1][c] = lds64(sbn + off[c]);
+        }
+        double2 a = make_double2(a0.x + a1.x + a2.x + a3.x, a0.y + a1.y + a2.y + a3.y);
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, 16);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, 16);
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, 8);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, 8);
+        double2 nb;
+        nb.x = __shfl_up_sync(0xffffffffu, a.x, 1, 8);
+        nb.y = __shfl_up_sync(0xffffffffu, a.y, 1, 8);
+        if (owned) myvd[(cur ^ 1) * WM + row] = make_double2(1e-2 * a.x - 1e-3 * nb.x, 1e-2 * a.y + 1e-3 * nb.y);
+        accoutd += a.x;
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory");
+      if (gtid == 0) mbar_arrive(&empty[g * NST + st]);
+      cur ^= 1;
+    }
+  }
+  long long t1 = clock64();
+  if (tid == 0) cyc[blockIdx.x] = t1 - t0;
+  if (owned) out[(long)blockIdx.x * 512 + tid] = make_float2(accout, (float)accoutd);
+}
+
+template <int NST, int CONV>
+void run32(const char* name, int ctas, const float2* F, int pks, long long* dcyc, float2* dout) {
+  const int steps = 2048;
+  size_t smem = 8ul * 2 * NST * (pks + 8) + 8 * 4 * NST + 8ul * 4 * WM + 16ul * 4 * WM + 4 * 64 + 256;
+  cudaFuncSetAttribute(k_step32<NST, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_step32<NST, CONV><<<ctas, 2 * NW * 32 + 64, smem>>>(steps, F, pks, dcyc, dout);
+  cudaEventRecord(e0);
+  k_step32<NST, CONV><<<ctas, 2 * NW * 32 + 64, smem>>>(steps, F, pks, dcyc, dout);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long h[160];
+  cudaMemcpy(h, dcyc, sizeof(long long) * ctas, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < ctas; ++i) avg += h[i];
+  avg /= ctas;
+  printf("%-40s ctas=%3d  %6.0f cycles/step  %6.3f ms  err=%s\n", name, ctas, avg / steps, ms,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -247,6 +411,13 @@ int main() {
   cudaMalloc(&dcyc, 8 * 1024);
   cudaMalloc(&dout, 16L * 160 * 512);
   printf("pk_size(35) = %d entries (%d bytes)\n", pks, pks * 16);
+  for (int ctas : {1, 132}) {
+    run<1, 4, 0>("fp64: 2 groups x 1 chain NST4 prefetch", ctas, F, pks, dcyc, dout);
+    run32<4, 0>("fp32 data path: 2 groups x 1 chain NST4", ctas, (const float2*)F, pks, dcyc, (float2*)dout);
+    run32<6, 0>("fp32 data path: 2 groups x 1 chain NST6", ctas, (const float2*)F, pks, dcyc, (float2*)dout);
+    run32<4, 1>("fp32 factors, fp64 vector+FMA NST4", ctas, (const float2*)F, pks, dcyc, (float2*)dout);
+    run32<6, 1>("fp32 factors, fp64 vector+FMA NST6", ctas, (const float2*)F, pks, dcyc, (float2*)dout);
+  }
   for (int ctas : {1, 136, nsm}) {
     run<1, 4, 0>("2 groups x 1 chain NST4 prefetch", ctas, F, pks, dcyc, dout);
     run<1, 4, 0, 1>("1 group x 1 chain NST4 prefetch", ctas, F, pks, dcyc, dout);
