@@ -398,6 +398,14 @@ def north_star_kernels(cfg, names, peak):
     stream = torch.cuda.current_stream()
     prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev))
     dirs = dict(zip(names, hs.make_sweeps(prob, names, n_strips=cfg.n_strips, overlap=cfg.overlap)))
+    # a batch of fewer directions leaves SMs free for more, shorter segments (P CTAs per
+    # direction): measured best P for C5 is 49 at t = 1, 41 at t = 2, 33 at t = 4
+    # (DESIGN.md §5); the t = 4 handles above use the automatic 33
+    seg_for_t = {1: 49, 2: 41}
+    extra = {t_: dict(zip(names[:1] if t_ == 1 else ["LRL", "BTB"],
+                          hs.make_sweeps(prob, ["LRL"] if t_ == 1 else ["LRL", "BTB"], n_strips=cfg.n_strips,
+                                         overlap=cfg.overlap, n_segments=seg_for_t[t_])))
+             for t_ in seg_for_t} if cfg.n_strips > 1 and cfg.nx >= 512 else {}
     # assembled nonzeros of the 7-point P1 stencil on the grid (7,346,177 for C5)
     nx, ny = cfg.nx, cfg.ny
     nnz = (nx + 1) * (ny + 1) + 2 * (nx * (ny + 1) + (nx + 1) * ny + nx * ny)
@@ -425,14 +433,16 @@ def north_star_kernels(cfg, names, peak):
             "frac_of_peak": round(model / (ms / 1e3) / 1e9 / peak, 4)}
     r = torch.tensor(random_vector(cfg.n, 6), device=dev)
     for combo in (["LRL"], ["LRL", "BTB"], ["LRL", "RLR", "BTB", "TBT"]):
-        ds = [dirs[nm] for nm in combo]
+        src = extra.get(len(combo), dirs)
+        ds = [src[nm] for nm in combo]
         Z = torch.zeros((len(ds), cfg.n), dtype=torch.complex128, device=dev)
         ms = timed(lambda: hs.sweep_apply(ds, r, Z, ldr=0), reps=10)
         model = sum(d.info().model_bytes_per_apply for d in ds)
         out[f"sweep_apply_t{len(ds)}"] = {
             "dirs": "+".join(combo), "ms": round(ms, 4), "applies_per_s": round(len(ds) / (ms / 1e3), 1),
             "model_bytes": model, "achieved_gbs": round(model / (ms / 1e3) / 1e9, 1),
-            "frac_of_peak": round(model / (ms / 1e3) / 1e9 / peak, 4), "kernel": hs.sweep_kernel_name()}
+            "frac_of_peak": round(model / (ms / 1e3) / 1e9 / peak, 4), "kernel": hs.sweep_kernel_name(),
+            "segments": ds[0].info().n_segments}
     return out
 
 

@@ -68,7 +68,8 @@ constexpr int WM = 40;    // vector stride
 constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
 constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA producer warps
 }  // namespace dualk
-constexpr int kXpartElems = 10 * dualk::WM;   // <= 10 consumer warps
+// partial sums of the transposed X part (HELM_DUAL_XSYM only): <= 10 consumer warps
+constexpr int kXpartElems = HELM_DUAL_XSYM ? 10 * dualk::WM : 0;
 
 // per-CTA cycle counters (tools/prof_sweep.py) only in the -DHELM_DUAL_PROF build
 // (python -m paper_2408_11929_b200.build --prof); the per-step sub-phase counters
