@@ -22,6 +22,7 @@ extrapolation; factor sets built before timing).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -187,6 +188,7 @@ def run_ours(args):
 
     # the clock sampler runs from before the warm-up; only its samples inside the
     # timed region are reported
+    gc.collect()
     sampler = ClockSampler(local)
     sampler.start()
     for _ in range(args.warmup):
@@ -366,18 +368,23 @@ def run_e2e(args, cfg, names, my_names=None, dp=None):
 
     for _ in range(args.warmup):
         step()
+    gc.collect()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     e0.record(stream)
-    its = [step() for _ in range(args.steps)]
+    its, step_wall = [], []
+    for _ in range(args.steps):
+        s0 = time.perf_counter()
+        its.append(step())
+        step_wall.append(round(1e3 * (time.perf_counter() - s0), 2))
     e1.record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
     ms = e0.elapsed_time(e1)
     return {"_ms_total": ms, "_applies": sum(its) * len(my_names), "unit": "applies/s",
             "h2d_bytes_per_step": 8 * cfg.n + 16 * cfg.n, "d2h_bytes_per_step": 16 * cfg.n,
-            "host_wall_ms_per_step": round(wall / len(its) * 1e3, 3),
+            "host_wall_ms_per_step": round(wall / len(its) * 1e3, 3), "host_wall_ms_each_step": step_wall,
             "steps": len(its), "warmup": args.warmup,
             "path": "helm_assemble(host c) + sweep_setup x4 + helm_load_vector(host f) + mpgmres_solve(x to host)"}
 

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <complex>
+#include <mutex>
 
 #include <cooperative_groups.h>
 
@@ -873,8 +874,27 @@ static int orth_fused(KrylovWS* ws, long n, cplx* V, int m, int t, cplx* W, cuda
   }
   const void* kfun = t <= 1 ? (const void*)k_orth<1> : t <= 2 ? (const void*)k_orth<2>
                    : t <= 4 ? (const void*)k_orth<4> : (const void*)k_orth<8>;
+  // occupancy per (kernel, shared memory), cached: the query sits on the host-synchronous
+  // iteration's critical path
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, kOrthThreads, smem);
+  cudaError_t e = cudaSuccess;
+  {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto& c : cache)
+        if (c.first.first == kfun && c.first.second == smem) { occ = c.second; hit = true; }
+    }
+    if (!hit) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, kOrthThreads, smem);
+      if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mu);
+        cache.push_back({{kfun, smem}, occ});
+      }
+    }
+  }
   if (e != cudaSuccess || occ < 1) return 0;
   long nblk = std::min<long>((long)nsm * std::min(occ, 4), (n + kOrthThreads - 1) / kOrthThreads);
   if ((long)nblk * (m + 1) * t > ws->partial_cap) nblk = ws->partial_cap / ((long)(m + 1) * t);

@@ -291,6 +291,11 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
     // pivot search: the largest |a_ik|^2 among unused rows, compared on the high
     // 32 bits of the (non-negative) double -- monotonic; candidates equal to ~1e-6
     // relative go to the lowest row -- with one warp max-reduction and a ballot
+#ifdef HELM_GJ_NOPIVOT
+    // ablation (timing only): diagonal pivots, no search
+    const int p = k;
+    (void)lane; (void)warp;
+#else
     const double mag = (active && !used && h == kh) ? cabs2(mine) : 0.0;
     const unsigned key = (active && !used && h == kh) ? (unsigned)__double2hiint(mag) + 1u : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
@@ -303,6 +308,7 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
     for (int q = 1; q < kRowWarps; ++q)
       if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
     if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
+#endif
     // pivot element to both halves of the pivot row; multiplier to both halves of the others
     cplx akk;
     akk.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);

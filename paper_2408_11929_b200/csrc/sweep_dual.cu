@@ -34,6 +34,7 @@
 // wavefronts and exposed latency, tools/bench_dualstep.cu).
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <type_traits>
 
@@ -1006,14 +1007,19 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + (2L + kTcW) * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
   const void* kfun = gsep ? (const void*)k_sweep_dual<true> : (const void*)k_sweep_dual<false>;
   if (smem > (size_t)kDualSmemMax) return -1;
-  // per-direction scratch: counters, parity-buffered yb / xb / xs, corrections
-  std::vector<size_t> off(t);
-  size_t total = 0;
+  // scratch: the counters of every direction first (one memset), then per
+  // direction the parity-buffered yb / xb / xs and the corrections
+  std::vector<size_t> off(t), coff(t);
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t ncnt = 0;
+  for (int d = 0; d < t; ++d) {
+    coff[d] = ncnt;
+    ncnt += 2 + dirs[d]->P;
+  }
+  size_t total = al(sizeof(unsigned) * ncnt);
   for (int d = 0; d < t; ++d) {
     const helm_sweep_s* h = dirs[d];
     off[d] = total;
-    total += al(sizeof(unsigned) * (2 + h->P));
     total += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax) * 2;
     total += al(sizeof(cplx) * 2L * h->P * h->wmax);
     total += al(sizeof(cplx) * (long)h->N * h->nc);
@@ -1050,7 +1056,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];
-    D.cnt = (unsigned*)q; D.flag = D.cnt + 2; q += al(sizeof(unsigned) * (2 + h->P));
+    D.cnt = reinterpret_cast<unsigned*>(scratch) + coff[d]; D.flag = D.cnt + 2;
     D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
@@ -1059,13 +1065,43 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.wmax = h->wmax;
     D.cta_base = base;
     base += h->P;
-    if (e == cudaSuccess) e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * (2 + h->P), st);
   }
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, sizeof(unsigned) * ncnt, st);
+  // the attribute / occupancy queries cost host time on every iteration's critical
+  // path (the solve is host-synchronous): cache them per (kernel, shared memory)
   int dev = 0, nsm = 0, occ = 0;
-  if (e == cudaSuccess) e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, threads, smem);
+  {
+    // (the dynamic shared-memory attribute is raised to the largest size ever
+    // launched, never lowered: a cached smaller setting must not cap a later launch)
+    struct OccKey { const void* f; size_t smem; int threads, dev; int nsm, occ; };
+    struct AttrMax { const void* f; int dev; size_t smem; };
+    static std::mutex mu;
+    static std::vector<OccKey> cache;
+    static std::vector<AttrMax> attr;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    bool raised = false;
+    for (AttrMax& a : attr)
+      if (a.f == kfun && a.dev == dev) {
+        raised = true;
+        if (smem > a.smem && e == cudaSuccess) {
+          e = cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e == cudaSuccess) a.smem = smem;
+        }
+      }
+    if (!raised && e == cudaSuccess) {
+      e = cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) attr.push_back(AttrMax{kfun, dev, smem});
+    }
+    bool hit = false;
+    for (const OccKey& c : cache)
+      if (c.f == kfun && c.smem == smem && c.threads == threads && c.dev == dev) { nsm = c.nsm; occ = c.occ; hit = true; }
+    if (!hit) {
+      if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, threads, smem);
+      if (e == cudaSuccess) cache.push_back(OccKey{kfun, smem, threads, dev, nsm, occ});
+    }
+  }
   if (e == cudaSuccess && occ * nsm < ctas) {
     cudaFreeAsync(scratch, st);
     return -1;   // not co-resident: the caller falls back to the single-chain kernel

@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-north-star > $O/${T}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_sweep_dual -s 2 -c 1 -o $O/${T}_dual \
   python tools/prof_sweep.py --reps 1 > $O/${T}_ncu_dual.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_spmm -s 1 -c 3 -o $O/${T}_spmm \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_spmm -s 1 -c 4 -o $O/${T}_spmm \
   python tools/prof_spmm.py 2 > $O/${T}_ncu_spmm.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_orth -s 11 -c 1 -o $O/${T}_orth \
   python tools/prof_setup.py 5 > $O/${T}_ncu_orth.log 2>&1
