@@ -355,6 +355,7 @@ extern "C" int helm_load_vector(helm_problem_t p, const double* f, double* b, vo
   cudaStream_t st = (cudaStream_t)stream;
   size_t vb = sizeof(cplx) * p->n;
   Staged sf, sb;
+  StageGuard gf(sf, st), gb(sb, st);
   HELM_TRY(helm_stage_in(f, vb, true, st, sf));
   HELM_TRY(helm_stage_in(b, vb, false, st, sb));
   long blocks = (p->n + 255) / 256;
@@ -376,6 +377,7 @@ extern "C" int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols
   cudaStream_t st = (cudaStream_t)stream;
   size_t vb = sizeof(cplx) * p->n * ncols;
   Staged sx, sy;
+  StageGuard gx(sx, st), gy(sy, st);
   HELM_TRY(helm_stage_in(X, vb, true, st, sx));
   HELM_TRY(helm_stage_in(Y, vb, false, st, sy));
   HELM_TRY(helm_spmm_dev(p, (const cplx*)sx.dev, (cplx*)sy.dev, ncols, p->n, st));

@@ -205,3 +205,10 @@ int helm_stage_in(const void* ptr, size_t bytes, bool copy_in, cudaStream_t st, 
 int helm_stage_out(Staged& s, cudaStream_t st);  // copy back to host if staged, then free
 void helm_stage_free(Staged& s, cudaStream_t st);
 bool helm_is_device_ptr(const void* p);
+// frees a staging buffer on every return path (helm_stage_free is idempotent)
+struct StageGuard {
+  Staged& s;
+  cudaStream_t st;
+  StageGuard(Staged& s_, cudaStream_t st_) : s(s_), st(st_) {}
+  ~StageGuard() { helm_stage_free(s, st); }
+};

@@ -949,7 +949,10 @@ static int mpgmres_core(helm_problem_t prob, const helm_sweep_t* dirs, int t_loc
   const long n = prob->n;
   Staged sb, sx;
   HELM_TRY(helm_stage_in(b_in, sizeof(cplx) * n, true, st, sb));
-  HELM_TRY(helm_stage_in(x_out, sizeof(cplx) * n, false, st, sx));
+  {
+    const int rs = helm_stage_in(x_out, sizeof(cplx) * n, false, st, sx);
+    if (rs != HELM_OK) { helm_stage_free(sb, st); return rs; }
+  }
   const cplx* b = (const cplx*)sb.dev;
   cplx* x = (cplx*)sx.dev;
 

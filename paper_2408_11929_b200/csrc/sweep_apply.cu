@@ -789,6 +789,7 @@ extern "C" int sweep_apply(const helm_sweep_t* dirs, int t, const double* Rin, l
   Staged sR, sZ;
   size_t rbytes = sizeof(cplx) * (ldr == 0 ? n : ldr * (t - 1) + n);
   size_t zbytes = sizeof(cplx) * (ldz * (t - 1) + n);
+  StageGuard gR(sR, st), gZ(sZ, st);
   HELM_TRY(helm_stage_in(Rin, rbytes, true, st, sR));
   HELM_TRY(helm_stage_in(Zout, zbytes, false, st, sZ));
   int rc = sweep_apply_dev(dirs, t, (const cplx*)sR.dev, ldr, (cplx*)sZ.dev, ldz, st);
