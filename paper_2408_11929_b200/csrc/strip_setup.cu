@@ -234,10 +234,15 @@ __global__ void k_factor_segments(FacArgs fa) {
 // single precision stays at least 1/(2w) away from the next integer
 __device__ __forceinline__ int div_w(int e, float invw) { return (int)(((float)e + 0.5f) * invw); }
 
+#ifndef HELM_ROW_LPR
+#define HELM_ROW_LPR 2      // threads per block row in the register-row Gauss-Jordan (2 or 4)
+#endif
 static constexpr int kRowW = 36;
-static constexpr int kRowHW = kRowW / 2;
-static constexpr int kRowThreads = 96;
+static constexpr int kLPR = HELM_ROW_LPR;                 // lanes per row: column j = kLPR jj + h
+static constexpr int kRowHW = kRowW / kLPR;               // columns (registers) per thread
+static constexpr int kRowThreads = kLPR == 2 ? 96 : 160;  // >= kRowW kLPR threads, whole warps
 static constexpr int kRowWarps = kRowThreads / 32;
+static_assert(kRowW % kLPR == 0 && kRowW * kLPR <= kRowThreads, "row layout");
 
 struct RowSmem {
   cplx mat[kRowW * kRowW];    // natural-order inverse of the current block / Y
@@ -252,7 +257,7 @@ struct RowSmem {
 // sm.mat (natural order, row stride kRowW).  Returns 1 (uniformly) on a zero pivot.
 __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i = tid >> 1, h = tid & 1;
+  const int i = tid / kLPR, h = tid % kLPR;
   const bool active = i < w;
   bool used = false;
   int kstep = 0;
@@ -261,8 +266,8 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
   // written back with unrolled selects
 #pragma unroll 1
   for (int k = 0; k < w; ++k) {
-    const int kh = k & 1, kj = k >> 1;
-    // a[kj] by a select tree on the bits of kj (depth 5, not a chain of 17)
+    const int kh = k % kLPR, kj = k / kLPR;
+    // a[kj] by a select tree on the bits of kj (depth log2, not a chain)
     cplx mine;
     {
       cplx t1[(kRowHW + 1) / 2];
@@ -280,13 +285,18 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
       for (int u = 0; u < n2 / 2; ++u) t3[u] = (kj & 4) ? t2[2 * u + 1] : t2[2 * u];
       if (n2 & 1) t3[n2 / 2] = t2[n2 - 1];
       constexpr int n3 = (n2 + 1) / 2;
-      cplx t4[(n3 + 1) / 2];
+      if constexpr (n3 == 1) {
+        mine = t3[0];
+      } else {
+        cplx t4[(n3 + 1) / 2];
 #pragma unroll
-      for (int u = 0; u < n3 / 2; ++u) t4[u] = (kj & 8) ? t3[2 * u + 1] : t3[2 * u];
-      if (n3 & 1) t4[n3 / 2] = t3[n3 - 1];
-      constexpr int n4 = (n3 + 1) / 2;
-      static_assert(n4 == 2, "select tree depth");
-      mine = (kj & 16) ? t4[1] : t4[0];
+        for (int u = 0; u < n3 / 2; ++u) t4[u] = (kj & 8) ? t3[2 * u + 1] : t3[2 * u];
+        if (n3 & 1) t4[n3 / 2] = t3[n3 - 1];
+        constexpr int n4 = (n3 + 1) / 2;
+        static_assert(n4 <= 2, "select tree depth");
+        if constexpr (n4 == 2) mine = (kj & 16) ? t4[1] : t4[0];
+        else mine = t4[0];
+      }
     }
     // pivot search: the largest |a_ik|^2 among unused rows, compared on the high
     // 32 bits of the (non-negative) double -- monotonic; candidates equal to ~1e-6
@@ -300,7 +310,7 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
     const unsigned key = (active && !used && h == kh) ? (unsigned)__double2hiint(mag) + 1u : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
     const unsigned who = __ballot_sync(0xffffffffu, key == kmax);
-    if (lane == 0 && warp < kRowWarps) { sm.redk[warp] = kmax; sm.redi[warp] = warp * 16 + ((__ffs(who) - 1) >> 1); }
+    if (lane == 0 && warp < kRowWarps) { sm.redk[warp] = kmax; sm.redi[warp] = warp * (32 / kLPR) + (__ffs(who) - 1) / kLPR; }
     __syncthreads();
     unsigned k0 = sm.redk[0];
     int p = sm.redi[0];
@@ -309,18 +319,20 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
       if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
     if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
 #endif
-    // pivot element to both halves of the pivot row; multiplier to both halves of the others
+    // pivot element to every lane of the pivot row; multiplier to every lane of the others
     cplx akk;
-    akk.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);
-    akk.y = __shfl_xor_sync(0xffffffffu, mine.y, 1);
-    if (h == kh) akk = mine;
+    {
+      const int src = (lane & ~(kLPR - 1)) | kh;
+      akk.x = __shfl_sync(0xffffffffu, mine.x, src);
+      akk.y = __shfl_sync(0xffffffffu, mine.y, src);
+    }
     if (i == p) {
       const cplx dinv = cinv(akk);
 #pragma unroll
       for (int jj = 0; jj < kRowHW; ++jj) {
         const cplx v = (h == kh && jj == kj) ? cmk(1.0, 0.0) : a[jj];
         a[jj] = cmul(v, dinv);
-        sm.prow[2 * jj + h] = a[jj];
+        sm.prow[kLPR * jj + h] = a[jj];
       }
       // the pivot column is broadcast as 1 + 1/piv, so the generic update of the
       // other rows, a_ik - f (1 + 1/piv) with f = a_ik, leaves -f/piv there
@@ -334,7 +346,7 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
       const cplx f = akk;
 #pragma unroll
       for (int jj = 0; jj < kRowHW; ++jj) {   // a -= f r, four fused multiply-adds
-        const cplx r = sm.prow[2 * jj + h];
+        const cplx r = sm.prow[kLPR * jj + h];
         a[jj].x = fma(-f.x, r.x, a[jj].x);
         a[jj].x = fma(f.y, r.y, a[jj].x);
         a[jj].y = fma(-f.x, r.y, a[jj].y);
@@ -346,7 +358,7 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
   if (active) {
 #pragma unroll
     for (int jj = 0; jj < kRowHW; ++jj) {
-      const int j = 2 * jj + h;
+      const int j = kLPR * jj + h;
       if (j < w) sm.mat[kstep * kRowW + sm.pivrow[j]] = a[jj];
     }
   }
@@ -358,14 +370,14 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
 //   td (kind 0): L = U_{c-1}^T, R = U_{c-1};  bu (kind 1): L = U_c, R = U_c^T
 __device__ __forceinline__ void row_schur(cplx (&a)[kRowHW], int w, const cplx* dg, const cplx* al, const cplx* cr,
                                           const cplx* ne, bool has, bool td, const RowSmem& sm) {
-  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  const int i = threadIdx.x / kLPR, h = threadIdx.x % kLPR;
   const cplx zero = cmk(0, 0);
   const cplx dgi = i < w ? __ldg(dg + i) : zero;
   const cplx ali = i + 1 < w ? __ldg(al + i) : zero;
   const cplx alm = (i >= 1 && i < w) ? __ldg(al + i - 1) : zero;
 #pragma unroll
   for (int jj = 0; jj < kRowHW; ++jj) {
-    const int q = 2 * jj + h;
+    const int q = kLPR * jj + h;
     a[jj] = q == i ? dgi : (q == i + 1 ? ali : (q + 1 == i ? alm : zero));
   }
   if (!has || i >= w) return;
@@ -377,7 +389,7 @@ __device__ __forceinline__ void row_schur(cplx (&a)[kRowHW], int w, const cplx* 
     const cplx* x1 = sm.mat + (i >= 1 ? i - 1 : 0) * kRowW;
 #pragma unroll
     for (int jj = 0; jj < kRowHW; ++jj) {
-      const int q = 2 * jj + h;
+      const int q = kLPR * jj + h;
       if (q >= w) break;
       cplx yq = cmul(ci, x0[q]);
       if (i >= 1) cfma(yq, nm, x1[q]);
@@ -395,7 +407,7 @@ __device__ __forceinline__ void row_schur(cplx (&a)[kRowHW], int w, const cplx* 
     const cplx* x1 = sm.mat + (i + 1 < w ? i + 1 : i) * kRowW;
 #pragma unroll
     for (int jj = 0; jj < kRowHW; ++jj) {
-      const int q = 2 * jj + h;
+      const int q = kLPR * jj + h;
       if (q >= w) break;
       cplx yq = cmul(ci, x0[q]);
       if (i + 1 < w) cfma(yq, ni, x1[q]);
@@ -442,7 +454,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
   cplx* fac = fa.fac + fa.fac_off[s];
   const long w2 = (long)w * w;
   cplx* scr = fa.scratch + ((long)s * fa.P + pseg) * fa.scratch_stride;
-  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  const int i = threadIdx.x / kLPR, h = threadIdx.x % kLPR;
   cplx a[kRowHW];
   auto B = [&](const cplx* base, int c) { return base + band + (long)c * fa.wmax; };
   if (kind == 0) {
@@ -463,7 +475,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
       if (i < w) {
         const cplx ci = __ldg(cr + i);
         const cplx ni = i + 1 < w ? __ldg(ne + i) : cmk(0, 0);
-        for (int q = h; q < w; q += 2) {
+        for (int q = h; q < w; q += kLPR) {
           cplx v = cmul(ci, sm.mat[i * kRowW + q]);
           if (i + 1 < w) cfma(v, ni, sm.mat[(i + 1) * kRowW + q]);
           sm.tmat[i * kRowW + q] = v;
@@ -574,7 +586,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   cplx* red = ra.red + ra.red_off[s];
   auto scr = [&](int p) { return ra.scratch + ((long)s * ra.P + p) * ra.scratch_stride; };
   const int P = ra.P;
-  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  const int i = threadIdx.x / kLPR, h = threadIdx.x % kLPR;
   // cp.async the operands of separator k into buffer k & 1: Sinv_{h_k}, X_{k+1}[lo,lo],
   // X_{k+1}[lo,hi] and the couplings of rows h_k, s_k, h_{k+1}
   auto stage = [&](int k) {
@@ -625,7 +637,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     cplx a[kRowHW];
 #pragma unroll
     for (int jj = 0; jj < kRowHW; ++jj) {
-      const int col = 2 * jj + h;
+      const int col = kLPR * jj + h;
       a[jj] = (i < w && col < w) ? S[i * w + col] : cmk(0, 0);
     }
     if (row_invert(a, w, sm)) {
