@@ -114,6 +114,20 @@ int sweep_setup(helm_problem_t p, int axis, int order, int n_strips, int overlap
                 int is_double, int gather, int n_segments, void* stream,
                 helm_sweep_t* out);
 
+/* sweep_set_precision -- opt-in INEXACT separator solve (
+ * "the subproblems can be solved to low accuracy without much deterioration",
+ * P:L278): separator_bits = 32 makes the two-chain sweep kernel multiply the
+ * separator right-hand side by a complex64 copy of the explicit
+ * separator-inverse rows with FP32 products and accumulation (half the bytes
+ * of that HBM-bound stage); 64 (default) restores the complex128 path.  The
+ * preconditioner then differs from the exact strip solves by ~1e-6 relative
+ * (the MPGMRES residual and x stay complex128); every other step is
+ * unchanged.  Applies when every direction of a batch asked for it and the
+ * two-chain kernel runs (strips <= 36 nodes, P > 1).  The complex64 copy is
+ * made once per factor set (device memory: half of the rows').
+ * Errors: HELM_EINVAL (bits not 32 / 64, or no separator rows), HELM_ENOMEM, HELM_ECUDA. */
+int sweep_set_precision(helm_sweep_t s, int separator_bits);
+
 /* Geometry / size report of a sweep handle (host-only query):
  *   info[0] n_strips, [1] n_c (cross rows), [2] w_max (nodes per block row),
  *   [3] n_segments, [4] local solves per apply, [5] factor bytes on device,

@@ -30,7 +30,7 @@ DIRECTIONS = {"LRL": (0, 0, 1), "RLR": (0, 1, 1), "BTB": (1, 0, 1), "TBT": (1, 1
 EXPORTS = ["helm_assemble", "helm_assemble_fd5", "helm_problem_info", "helm_get_diagonals", "helm_load_vector", "helm_spmv",
            "sweep_setup", "sweep_info", "sweep_apply", "mpgmres_solve", "helm_problem_destroy",
            "sweep_destroy", "helm_strerror", "helm_last_error", "helm_kernel_launches", "helm_sweep_kernel_name",
-           "helm_set_knob", "mpgmres_solve_dist"]
+           "helm_set_knob", "mpgmres_solve_dist", "sweep_set_precision"]
 
 
 class HelmError(RuntimeError):
@@ -79,6 +79,8 @@ def load():
     L.helm_spmv.argtypes = [vp, vp, vp, i, vp]
     L.sweep_setup.argtypes = [vp, i, i, i, i, i, i, i, vp, ctypes.POINTER(vp)]
     L.sweep_info.argtypes = [vp, ctypes.POINTER(l)]
+    L.sweep_set_precision.argtypes = [vp, i]
+    L.sweep_set_precision.restype = i
     L.sweep_apply.argtypes = [ctypes.POINTER(vp), i, vp, l, vp, l, vp]
     L.mpgmres_solve.argtypes = [vp, ctypes.POINTER(vp), i, vp, vp, d, i, ctypes.POINTER(MPGMRESStats), vp]
     L.helm_problem_destroy.argtypes = [vp]
@@ -258,6 +260,11 @@ class Sweep:
                                   n_segments, _stream(stream), ctypes.byref(handle)), "sweep_setup")
         self.handle = handle
         self.problem = problem
+
+    def set_precision(self, separator_bits: int):
+        """sweep_set_precision: 32 = opt-in inexact (complex64) separator solve, 64 = exact."""
+        _check(load().sweep_set_precision(self.handle, int(separator_bits)), "sweep_set_precision")
+        return self
 
     def info(self) -> SweepInfo:
         arr = (ctypes.c_long * 10)()

@@ -179,6 +179,11 @@ struct helm_sweep_s {
   // explicit rows of the separator inverse (w <= 36 only): per strip, separator k:
   // w x (K w) row-major at xinv_off[s] + k * w * K * w
   cplx* d_xinv = nullptr; std::vector<long> xinv_off; long* d_xinv_off = nullptr;
+  long xinv_elems = 0;
+  // opt-in inexact separator solve (sweep_set_precision): complex64 copy of the
+  // explicit separator-inverse rows, shared by the handles of one factor set
+  float2* d_xinv32 = nullptr;
+  int sep_fp32 = 0;
   // two-chain kernel (sweep_dual.cu): the top-down inverses Sinv_c (d_facp) and the
   // bottom-up inverses S'^{-1}_c (d_fac2) of every segment row, complex symmetric,
   // stored as packed upper triangles (row r holds columns r..w-1), w(w+1)/2 per

@@ -35,6 +35,8 @@ struct SharedFactors {
   int axis, N, overlap, P;
   cplx *dg, *al, *cr, *ne, *tc, *fac, *red, *xinv, *fac2, *facp;
   long factor_bytes;
+  float2* xinv32 = nullptr;   // complex64 separator-inverse rows, made on the first sweep_set_precision(32)
+  long xinv_elems = 0;
 };
 static std::vector<SharedFactors*> g_shared;
 static std::mutex g_shared_mu;   // setups of different axes may run on concurrent host threads
@@ -1043,6 +1045,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     h->d_dg = sf->dg; h->d_al = sf->al; h->d_cr = sf->cr; h->d_ne = sf->ne; h->d_tc = sf->tc;
     h->d_fac = sf->fac; h->d_red = sf->red; h->d_xinv = sf->xinv; h->d_fac2 = sf->fac2; h->d_facp = sf->facp;
     h->factor_bytes = sf->factor_bytes;
+    h->xinv_elems = sf->xinv_elems;
     h->shared = sf;
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
@@ -1179,6 +1182,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   }
   sf = new SharedFactors{1, prob->uid, axis, n_strips, overlap, P, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc,
                          h->d_fac, h->d_red, h->d_xinv, h->d_fac2, h->d_facp, h->factor_bytes};
+  sf->xinv_elems = h->xinv_elems = want_xinv ? xinv_total : 0;
   {
     std::lock_guard<std::mutex> lk(g_shared_mu);
     g_shared.push_back(sf);
@@ -1214,6 +1218,49 @@ extern "C" int sweep_info(helm_sweep_t h, long* info) {
   return HELM_OK;
 }
 
+// ------------------------------------------------------------------ inexact separator solve
+__global__ void k_to_c64(const cplx* __restrict__ x, float2* __restrict__ y, long n) {
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+    y[e] = make_float2((float)x[e].x, (float)x[e].y);
+}
+
+extern "C" int sweep_set_precision(helm_sweep_t h, int separator_bits) {
+  if (!h || (separator_bits != 32 && separator_bits != 64)) {
+    helm_set_error("sweep_set_precision: need a handle and 32 or 64 separator bits");
+    return HELM_EINVAL;
+  }
+  if (separator_bits == 64) { h->sep_fp32 = 0; return HELM_OK; }
+  if (!h->d_xinv || h->xinv_elems <= 0) {
+    helm_set_error("sweep_set_precision: this sweep has no explicit separator-inverse rows (P = 1)");
+    return HELM_EINVAL;
+  }
+  SharedFactors* sf = h->shared;
+  std::lock_guard<std::mutex> lk(g_shared_mu);
+  if (!sf->xinv32) {
+    float2* y = nullptr;
+    cudaError_t e = helm_dev_alloc((void**)&y, sizeof(float2) * h->xinv_elems);
+    cudaStream_t st = nullptr;
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+      k_to_c64<<<148 * 8, 256, 0, st>>>(h->d_xinv, y, h->xinv_elems);
+      g_helm_launches++;
+      e = cudaGetLastError();
+      const cudaError_t es = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = es;
+      cudaStreamDestroy(st);
+    }
+    if (e != cudaSuccess) {
+      helm_dev_free(y);
+      helm_set_error("sweep_set_precision: %s", cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? HELM_ENOMEM : HELM_ECUDA;
+    }
+    sf->xinv32 = y;
+  }
+  h->d_xinv32 = sf->xinv32;
+  h->sep_fp32 = 1;
+  return HELM_OK;
+}
+
 extern "C" void sweep_destroy(helm_sweep_t h) {
   if (!h) return;
   helm_dev_free(h->d_a); helm_dev_free(h->d_w); helm_dev_free(h->d_own_lo); helm_dev_free(h->d_own_hi);
@@ -1229,6 +1276,7 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
     } else {
       for (size_t k = 0; k < g_shared.size(); ++k)
         if (g_shared[k] == sf) { g_shared.erase(g_shared.begin() + k); break; }
+      helm_dev_free(sf->xinv32);
       delete sf;
     }
   }

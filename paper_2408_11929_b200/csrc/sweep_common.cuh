@@ -25,6 +25,7 @@ struct DirArgs {
   unsigned* cnt;         // [0] segment arrivals, [1] reducer releases
   unsigned* flag;        // fast kernel: per-separator publication flags (solve index + 1)
   const cplx* xinv;      // explicit separator-inverse rows (fast kernel), NULL if absent
+  const float2* xinv32;  // their complex64 copy (inexact separator solve, two-chain kernel), NULL if off
   const long* xinv_off;
   int wmax;
   int cta_base;

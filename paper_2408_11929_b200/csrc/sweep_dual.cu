@@ -106,6 +106,7 @@ struct DualTab {
   const cplx* fac;
   const cplx* fac2;
   const cplx* xinv;
+  const float2* xinv32;   // complex64 rows (XF32 instantiation only)
   int w, a, s, pks;   // pks: entries per padded packed block (pk_size(w))
 };
 
@@ -136,6 +137,12 @@ __device__ __forceinline__ cplx ld_cg_hint(const cplx* a, uint64_t pol) {
   return v;
 }
 
+__device__ __forceinline__ float2 ld_cg_hint_f2(const float2* a, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ void dprefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
   asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
                : "memory");
@@ -154,7 +161,7 @@ __device__ __forceinline__ void chain_row(int g, int e, int m, int lo, int hi, i
 // GSEP: the separator RHS g has its own shared-memory area (more separators
 // than segment rows, e.g. C2 with 32 segments); else it aliases xa.  A template
 // parameter, not a runtime choice: the kernel is at its register cap.
-template <bool GSEP>
+template <bool GSEP, bool XF32>
 __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_constant__ DualArgs A) {
   using namespace dualk;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -204,6 +211,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     tab[i].fac = D_.facp + D_.pfac_off[s];
     tab[i].fac2 = D_.fac2 + D_.pfac_off[s];
     tab[i].xinv = D_.xinv + D_.xinv_off[s];
+    tab[i].xinv32 = D_.xinv32 ? D_.xinv32 + D_.xinv_off[s] : nullptr;
     tab[i].w = D_.w[s];
     tab[i].a = D_.a[s];
     tab[i].s = s;
@@ -480,9 +488,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       // block (p, k) transposed (X = R^{-1} is complex symmetric)
       const long ld = x_ld(K, w);
       const int kc = HELM_DUAL_XSYM ? p : 0;   // first column block read from block row p
-      const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(cplx));
-      for (int r = tid; r < w; r += 32)
-        dprefetch_l2(tab[i].xinv + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
+      if constexpr (XF32) {
+        const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(float2));
+        for (int r = tid; r < w; r += 32)
+          dprefetch_l2(tab[i].xinv32 + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
+      } else {
+        const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(cplx));
+        for (int r = tid; r < w; r += 32)
+          dprefetch_l2(tab[i].xinv + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
+      }
     }
     // publish this segment's contributions to its two separator right-hand sides:
     //   yb[0..w)   = U_{lo-1} x0_lo   (enters g_{p-1}),  yb[wmax..) = U_hi^T x0_hi  (enters g_p)
@@ -597,6 +611,50 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
       const long c0 = HELM_DUAL_XSYM ? (long)p * w : 0;
       constexpr int XCH = HELM_DUAL_XCH;
+      if constexpr (XF32) {
+        // inexact separator solve (sweep_set_precision(32)): complex64 rows of R^{-1}, FP32
+        // products and accumulation -- half the separator-inverse bytes, twice the columns
+        // in flight for the same registers
+        for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
+          const float2* Xr[4];
+          bool ok[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ok[u] = rb + u < w;
+            Xr[u] = tab[i].xinv32 + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
+          }
+          float2 acc[4] = {make_float2(0, 0), make_float2(0, 0), make_float2(0, 0), make_float2(0, 0)};
+          for (long jj = lane; jj < Kw; jj += 32 * 8) {
+            float2 xv[4][8], gv[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const bool in = jj + 32 * v < Kw;
+              const cplx gd = in ? gsm[jj + 32 * v] : cmk(0, 0);
+              gv[v] = make_float2((float)gd.x, (float)gd.y);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ld_cg_hint_f2(Xr[u] + jj + 32 * v, pol_first) : make_float2(0, 0);
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                acc[u].x = fmaf(xv[u][v].x, gv[v].x, acc[u].x);
+                acc[u].x = fmaf(-xv[u][v].y, gv[v].y, acc[u].x);
+                acc[u].y = fmaf(xv[u][v].x, gv[v].y, acc[u].y);
+                acc[u].y = fmaf(xv[u][v].y, gv[v].x, acc[u].y);
+              }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+              acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
+              acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+            }
+            if (lane == 0 && ok[u]) xhi[rb + u] = cmk((double)acc[u].x, (double)acc[u].y);
+          }
+        }
+      } else {
       // normal part: 4 rows per warp, lanes over the columns, 4 XCH loads in flight per lane
       for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
         const cplx* Xr[4];
@@ -631,15 +689,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           if (lane == 0 && ok[u]) xhi[rb + u] = acc[u];
         }
       }
+      }
       // transposed part: rows (k, i), k < p, of the blocks (k, p), lanes over r;
       // 4 rows in flight per lane, per-warp partial sums combined in a fixed order
-      constexpr int XTU = HELM_DUAL_XTU;
       cplx t0 = cmk(0, 0), t1 = cmk(0, 0);
       const int nrow = HELM_DUAL_XSYM ? p * w : 0;
-      for (int e0 = cw; e0 < nrow; e0 += XTU * ncw) {
-        cplx xa0[XTU], xa1[XTU], gv[XTU];
+      for (int e0 = cw; e0 < nrow; e0 += HELM_DUAL_XTU * ncw) {
+        cplx xa0[HELM_DUAL_XTU], xa1[HELM_DUAL_XTU], gv[HELM_DUAL_XTU];
 #pragma unroll
-        for (int u = 0; u < XTU; ++u) {
+        for (int u = 0; u < HELM_DUAL_XTU; ++u) {
           const int e = e0 + u * ncw;
           const bool ok = e < nrow;
           const cplx* row = tab[i].xinv + (long)(ok ? e : 0) * xld + c0;   // row (k, i) = global row e = k w + i
@@ -648,7 +706,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           gv[u] = ok ? gsm[e] : cmk(0, 0);                                   // g_k[i] = gsm[k w + i]
         }
 #pragma unroll
-        for (int u = 0; u < XTU; ++u) {
+        for (int u = 0; u < HELM_DUAL_XTU; ++u) {
           cfma(t0, xa0[u], gv[u]);
           cfma(t1, xa1[u], gv[u]);
         }
@@ -1005,7 +1063,11 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * (WM + pmax) + 256;
   const bool gsep = gsm_elems > vec_elems;
   smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + (2L + kTcW) * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
-  const void* kfun = gsep ? (const void*)k_sweep_dual<true> : (const void*)k_sweep_dual<false>;
+  // inexact separator solve only when every direction of the batch asked for it
+  bool xf32 = true;
+  for (int d = 0; d < t; ++d) xf32 = xf32 && dirs[d]->sep_fp32 && dirs[d]->d_xinv32;
+  const void* kfun = gsep ? (xf32 ? (const void*)k_sweep_dual<true, true> : (const void*)k_sweep_dual<true, false>)
+                          : (xf32 ? (const void*)k_sweep_dual<false, true> : (const void*)k_sweep_dual<false, false>);
   if (smem > (size_t)kDualSmemMax) return -1;
   // scratch: the counters of every direction first (one memset), then per
   // direction the parity-buffered yb / xb / xs and the corrections
@@ -1053,6 +1115,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.cr = h->d_cr; D.ne = h->d_ne; D.tc = h->d_tc;
     D.fac = h->d_fac; D.fac2 = h->d_fac2; D.facp = h->d_facp; D.pfac_off = h->d_pfac_off; D.fac_off = h->d_fac_off; D.red = h->d_red; D.red_off = h->d_red_off;
     D.xinv = h->d_xinv; D.xinv_off = h->d_xinv_off;
+    D.xinv32 = xf32 ? h->d_xinv32 : nullptr;
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];

@@ -486,3 +486,38 @@ def test_overlap2(kernel, knob):
     for k, P in enumerate(_oracle_precs(cfg, A, names, n_strips=5, overlap=2)):
         z = P.apply(R[k])
         assert rel(Zh[k], z) <= 1e-10 and elementwise(Zh[k], z) <= 1e-10, (kernel, names[k])
+
+
+@pytest.mark.parametrize("name", ["C2", "C5s"])
+def test_inexact_separator_fp32(name):
+    """Opt-in inexact separator solve (sweep_set_precision(32)):
+    the apply stays within 1e-5 of the oracle's exact sweep; MPGMRES with the
+    inexact preconditioners converges with at most one extra iteration and its
+    x satisfies the same residual tolerance; switching back to 64 bits restores
+    the exact (1e-10) apply."""
+    cfg = CFGS[name]()
+    A = p1.assemble(cfg)
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+    precs = _oracle_precs(cfg, A, names)
+    R = random_vector(cfg.n, 31, len(names))
+    Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+    for d in dirs:
+        d.set_precision(32)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    Zh = Z.cpu().numpy()
+    errs = [rel(Zh[k], P.apply(R[k])) for k, P in enumerate(precs)]
+    assert max(errs) <= 1e-5 and max(errs) > 1e-12, errs          # inexact, and really used
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    prob.load_vector(to_dev(cfg.f.ravel()), b)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=cfg.tol)
+    x_ref, st_ref = krylov.mpgmres(A, [P.apply for P in precs], p1.load_vector(cfg), tol=cfg.tol, maxit=200)
+    assert st["converged"] == 1 and st["iterations"] <= st_ref.iterations + 1
+    assert st["true_rel_res"] <= 10 * cfg.tol
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-4
+    for d in dirs:
+        d.set_precision(64)
+    hs.sweep_apply(dirs, to_dev(R), Z)
+    assert max(rel(Z[k].cpu().numpy(), P.apply(R[k])) for k, P in enumerate(precs)) <= 1e-10
