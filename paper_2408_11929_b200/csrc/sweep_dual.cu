@@ -49,6 +49,12 @@
 #ifndef HELM_DUAL_GSRC
 #define HELM_DUAL_GSRC 1   // 1: the separator-row source is staged into the g area at the pre-actions
 #endif
+#ifndef HELM_DUAL_XPRE
+#define HELM_DUAL_XPRE 0   // experiment: prefetch the next solve's X rows during phase 3 (1 evict_last, 2 normal, 3 evict_first)
+#endif
+#ifndef HELM_DUAL_XPRE_FRAC
+#define HELM_DUAL_XPRE_FRAC 4   // quarters of each X row prefetched early
+#endif
 #ifndef HELM_DUAL_XSYM
 #define HELM_DUAL_XSYM 0    // 1: read only the upper block triangle of X (each block by its two users)
 #endif
@@ -1006,6 +1012,22 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       pacc(1, pclk() - c0);
 #ifndef HELM_DUAL_ABL_NONEXT
       stage_next(i);
+#if HELM_DUAL_XPRE
+      // experiment: stream the NEXT solve's separator-inverse rows into L2 during this
+      // solve's phase 3 (the factor stream then mostly hits L2), so the next
+      // separator stage finds part of them resident
+      if (i + 1 < nsolve && p < P - 1 && tid >= 32 * (2 * A.nw - 1)) {
+        const int wn = tab[i + 1].w;
+        const long ld = x_ld(K, wn);
+        const uint32_t bytes = (uint32_t)((long)K * wn * (long)sizeof(cplx) * HELM_DUAL_XPRE_FRAC / 4);
+        const uint64_t pol = HELM_DUAL_XPRE == 1 ? pol_last : (HELM_DUAL_XPRE == 2 ? 0ull : pol_first);
+        for (int r = tid - 32 * (2 * A.nw - 1); r < wn; r += 32) {
+          const cplx* src = tab[i + 1].xinv + ((long)p * wn + r) * ld;
+          if (HELM_DUAL_XPRE == 2) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+          else dprefetch_l2(src, bytes, pol);
+        }
+      }
+#endif
 #else
       if (tid == 0) mbar_expect_tx(&sbar[0], 0);
 #endif
