@@ -34,6 +34,10 @@
 
 #include "sweep_common.cuh"
 
+#ifndef HELM_GEN_XPIPE
+#define HELM_GEN_XPIPE 0   // 1: pipelined L2 prefetch of the separator-inverse rows (wide strips)
+#endif
+
 // ------------------------------------------------------------------ tile pipeline
 // Warp-specialised ring: the last warp of the CTA is the TMA producer (one
 // elected lane walks the exact tile sequence the consumers will ask for and
@@ -467,8 +471,12 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         const long Kw = (long)K * w, xld = x_ld(K, w);
         if (p < D.P - 1 && tid < 32) {
           // this CTA's rows of the separator inverse into L2 during the gather
+          // (HELM_GEN_XPIPE: only the rows of the mat-vec's first pass; each warp then
+          // prefetches its next pass's rows while it computes the current one, so wide
+          // strips -- 5 MB of rows per CTA at C4 -- do not overflow L2)
           const char* xp = reinterpret_cast<const char*>(D.xinv + D.xinv_off[s] + (long)p * w * xld);
-          const long bytes = (long)w * xld * (long)sizeof(cplx);
+          const long rows_pf = HELM_GEN_XPIPE ? std::min<long>(w, 4L * (ncons >> 5)) : w;
+          const long bytes = rows_pf * xld * (long)sizeof(cplx);
           for (long o = (long)tid * 32768; o < bytes; o += 32L * 32768)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xp + o),
                          "r"((uint32_t)(bytes - o < 32768L ? bytes - o : 32768L)) : "memory");
@@ -543,6 +551,10 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
               ok[u] = rb + u < w;
               Xr[u] = D.xinv + D.xinv_off[s] + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
             }
+            if (HELM_GEN_XPIPE && lane < 4 && rb + 4 * ncw + lane < w)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                               D.xinv + D.xinv_off[s] + ((long)p * w + rb + 4 * ncw + lane) * xld),
+                           "r"((uint32_t)(Kw * (long)sizeof(cplx))) : "memory");
             cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
 #pragma unroll 2
             for (long jj = lane; jj < Kw; jj += 128) {   // two iterations' loads in flight
