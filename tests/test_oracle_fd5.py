@@ -124,7 +124,6 @@ def test_fd5_paper_table4_h8(gather):
     assert abs(_iters(fd5_cfg(256, 50.0), ["LRL", "BTB"], gather) - 8) <= 1
 
 
-@pytest.mark.slow
 @pytest.mark.parametrize("gather", ["recent", "core"])
 def test_fd5_paper_table1_k50(gather):
     """Table 1 / Table 2 / Table 5, h = 2^-9
@@ -133,7 +132,6 @@ def test_fd5_paper_table1_k50(gather):
     assert abs(_iters(fd5_cfg(512, 50.0), ["LRL", "BTB"], gather) - 9) <= 1
 
 
-@pytest.mark.slow
 def test_fd5_paper_table1_lrl_core():
     """Table 1, LRL alone at h = 2^-9, k = 50, N = 8: paper 20 iterations; the
     oracle with the "core" gather takes 17 (the literal "recent" gather
