@@ -159,3 +159,19 @@ def test_fd5_paper_table1_on_gpu(k, paper):
     _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=1e-6, maxit=120)
     assert st["converged"] == 1 and st["true_rel_res"] <= 1e-5
     assert abs(st["iterations"] - paper) <= 1, (k, st["iterations"], paper)
+
+
+@pytest.mark.parametrize("N,paper", [(16, 10), (32, 13)])
+def test_fd5_paper_table5_on_gpu(N, paper):
+    """The paper's Table 5, h = 2^-9, k = 50, LRL+BTB with N = 16 / 32
+    strips: 10 / 13 iterations.  The "core" gather (A16) reproduces the column
+    exactly (tools/fd5_tables_gpu.py --core --tables 5); +-1 here."""
+    cfg = fd5_cfg(512, 50.0, N=N)
+    prob = gpu_problem(cfg)
+    dirs = [hs.Sweep(prob, nm, n_strips=N, overlap=1, gather=1) for nm in ["LRL", "BTB"]]
+    b = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    prob.load_vector(to_dev(fd5.source(cfg)), b)
+    x = torch.zeros(cfg.n, dtype=torch.complex128, device=DEV)
+    _, st = hs.mpgmres_solve(prob, dirs, b, x, tol=1e-6, maxit=120)
+    assert st["converged"] == 1
+    assert abs(st["iterations"] - paper) <= 1, (N, st["iterations"], paper)
