@@ -140,7 +140,10 @@ __global__ void k_axpy_sub(long n, const cplx* __restrict__ b, const cplx* __res
 // summed redundantly by every block, which saves the grid sync that would
 // broadcast the keep/drop decision.  ~5 grid syncs per column instead of ~10
 // launches and a host round trip per column.
-static constexpr int kOrthTile = 1024;
+#ifndef HELM_ORTH_TILE
+#define HELM_ORTH_TILE 1024
+#endif
+static constexpr int kOrthTile = HELM_ORTH_TILE;
 static constexpr int kOrthThreads = 256;
 static constexpr int kIntraNV = 2 * 8 + 1;     // intra-block partial values per block (t <= 8)
 static constexpr long kIntraMaxBlk = 1024;     // blocks the intra-block partial region covers

@@ -66,6 +66,22 @@ def test_no_device_fails_loudly(lib):
     assert ei.value.code == 4   # HELM_ECUDA
 
 
+def test_missing_library_fails_loudly(tmp_path):
+    """Without the built CUDA library the product path raises at the first call
+    (there is no CPU fallback to land on)."""
+    import subprocess
+    import sys
+    code = ("import paper_2408_11929_b200 as hs\n"
+            "try:\n"
+            "    hs.Problem(8, 8, 1.0 / 8, 5.0)\n"
+            "except ImportError as e:\n"
+            "    print('IMPORTERROR', e)\n")
+    env = dict(os.environ, HELM_LIB=str(tmp_path / "libhelmsweep.so"), PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "IMPORTERROR" in out.stdout and "not built" in out.stdout
+
+
 def test_knobs_are_explicit_calls(lib):
     """Kernel / path choices are explicit helm_set_knob calls (no environment
     variable is read by the library); unknown names and values are rejected."""
