@@ -823,22 +823,6 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   // directions (P segment CTAs each, plus a reducer in the general kernel) must
   // be co-resident, one per SM.  A batch that cannot be (e.g. t = 8 with 33
   // segments) runs as two half batches, in order on the same stream.
-  if (t > 1) {
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    long need = 0;
-    for (int d = 0; d < t; ++d) need += dirs[d]->P + 1;
-    if (need > nsm) {
-      const int h = t / 2;
-      int rc = sweep_apply_dev(dirs, h, Rdev, ldr, Zdev, ldz, st);
-      if (rc != HELM_OK) return rc;
-      return sweep_apply_dev(dirs + h, t - h, Rdev + (ldr == 0 ? 0 : (long)h * ldr), ldr, Zdev + (long)h * ldz, ldz, st);
-    }
-  }
   // kernel choice: the two-chain block kernel (sweep_dual.cu) where it applies
   // (w <= 36, P > 1), else the single-chain register-streaming kernel
   // (sweep_fast.cu, w <= 36), else the general TMA-ring kernel.
@@ -846,10 +830,27 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   // (parity tests of every kernel); read per call.
   const int kn = helm_knob(KNOB_SWEEP_KERNEL);
   const int level = kn == 2 || kn == 3 ? kn : 1;
-  if (level <= 1) {
+  static int nsm_dev = 0;
+  if (!nsm_dev) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm_dev, cudaDevAttrMultiProcessorCount, dev);
+  }
+  long need = 0, need_dual = 0;   // CTAs: P per direction (two-chain), P + 1 (the others: a reducer each)
+  for (int d = 0; d < t; ++d) {
+    need += dirs[d]->P + 1;
+    need_dual += dirs[d]->P;
+  }
+  if (level <= 1 && need_dual <= nsm_dev) {
     g_sweep_kernel = "k_sweep_dual";
     int rc = sweep_apply_dual(dirs, t, Rdev, ldr, Zdev, ldz, st);
     if (rc != -1) return rc;
+  }
+  if (t > 1 && need > nsm_dev) {
+    const int h = t / 2;
+    int rc = sweep_apply_dev(dirs, h, Rdev, ldr, Zdev, ldz, st);
+    if (rc != HELM_OK) return rc;
+    return sweep_apply_dev(dirs + h, t - h, Rdev + (ldr == 0 ? 0 : (long)h * ldr), ldr, Zdev + (long)h * ldz, ldz, st);
   }
   if (level <= 2) {
     g_sweep_kernel = "k_sweep_fast";

@@ -64,6 +64,7 @@ if os.environ.get("HELM_CYCLES"):
         print(f"  separator stage per solve (cycles, thread 0): gather wait {sel[:,12].mean()/63:.0f}  "
               f"corrections+g {sel[:,14].mean()/63:.0f}  X mat-vec {sel[:,2].mean()/63:.0f}  neighbour wait {sel[:,13].mean()/63:.0f}  "
               f"total {sel[:,1].mean()/63:.0f};  pre-actions {sel[:,0].mean()/63:.0f}")
+        print(f"  balanced separator stage (thread 0, per solve): pass A {sel[:,15].mean()/63:.0f}  pass B {sel[:,11].mean()/63:.0f}")
     for role in (0, 1):
         sel = b[b[:, 6] == role]
         if len(sel) == 0:
