@@ -81,6 +81,9 @@
 #ifndef HELM_DUAL_BANDPF
 #define HELM_DUAL_BANDPF 0    // (measured 1% slower) 1: the next solve's couplings are prefetched into L2 at the start of phase 3
 #endif
+#ifndef HELM_DUAL_XPF_EARLY
+#define HELM_DUAL_XPF_EARLY 0   // > 0: the X rows are prefetched into L2 by the producer this many phase-1 blocks before the end
+#endif
 #ifndef HELM_DUAL_XBAL_PF
 #define HELM_DUAL_XBAL_PF 1   // balanced stage: L2 prefetch of the CTA's blocks (0 none, 1 normal priority, 2 evict_first)
 #endif
@@ -302,6 +305,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           const int ph = e >= m ? 1 : 0, js = e - ph * m;
           const bool up = (pg == 0) == (ph == 0);
           const cplx* src = fbase + (long)(up ? lo + js : hi - js) * pw;
+#if HELM_DUAL_XPF_EARLY > 0
+          if (!XF32 && pg == 0 && e == std::max(m - HELM_DUAL_XPF_EARLY, 0) && p < P - 1) {
+            // this solve's separator-inverse rows into L2 while phase 1 still runs
+            const int w2 = tab[i2].w;
+            const long ld = x_ld(K, w2);
+            for (int r = 0; r < w2; ++r)
+              dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
+          }
+#endif
           const int st = f % NST;
           if (f >= (uint32_t)NST) mbar_wait(&empty[pg * NST + st], ((f / NST) - 1) & 1);
           uint64_t* bar = &full[pg * NST + st];
@@ -535,7 +547,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int par = i & 1, ppar = par ^ 1;
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
-    if (p < P - 1 && tid < 32) {
+    if (p < P - 1 && tid < 32 && (HELM_DUAL_XPF_EARLY == 0 || XF32)) {
       // stream this CTA's part of the UPPER block triangle of the separator inverse
       // (row r of block row p, columns p w .. K w) into L2 while the all-gather
       // completes; the mat-vec reads it from L2, and so does CTA k > p, which uses
