@@ -250,10 +250,121 @@ struct RowSmem {
   cplx mat[kRowW * kRowW];    // natural-order inverse of the current block / Y
   cplx tmat[kRowW * kRowW];   // U_c Y (kind 0, X[lo,hi] chain)
   cplx prow[kRowW];
-  unsigned redk[kRowWarps];
-  int redi[kRowWarps];
+  cplx pcol[2][kRowW];        // row_invert_g: pivot-column entries (multipliers), by step parity
+  cplx pdinv;                 // row_invert_g: 1 / pivot
+  unsigned redk[12];
+  int redi[12];
   int pivrow[kRowW];
 };
+
+__device__ long long g_red_prof[8];   // diagnostics (setup_timing knob): block 0 sub-phase cycles
+// a[kj] for a runtime index kj < N by a select tree on the bits of kj
+template <int N>
+__device__ __forceinline__ cplx sel_idx(const cplx (&a)[N], int kj) {
+  cplx t[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) t[u] = a[u];
+#pragma unroll
+  for (int st = 1; st < N; st <<= 1) {
+    const bool bit = kj & st;
+#pragma unroll
+    for (int u = 0; u + st < N; u += 2 * st) t[u] = bit ? t[u + st] : t[u];
+  }
+  return t[0];
+}
+
+// Gauss-Jordan inversion of the w x w block held LPR threads per row (thread
+// (i, h) holds columns LPR jj + h), the same pivot rule and elementary operations
+// as row_invert; the pivot row is broadcast raw with 1/pivot (the scaling of the
+// pivot row itself and of the multipliers happens after the broadcast barrier,
+// off its critical path), the multipliers through shared memory (rows may straddle
+// warps).  Used by k_reduced with more threads per row (shorter pivot steps).
+template <int LPR>
+__device__ __forceinline__ int row_invert_g(cplx (&a)[kRowW / LPR], int w, RowSmem& sm) {
+  constexpr int HW = kRowW / LPR;
+  constexpr int NWR = (kRowW * LPR + 31) / 32;   // warps holding rows
+  static_assert(kRowW % LPR == 0 && NWR <= 12, "row_invert_g layout");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i = tid / LPR, h = tid % LPR;
+  const bool active = i < w;
+  bool used = false;
+  int kstep = 0;
+#pragma unroll 1
+  for (int k = 0; k < w; ++k) {
+    const int kh = k % LPR, kj = k / LPR, par = k & 1;
+#ifdef HELM_GJ_PROF
+    const bool pr = blockIdx.x == 0 && tid == 0;
+    long long q0 = pr ? clock64() : 0;
+#endif
+    const cplx mine = sel_idx(a, kj);
+    const bool cand = active && !used && h == kh;
+    const unsigned key = cand ? (unsigned)__double2hiint(cabs2(mine)) + 1u : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    const unsigned who = __ballot_sync(0xffffffffu, key == kmax);
+    if (lane == 0 && warp < NWR) { sm.redk[warp] = kmax; sm.redi[warp] = (warp * 32 + __ffs(who) - 1) / LPR; }
+    if (active && h == kh) sm.pcol[par][i] = mine;
+    __syncthreads();
+#ifdef HELM_GJ_PROF
+    long long q1 = pr ? clock64() : 0;
+    if (pr) g_red_prof[3] += q1 - q0;
+#endif
+    unsigned k0 = sm.redk[0];
+    int p = sm.redi[0];
+#pragma unroll
+    for (int q = 1; q < NWR; ++q)
+      if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
+    if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
+    if (i == p) {
+#pragma unroll
+      for (int jj = 0; jj < HW; ++jj) sm.prow[LPR * jj + h] = a[jj];
+      if (h == kh) {
+        // the pivot column is broadcast as pivot + 1: a_ik - (a_ik / piv)(piv + 1) = -a_ik / piv
+        sm.prow[k] = cmk(mine.x + 1.0, mine.y);
+#ifdef HELM_GJ_DRCP
+        { const double dd = __drcp_rn(cabs2(mine)); sm.pdinv = cmk(mine.x * dd, -mine.y * dd); }
+#else
+        sm.pdinv = cinv(mine);
+#endif
+      }
+    }
+    __syncthreads();
+#ifdef HELM_GJ_PROF
+    long long q2 = pr ? clock64() : 0;
+    if (pr) g_red_prof[4] += q2 - q1;
+#endif
+    const cplx dinv = sm.pdinv;
+    if (i == p) {
+#pragma unroll
+      for (int jj = 0; jj < HW; ++jj) a[jj] = (h == kh && jj == kj) ? dinv : cmul(a[jj], dinv);
+      used = true;
+      kstep = k;
+      if (h == 0) sm.pivrow[k] = p;
+    } else if (active) {
+      const cplx f = cmul(sm.pcol[par][i], dinv);
+#pragma unroll
+      for (int jj = 0; jj < HW; ++jj) {
+        const cplx r = sm.prow[LPR * jj + h];
+        a[jj].x = fma(-f.x, r.x, a[jj].x);
+        a[jj].x = fma(f.y, r.y, a[jj].x);
+        a[jj].y = fma(-f.x, r.y, a[jj].y);
+        a[jj].y = fma(-f.y, r.x, a[jj].y);
+      }
+    }
+#ifdef HELM_GJ_PROF
+    if (pr) { __syncwarp(1u); g_red_prof[5] += clock64() - q2; }
+#endif
+  }
+  __syncthreads();   // pivrow complete; everyone is done reading mat from the previous block
+  if (active) {
+#pragma unroll
+    for (int jj = 0; jj < HW; ++jj) {
+      const int j = LPR * jj + h;
+      if (j < w) sm.mat[kstep * kRowW + sm.pivrow[j]] = a[jj];
+    }
+  }
+  __syncthreads();
+  return 0;
+}
 
 // Invert the w x w block held as described above; leaves the inverse in
 // sm.mat (natural order, row stride kRowW).  Returns 1 (uniformly) on a zero pivot.
@@ -443,6 +554,9 @@ __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem
   }
 }
 
+#ifndef HELM_FAC_G
+#define HELM_FAC_G 0        // 1: k_factor_rows uses row_invert_g (raw pivot-row broadcast)
+#endif
 #ifndef HELM_FAC_MINB
 #define HELM_FAC_MINB 5   // 5 CTAs per SM (a few spills) beat 4 without
 #endif
@@ -462,7 +576,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
   if (kind == 0) {
     for (int c = lo; c <= hi; ++c) {
       row_schur(a, w, B(fa.dg, c), B(fa.al, c), B(fa.cr, c - 1), B(fa.ne, c - 1), c > lo, true, sm);
-      if (row_invert(a, w, sm)) {
+      if (HELM_FAC_G ? row_invert_g<kLPR>(a, w, sm) : row_invert(a, w, sm)) {
         if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
         return;
       }
@@ -471,7 +585,11 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
     }
     if (fa.P == 1) return;
     // X[lo,hi]: Y_hi = Sinv_hi (in sm.mat); Y_c = -Sinv_c (U_c Y_{c+1})
+#ifdef HELM_FAC_NOXCHAIN
+    for (int c = hi - 1; c >= hi; --c) {   // ablation (timing only): no X chain
+#else
     for (int c = hi - 1; c >= lo; --c) {
+#endif
       const cplx* cr = B(fa.cr, c);
       const cplx* ne = B(fa.ne, c);
       if (i < w) {
@@ -535,7 +653,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
   } else {
     for (int c = hi; c >= lo; --c) {
       row_schur(a, w, B(fa.dg, c), B(fa.al, c), B(fa.cr, c), B(fa.ne, c), c < hi, false, sm);
-      if (row_invert(a, w, sm)) {
+      if (HELM_FAC_G ? row_invert_g<kLPR>(a, w, sm) : row_invert(a, w, sm)) {
         if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
         return;
       }
@@ -566,11 +684,14 @@ struct RedArgs {
 // separator block-Thomas is a chain).  Block inverses use the register-row
 // Gauss-Jordan of k_factor_rows; products use register-tiled smem matmuls.
 // Shared memory: RowSmem (static) + S, T1 (R_{k,k+1}), T2 (F_k) (dynamic).
-__device__ long long g_red_prof[8];   // diagnostics (setup_timing knob): block 0 sub-phase cycles
 
 // 384 threads: the register-row Gauss-Jordan uses the first 96 (the others only
 // join its barriers); the products, stencil applications and copies use all.
 static constexpr int kRedThreads = 384;
+#ifndef HELM_RED_LPR
+#define HELM_RED_LPR 9      // threads per block row of k_reduced's Gauss-Jordan (kRowW * LPR <= 384)
+#endif
+static constexpr int kRedLPR = HELM_RED_LPR;
 __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   __shared__ RowSmem sm;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -635,14 +756,17 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     if (k >= 1) blk_mm_tiled2(S, w, T1, w, true, T2, w, w, -1.0, true);
     long long c1 = pr ? clock64() : 0;
     if (pr) g_red_prof[0] += c1 - c0;
-    // Rinv_k (register-row Gauss-Jordan; result in sm.mat, row stride kRowW)
-    cplx a[kRowHW];
+    // Rinv_k (register-row Gauss-Jordan, kRedLPR threads per row; result in sm.mat, row stride kRowW)
+    cplx a[kRowW / kRedLPR];
+    {
+      const int ir = threadIdx.x / kRedLPR, hr = threadIdx.x % kRedLPR;
 #pragma unroll
-    for (int jj = 0; jj < kRowHW; ++jj) {
-      const int col = kLPR * jj + h;
-      a[jj] = (i < w && col < w) ? S[i * w + col] : cmk(0, 0);
+      for (int jj = 0; jj < kRowW / kRedLPR; ++jj) {
+        const int col = kRedLPR * jj + hr;
+        a[jj] = (ir < w && col < w) ? S[ir * w + col] : cmk(0, 0);
+      }
     }
-    if (row_invert(a, w, sm)) {
+    if (row_invert_g<kRedLPR>(a, w, sm)) {
       if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
       return;
     }
@@ -1160,8 +1284,10 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
             t1, t2, t3, t4);
     long long rp[8];
     if (cudaMemcpyFromSymbol(rp, g_red_prof, sizeof(rp)) == cudaSuccess && P > 1) {
-      fprintf(stderr, "[k_reduced] per separator (block 0): build+RtF %lld, invert %lld, store+G+F %lld cycles\n",
-              rp[0] / (P - 1), rp[1] / (P - 1), rp[2] / (P - 1));
+      fprintf(stderr, "[k_reduced] per separator (block 0): build+RtF %lld, invert %lld, store+G+F %lld cycles"
+              " | per pivot: search %lld, publish %lld, update %lld\n",
+              rp[0] / (P - 1), rp[1] / (P - 1), rp[2] / (P - 1), rp[3] / ((P - 1) * (long long)wmax),
+              rp[4] / ((P - 1) * (long long)wmax), rp[5] / ((P - 1) * (long long)wmax));
       long long z[8] = {0};
       cudaMemcpyToSymbol(g_red_prof, z, sizeof(z));
     }
