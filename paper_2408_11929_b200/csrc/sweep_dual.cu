@@ -84,6 +84,12 @@
 #ifndef HELM_DUAL_XPF_EARLY
 #define HELM_DUAL_XPF_EARLY 0   // > 0: the X rows are prefetched into L2 by the producer this many phase-1 blocks before the end
 #endif
+#ifndef HELM_DUAL_XPF_PROD
+#define HELM_DUAL_XPF_PROD 1    // 1: the X-row L2 prefetch is issued by the chain-A producer warp when phase 1 ends
+#endif
+#ifndef HELM_DUAL_EPIREL
+#define HELM_DUAL_EPIREL 1    // 1: the epilogue counter is released by chain B's producer lane (not thread 0 before a barrier)
+#endif
 #ifndef HELM_DUAL_XBAL_PF
 #define HELM_DUAL_XBAL_PF 1   // balanced stage: L2 prefetch of the CTA's blocks (0 none, 1 normal priority, 2 evict_first)
 #endif
@@ -132,7 +138,7 @@ struct DualArgs {
   int stage_elems;  // cplx per ring stage (>= largest packed block + 1 zero entry)
   int mmax;         // largest segment (rows)
   int xbw_off;      // cplx offset from the vector areas of the balanced separator solve's workspace
-  long long* prof;  // optional per-CTA counters (16 per CTA)
+  long long* prof;  // optional per-CTA counters (24 per CTA)
 };
 
 struct DualTab {
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       mbar_init(&full[e], 1);
       mbar_init(&empty[e], 1);
     }
-    for (int e = 0; e < 3; ++e) mbar_init(&sbar[e], 1);
+    for (int e = 0; e < 4; ++e) mbar_init(&sbar[e], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int lo = D_.seg_lo[p], hi = D_.seg_hi[p];
@@ -316,6 +322,25 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
           const int st = f % NST;
           if (f >= (uint32_t)NST) mbar_wait(&empty[pg * NST + st], ((f / NST) - 1) & 1);
+#if HELM_DUAL_EPIREL
+          if (pg == 1 && i2 >= 1 && e == std::min(NST - 1, 2 * m - 1)) {
+            // the epilogue of solve i2 - 1 is complete (CTA-scope arrival of thread 0 after
+            // the consumers' barrier): publish it to the other segments
+            mbar_wait(&sbar[3], (i2 - 1) & 1);
+            red_release_add(&D_.cnt[1], 1u);
+          }
+#endif
+#if HELM_DUAL_XPF_PROD
+          if (!XF32 && pg == 0 && e == std::min(m + NST - 1, 2 * m - 1) && p < P - 1) {
+            // chain A has released its last phase-1 block: this solve's separator stage
+            // starts now -- stream this CTA's separator-inverse rows into L2 from here
+            // (off the consumers' barriers)
+            const int w2 = tab[i2].w;
+            const long ld = x_ld(K, w2);
+            for (int r = 0; r < w2; ++r)
+              dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
+          }
+#endif
           uint64_t* bar = &full[pg * NST + st];
           const uint32_t bytes = (uint32_t)(pw * sizeof(cplx));
           mbar_expect_tx(bar, bytes);
@@ -338,14 +363,14 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // they cost no registers: [0] pre-actions [1] separator stage [2] X mat-vec
   // [4] waits [8..11] step sub-phases (mat-vec, loads+reduce, writer, barrier)
   // [12] gather wait [13] neighbour wait [14] corrections + g
-  __shared__ long long profs[16];
+  __shared__ long long profs[24];
   auto pacc = [&](int k, long long v) {
     if constexpr (kProf) {
       if (tid == 0) profs[k] += v;
     }
   };
   if (kProf && tid == 0)
-    for (int k = 0; k < 16; ++k) profs[k] = 0;
+    for (int k = 0; k < 24; ++k) profs[k] = 0;
   const long long t_start = pclk();
   auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
   auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory"); };
@@ -547,7 +572,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int par = i & 1, ppar = par ^ 1;
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
-    if (p < P - 1 && tid < 32 && (HELM_DUAL_XPF_EARLY == 0 || XF32)) {
+    const long long csep0 = pclk();
+    if (p < P - 1 && tid < 32 && ((HELM_DUAL_XPF_EARLY == 0 && !HELM_DUAL_XPF_PROD) || XF32)) {
       // stream this CTA's part of the UPPER block triangle of the separator inverse
       // (row r of block row p, columns p w .. K w) into L2 while the all-gather
       // completes; the mat-vec reads it from L2, and so does CTA k > p, which uses
@@ -598,6 +624,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     }
     cbar();
     const long long cw0 = pclk();
+    pacc(16, cw0 - csep0);
     const bool need_corr = st > 0 || bwd;
     if (tid == 0) {
       HELM_DUAL_FENCE();
@@ -952,6 +979,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         st_release(&D_.flag[p], (unsigned)(i + 1));
       }
     }
+    pacc(17, pclk() - cx0);   // X mat-vec + fixups + publication
     if (p > 0) {
       const long long cw1 = pclk();
       if (tid == 0) {
@@ -965,6 +993,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       cbar();
     }
     }
+    const long long cvi = pclk();
     // phase-3 inputs: chain A  U_hi x_p;  chain B  -U_{lo-1}^T x_{p-1}
     cplx* vA = vbuf + 0 * 2 * WM + cur * WM;
     cplx* vB = vbuf + 1 * 2 * WM + cur * WM;
@@ -978,6 +1007,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (qq >= 1) cfma(tb, bne[qq - 1], xlo[qq - 1]);
       vB[qq] = cscale(tb, -1.0);
     }
+    pacc(18, pclk() - cvi);
   };
 
   // ------------------------------------------------------------ one phase of this group's chain
@@ -1167,21 +1197,34 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       // ---- pre-actions: epilogue of the previous solve, RHS, phase-1 inputs
       long long c0 = pclk();
       cbar();
+      if (!kProfStep) pacc(9, pclk() - c0);   // the other chain group's phase 3 tail
+      const long long csb = pclk();
       stage_bands(i);
+      pacc(22, pclk() - csb);
       if (i == 0) {
         stage_rhs0();
         mbar_wait(&sbar[2], 0);
       } else {
         mbar_wait(&sbar[0], (i - 1) & 1);   // staged during phase 3 of solve i-1
         cp_async_wait_all();
+        pacc(23, pclk() - csb);
         seg_epilogue(i - 1);
         cbar();
         // epilogue counter: solve i-1's boundary rows (xb) and separators (xs) are
         // published; the separator stage of solve i forms its corrections from them
+#if HELM_DUAL_EPIREL
+        // (the release itself -- a gpu-scope fence behind this CTA's Z stores -- is
+        // done by chain B's producer lane after this CTA-scope arrival, off the barrier)
+        if (tid == 0) mbar_arrive(&sbar[3]);
+#else
         if (tid == 0) red_release_add(&D_.cnt[1], 1u);
+#endif
       }
+      const long long cpb = pclk();
+      if (!kProfStep) pacc(10, cpb - c0);
       mbar_wait(&sbar[1], i & 1);
       cbar();
+      if (!HELM_DUAL_XBAL) pacc(15, pclk() - cpb);   // couplings landed
       seg_rhs(i);
 #if HELM_DUAL_GSRC
       {
@@ -1211,6 +1254,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       }
       cbar();
       pacc(0, pclk() - c0);
+      const long long cph1 = pclk();
 #if HELM_DUAL_ONELOOP
       if (g == 0) run_phase(i, I0{}, I0{});
       else run_phase(i, I1{}, I0{});
@@ -1219,10 +1263,12 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
       // ---- separator stage, phase-3 inputs
       c0 = pclk();
+      pacc(19, c0 - cph1);
       cbar();
       seg_separators(i);
       cbar();
       pacc(1, pclk() - c0);
+      const long long csn = pclk();
 #ifndef HELM_DUAL_ABL_NONEXT
       stage_next(i);
 #if HELM_DUAL_XPRE
@@ -1244,12 +1290,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #else
       if (tid == 0) mbar_expect_tx(&sbar[0], 0);
 #endif
+      const long long cph3 = pclk();
+      pacc(21, cph3 - csn);
 #if HELM_DUAL_ONELOOP
       if (g == 0) run_phase(i, I0{}, I1{});
       else run_phase(i, I1{}, I1{});
 #else
       run_phase(i, G_, I1{});
 #endif
+      pacc(20, pclk() - cph3);
     }
   };
 #if HELM_DUAL_ONELOOP
@@ -1262,8 +1311,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   mbar_wait(&sbar[0], (nsolve - 1) & 1);
   seg_epilogue(nsolve - 1);
   if (kProf && A.prof && tid == 0) {
-    long long* o = A.prof + (long)blockIdx.x * 16;
-    for (int k = 0; k < 16; ++k) o[k] = profs[k];
+    long long* o = A.prof + (long)blockIdx.x * 24;
+    for (int k = 0; k < 24; ++k) o[k] = profs[k];
     o[3] = total;
     o[5] = pclk() - t_start; o[6] = 1; o[7] = d;
   }

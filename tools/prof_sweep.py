@@ -47,7 +47,7 @@ if os.environ.get("HELM_CYCLES"):
     import ctypes
     L = hs.load()
     ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)  # upper bound
-    stride = 16 if hs.sweep_kernel_name() == "k_sweep_dual" else 8
+    stride = 24 if hs.sweep_kernel_name() == "k_sweep_dual" else 8
     buf = torch.zeros(ctas * stride, dtype=torch.int64, device=dev)
     L.helm_sweep_profile.argtypes = [ctypes.c_void_p]
     L.helm_sweep_profile(ctypes.c_void_p(buf.data_ptr()))
@@ -55,7 +55,7 @@ if os.environ.get("HELM_CYCLES"):
     torch.cuda.synchronize()
     L.helm_sweep_profile(ctypes.c_void_p(0))
     b = buf.view(ctas, stride).cpu().numpy()
-    if stride == 16:
+    if stride == 24:
         sel = b[b[:, 3] > 0]
         tp = sel[:, 8:12].mean(axis=0) / sel[:, 3].mean()
         print(f"  dual step sub-phases (cycles/step, thread 0): mat-vec {tp[0]:.0f}  loads+reduce+nb {tp[1]:.0f}  "
@@ -65,6 +65,10 @@ if os.environ.get("HELM_CYCLES"):
               f"corrections+g {sel[:,14].mean()/63:.0f}  X mat-vec {sel[:,2].mean()/63:.0f}  neighbour wait {sel[:,13].mean()/63:.0f}  "
               f"total {sel[:,1].mean()/63:.0f};  pre-actions {sel[:,0].mean()/63:.0f}")
         print(f"  balanced separator stage (thread 0, per solve): pass A {sel[:,15].mean()/63:.0f}  pass B {sel[:,11].mean()/63:.0f}")
+        print(f"  pre-actions (thread 0, per solve): other group's tail {sel[:,9].mean()/63:.0f}  through epilogue {sel[:,10].mean()/63:.0f}  "
+              f"coupling wait (slot 15) {sel[:,15].mean()/63:.0f}  stage_bands issue {sel[:,22].mean()/63:.0f}  +staging waits {sel[:,23].mean()/63:.0f}")
+        print(f"  phases (thread 0, per solve): phase 1 {sel[:,19].mean()/63:.0f}  phase 3 {sel[:,20].mean()/63:.0f}  stage_next {sel[:,21].mean()/63:.0f} | "
+              f"separator stage: yb {sel[:,16].mean()/63:.0f}  X+publish {sel[:,17].mean()/63:.0f}  x_lo+inputs {sel[:,18].mean()/63:.0f}")
     for role in (0, 1):
         sel = b[b[:, 6] == role]
         if len(sel) == 0:

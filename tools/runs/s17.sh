@@ -1,0 +1,5 @@
+HELM_CYCLES=1 HELM_LIB=$PWD/paper_2408_11929_b200/libhelmsweep_prof.so python tools/prof_sweep.py --reps 5 2>&1 | grep -v "Warn\|nan\|^  st\|^  ret\|^  print\|^  f\"\|sub-phases"
+python tools/prof_sweep.py --reps 20
+HELM_LIB=$PWD/paper_2408_11929_b200/libhelmsweep_ep0.so python tools/prof_sweep.py --reps 20
+python tools/prof_sweep.py --reps 20
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
