@@ -231,6 +231,7 @@ const char* helm_sweep_kernel_name(void);
  *   "orth_unfused"     1: multi-launch BCGS2 instead of the fused k_orth
  *   "setup_timing"     1: sweep_setup prints its phase times to stderr
  *   "orth_prof"        1: k_orth prints phase clock stamps to stderr
+ *   "setup_chunks"     n > 1: sweep_setup pipelines its strips in n chunks on forked streams (0 / 1: one pass)
  * Every knob selects a different, parity-tested kernel or schedule for the same
  * arithmetic.  Not synchronised with calls running on other host threads.
  * Errors: HELM_EINVAL (unknown name or value). */

@@ -51,6 +51,7 @@ enum HelmKnob {
   KNOB_ORTH_UNFUSED,        // 1: multi-launch BCGS2 instead of the fused cooperative k_orth
   KNOB_SETUP_TIMING,        // 1: sweep_setup prints its phase times to stderr
   KNOB_ORTH_PROF,           // 1: k_orth phase clock stamps to stderr
+  KNOB_SETUP_CHUNKS,        // 0 auto, n: sweep_setup pipelines its strips in n chunks (1 = one pass)
   KNOB_COUNT
 };
 int helm_knob(int id);

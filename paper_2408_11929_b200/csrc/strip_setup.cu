@@ -149,6 +149,7 @@ struct FacArgs {
   cplx* fac2;      // packed bottom-up inverses S'^{-1}_c, NULL = not kept
   cplx* facp;      // packed top-down inverses Sinv_c, NULL = not kept
   const long* pfac_off;
+  int s0;          // first strip of this launch (the setup runs in strip chunks)
 };
 
 __device__ inline void build_D(cplx* S, const cplx* dg, const cplx* al, int w) {
@@ -165,7 +166,7 @@ __device__ inline void build_D(cplx* S, const cplx* dg, const cplx* al, int w) {
 
 __global__ void k_factor_segments(FacArgs fa) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.y, pseg = blockIdx.x;
+  const int s = blockIdx.y + fa.s0, pseg = blockIdx.x;
   const int w = fa.w[s];
   cplx* S = reinterpret_cast<cplx*>(smem_raw);
   cplx* colv = S + w * w;
@@ -562,7 +563,7 @@ __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem
 #endif
 __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacArgs fa) {
   __shared__ RowSmem sm;
-  const int s = blockIdx.y, pseg = blockIdx.x, kind = blockIdx.z;
+  const int s = blockIdx.y + fa.s0, pseg = blockIdx.x, kind = blockIdx.z;
   if (kind == 1 && fa.P == 1) return;
   const int w = fa.w[s];
   const int lo = fa.seg_lo[pseg], hi = fa.seg_hi[pseg];
@@ -678,6 +679,7 @@ struct RedArgs {
   cplx* red;
   cplx* rscratch;  // per strip: 2 w^2 (R_{k,k+1} of the previous separator, temp)
   int* status;
+  int s0;          // first strip of this launch
 };
 
 // One CTA (96 threads) per strip walks the K = P-1 separators in order (the
@@ -695,7 +697,7 @@ static constexpr int kRedLPR = HELM_RED_LPR;
 __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   __shared__ RowSmem sm;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.x;
+  const int s = blockIdx.x + ra.s0;
   const int w = ra.w[s];
   const long w2 = (long)w * w;
   cplx* S = reinterpret_cast<cplx*>(smem_raw);
@@ -797,7 +799,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
 // general block width (w > 36): generic smem Gauss-Jordan and matmuls
 __global__ void k_reduced_generic(RedArgs ra) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.x;
+  const int s = blockIdx.x + ra.s0;
   const int w = ra.w[s];
   const long w2 = (long)w * w;
   cplx* S = reinterpret_cast<cplx*>(smem_raw);
@@ -863,7 +865,7 @@ __global__ void k_reduced_generic(RedArgs ra) {
 template <int NT>
 __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.y, j = blockIdx.x;
+  const int s = blockIdx.y + ra.s0, j = blockIdx.x;
   const int K = ra.P - 1;
   if (j >= K) return;
   const int w = ra.w[s];
@@ -944,7 +946,7 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
 // operands from L1/L2.  The CTA only reads blocks it wrote itself (same SM: the
 // write-through L1 stays coherent after the barrier ending each product).
 __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* xinv, const long* xinv_off) {
-  const int s = blockIdx.y, j = blockIdx.x;
+  const int s = blockIdx.y + ra.s0, j = blockIdx.x;
   const int K = ra.P - 1;
   if (j >= K) return;
   const int w = ra.w[s];
@@ -980,6 +982,9 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
 // and 4 directions x 33 segments = 132 CTAs fit the 148 SMs; C2: 16 / 24 / 32
 // segments 0.56 / 0.50 / 0.53 ms -- more, shorter segments pay while the
 // separator system stays small).
+#ifndef HELM_SEG_EXTRA
+#define HELM_SEG_EXTRA 0   // where the segments with one more row go (0 first, 1 last, 2 middle)
+#endif
 static int choose_segments(int nc, int requested) {
   if (requested > 0) return requested;
   int P = 33;
@@ -1056,7 +1061,13 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   {
     int rows = nc - (P - 1), sb = rows / P, se = rows % P, c = 0;
     for (int p = 0; p < P; ++p) {
+#if HELM_SEG_EXTRA == 1
+      int m = sb + (p >= P - se ? 1 : 0);                 // the longer segments last
+#elif HELM_SEG_EXTRA == 2
+      int m = sb + ((p >= (P - se) / 2 && p < (P - se) / 2 + se) ? 1 : 0);   // in the middle
+#else
       int m = sb + (p < se ? 1 : 0);
+#endif
       h->seg_lo.push_back(c);
       h->seg_hi.push_back(c + m - 1);
       c += m + 1;  // skip the separator row
@@ -1219,49 +1230,82 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   int threads = wmax * wmax >= 1024 ? 512 : 256;
   FacArgs fa{h->d_w, h->d_fac_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr, h->d_ne,
              nc, wmax, P, h->d_fac, scratch, sstride, d_status, h->d_fac2, h->d_facp, h->d_pfac_off};
-  if (timing) cudaEventRecord(tev[1], st);
-  if (wmax <= kRowW && !helm_knob(KNOB_FACTOR_GENERIC))
-    k_factor_rows<<<dim3(P, n_strips, 2), kRowThreads, 0, st>>>(fa);
-  else
-    k_factor_segments<<<dim3(P, n_strips), threads, smem, st>>>(fa);
-  if (timing) cudaEventRecord(tev[2], st);
-  g_helm_launches++;
-  e = cudaGetLastError();
-  if (e == cudaSuccess && P > 1) {
-    RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
-               h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
-    if (wmax <= kRowW) {
-      const size_t smr = sizeof(cplx) * (9 * (size_t)wmax * wmax + 12 * (size_t)wmax);
-      cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-      k_reduced<<<n_strips, kRedThreads, smr, st>>>(ra);
-    } else {
-      k_reduced_generic<<<n_strips, threads, smem, st>>>(ra);
-    }
-    if (timing) cudaEventRecord(tev[3], st);
+  RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
+             h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
+  const size_t smr = sizeof(cplx) * (9 * (size_t)wmax * wmax + 12 * (size_t)wmax);
+  const size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
+  if (P > 1 && wmax <= kRowW) cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+  if (P > 1 && want_xinv && wmax <= kXinvMaxW)
+    cudaFuncSetAttribute(k_reduced_inverse<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+  const bool rows_kernel = wmax <= kRowW && !helm_knob(KNOB_FACTOR_GENERIC);
+  // strips [s0, s0 + ns): segment factors, separator factors, separator-inverse rows
+  auto run_chunk = [&](cudaStream_t cs, int s0, int ns, cudaEvent_t fac_done) {
+    FacArgs fc = fa;
+    fc.s0 = s0;
+    if (timing) cudaEventRecord(tev[1], cs);
+    if (rows_kernel)
+      k_factor_rows<<<dim3(P, ns, 2), kRowThreads, 0, cs>>>(fc);
+    else
+      k_factor_segments<<<dim3(P, ns), threads, smem, cs>>>(fc);
+    if (fac_done) cudaEventRecord(fac_done, cs);
+    if (timing) cudaEventRecord(tev[2], cs);
     g_helm_launches++;
-    e = cudaGetLastError();
-    if (e == cudaSuccess && want_xinv) {
-      // explicit separator inverse rows for the register-streaming kernel
-      const long tot = xinv_total;
-      if (e == cudaSuccess) {
-        size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
-        const int ri_nt = 128;   // 256 threads measured slower (round 1)
-        if (wmax > kXinvMaxW) {
-          k_reduced_inverse_glb<<<dim3(P - 1, n_strips), 256, 0, st>>>(ra, h->d_xinv, h->d_xinv_off);
-        } else if (ri_nt >= 256) {
-          cudaFuncSetAttribute(k_reduced_inverse<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-          k_reduced_inverse<256><<<dim3(P - 1, n_strips), 256, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
-        } else {
-          cudaFuncSetAttribute(k_reduced_inverse<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-          k_reduced_inverse<128><<<dim3(P - 1, n_strips), 128, sm3, st>>>(ra, h->d_xinv, h->d_xinv_off);
-        }
-        if (timing) cudaEventRecord(tev[4], st);
+    cudaError_t e2 = cudaGetLastError();
+    if (e2 == cudaSuccess && P > 1) {
+      RedArgs rc = ra;
+      rc.s0 = s0;
+      if (wmax <= kRowW) k_reduced<<<ns, kRedThreads, smr, cs>>>(rc);
+      else k_reduced_generic<<<ns, threads, smem, cs>>>(rc);
+      if (timing) cudaEventRecord(tev[3], cs);
+      g_helm_launches++;
+      e2 = cudaGetLastError();
+      if (e2 == cudaSuccess && want_xinv) {
+        // explicit separator inverse rows for the register-streaming kernel
+        // (128 threads: 256 measured slower, round 1)
+        if (wmax > kXinvMaxW) k_reduced_inverse_glb<<<dim3(P - 1, ns), 256, 0, cs>>>(rc, h->d_xinv, h->d_xinv_off);
+        else k_reduced_inverse<128><<<dim3(P - 1, ns), 128, sm3, cs>>>(rc, h->d_xinv, h->d_xinv_off);
+        if (timing) cudaEventRecord(tev[4], cs);
         g_helm_launches++;
-        e = cudaGetLastError();
-        h->factor_bytes += tot * (long)sizeof(cplx);
+        e2 = cudaGetLastError();
       }
     }
+    if (e == cudaSuccess) e = e2;
+  };
+  // Optional (setup_chunks knob): the strips pipelined in chunks on forked
+  // streams, chunk c + 1's segment factors starting when chunk c's are done, so
+  // that chunk c's separator chain (long latency, one CTA per strip) runs beside
+  // them.  Measured slower on C5 (both axes: 1 chunk 15.8 ms, 2: 16.9, 4: 18.5,
+  // 8: 23.9) -- a chunk's segment factors are one long partial wave -- so the
+  // default is one pass.
+  int nchunk = helm_knob(KNOB_SETUP_CHUNKS);
+  if (nchunk <= 0) nchunk = 1;
+  if (timing) nchunk = 1;
+  nchunk = std::min(std::min(nchunk, n_strips), 8);
+  if (nchunk == 1) {
+    run_chunk(st, 0, n_strips, nullptr);
+  } else {
+    // per host thread (the two axes are set up from two threads concurrently)
+    thread_local cudaStream_t cs[8] = {};
+    thread_local cudaEvent_t ev_fac[8] = {}, ev_done[8] = {}, ev_fork = nullptr;
+    if (!ev_fork) {
+      for (int c = 0; c < 8; ++c) {
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs[c], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_fac[c], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done[c], cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ev_fork, st);
+    for (int c = 0; c < nchunk && e == cudaSuccess; ++c) {
+      const int s0 = (int)((long)n_strips * c / nchunk), s1 = (int)((long)n_strips * (c + 1) / nchunk);
+      cudaStreamWaitEvent(cs[c], ev_fork, 0);
+      if (c > 0) cudaStreamWaitEvent(cs[c], ev_fac[c - 1], 0);
+      run_chunk(cs[c], s0, s1 - s0, ev_fac[c]);
+      cudaEventRecord(ev_done[c], cs[c]);
+      cudaStreamWaitEvent(st, ev_done[c], 0);
+    }
   }
+  if (P > 1 && want_xinv) h->factor_bytes += xinv_total * (long)sizeof(cplx);
   // wait for this setup's kernels first, then read the status: a pageable copy
   // issued while the stream is busy blocks inside the driver and serialises
   // setups running concurrently on other streams / host threads

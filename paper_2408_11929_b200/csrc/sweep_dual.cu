@@ -316,8 +316,18 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
             // this solve's separator-inverse rows into L2 while phase 1 still runs
             const int w2 = tab[i2].w;
             const long ld = x_ld(K, w2);
-            for (int r = 0; r < w2; ++r)
-              dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
+            if (HELM_DUAL_XBAL) {
+              const int last = xbal_last(p, K);
+              const int n1 = std::min(last + 1, K - p), n2 = last + 1 - n1;
+              for (int r = 0; r < w2; ++r) {
+                const cplx* row = tab[i2].xinv + ((long)p * w2 + r) * ld;
+                dprefetch_l2(row + (long)p * w2, (uint32_t)((long)n1 * w2 * sizeof(cplx)), polF);
+                if (n2 > 0) dprefetch_l2(row, (uint32_t)((long)n2 * w2 * sizeof(cplx)), polF);
+              }
+            } else {
+              for (int r = 0; r < w2; ++r)
+                dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
+            }
           }
 #endif
           const int st = f % NST;
@@ -1264,6 +1274,11 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       // ---- separator stage, phase-3 inputs
       c0 = pclk();
       pacc(19, c0 - cph1);
+      if (kProf && A.prof && tid == 0 && i < 64) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        A.prof[(long)gridDim.x * 24 + (long)blockIdx.x * 64 + i] = (long long)gt;   // phase-1 end, ns
+      }
       cbar();
       seg_separators(i);
       cbar();
