@@ -406,8 +406,8 @@ def north_star_kernels(cfg, names, peak):
     prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(cfg.c.ravel(), dtype=torch.float64, device=dev))
     dirs = dict(zip(names, hs.make_sweeps(prob, names, n_strips=cfg.n_strips, overlap=cfg.overlap)))
     # a batch of fewer directions leaves SMs free for more, shorter segments (P CTAs per
-    # direction): measured best P for C5 is 49 at t = 1, 41 at t = 2, 33 at t = 4
-    # (DESIGN.md §5); the t = 4 handles above use the automatic 33
+    # direction): measured best P for C5 is 49 at t = 1, 41 at t = 2, 36 at t = 4
+    # (DESIGN.md §5); the t = 4 handles above use the automatic 36
     seg_for_t = {1: 49, 2: 41}
     extra = {t_: dict(zip(names[:1] if t_ == 1 else ["LRL", "BTB"],
                           hs.make_sweeps(prob, ["LRL"] if t_ == 1 else ["LRL", "BTB"], n_strips=cfg.n_strips,

@@ -105,8 +105,8 @@ int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols, void* str
  *   gather     0 = "recent" (P:L93 literal rule), 1 = "core" ownership (A16)
  *   n_segments P >= 1 cross-row segments per strip for the partitioned
  *              (separator) strip solve; 0 = choose automatically (the
- *              largest P <= 33 whose segments have >= 8 cross rows;
- *              DESIGN.md §5)
+ *              largest P <= 36 whose segments have >= 8 cross rows: four
+ *              directions of 36 segment CTAs fill a B200)
  * Each strip's local block-tridiagonal matrix is factored once on the device
  * (block-Thomas per segment plus the separator Schur complement).
  * Errors: HELM_EINVAL, HELM_ESINGULAR, HELM_ENOMEM, HELM_ECUDA.  Synchronous. */

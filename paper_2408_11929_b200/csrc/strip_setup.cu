@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
 #endif
 static int choose_segments(int nc, int requested) {
   if (requested > 0) return requested;
-  int P = 33;
+  int P = 36;   // t = 4 batches: 144 segment CTAs on 148 SMs (C5 t = 4 apply: P = 33 3.83, 36 3.75, 37 3.81 ms)
   while (P > 1 && (nc - (P - 1)) / P < 8) --P;
   return P;
 }

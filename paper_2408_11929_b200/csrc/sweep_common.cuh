@@ -22,8 +22,7 @@ struct DirArgs {
   const cplx* R;         // source column
   cplx* Z;               // output column
   cplx *yb, *xs, *xb, *corr_prev, *corr_next;
-  cplx* xc;              // two-chain kernel: separator-inverse partial products [2][K][K/2+1][wmax]
-  unsigned* cnt;         // [0] segment arrivals, [1] reducer releases (two-chain: [2] partial products)
+  unsigned* cnt;         // [0] segment arrivals, [1] reducer releases
   unsigned* flag;        // fast kernel: per-separator publication flags (solve index + 1)
   const cplx* xinv;      // explicit separator-inverse rows (fast kernel), NULL if absent
   const float2* xinv32;  // their complex64 copy (inexact separator solve, two-chain kernel), NULL if off

@@ -64,9 +64,6 @@
 #ifndef HELM_DUAL_XTU
 #define HELM_DUAL_XTU 4     // rows in flight per lane in the transposed X part (XSYM)
 #endif
-#ifndef HELM_DUAL_XBAL
-#define HELM_DUAL_XBAL 0    // 1: balanced symmetric separator solve (each block of R^{-1} read once, see xbal_* below; measured slower)
-#endif
 #ifndef HELM_DUAL_ONELOOP
 #define HELM_DUAL_ONELOOP 1   // 1: one copy of the solve loop (the chain phases dispatch on the group): half the code
 #endif
@@ -89,12 +86,6 @@
 #endif
 #ifndef HELM_DUAL_EPIREL
 #define HELM_DUAL_EPIREL 1    // 1: the epilogue counter is released by chain B's producer lane (not thread 0 before a barrier)
-#endif
-#ifndef HELM_DUAL_XBAL_PF
-#define HELM_DUAL_XBAL_PF 1   // balanced stage: L2 prefetch of the CTA's blocks (0 none, 1 normal priority, 2 evict_first)
-#endif
-#ifndef HELM_DUAL_XBAL_LDA
-#define HELM_DUAL_XBAL_LDA 0  // balanced stage, pass A loads: 0 ld.cg, 1 evict_first hint, 2 evict_last hint
 #endif
 #ifndef HELM_DUAL_RHS_TMA
 #define HELM_DUAL_RHS_TMA 0   // stage the next RHS by bulk copies (1) or per-element cp.async (0)
@@ -137,7 +128,6 @@ struct DualArgs {
   int pmax;
   int stage_elems;  // cplx per ring stage (>= largest packed block + 1 zero entry)
   int mmax;         // largest segment (rows)
-  int xbw_off;      // cplx offset from the vector areas of the balanced separator solve's workspace
   long long* prof;  // optional per-CTA counters (24 per CTA)
 };
 
@@ -197,25 +187,11 @@ __device__ __forceinline__ void chain_row(int g, int e, int m, int lo, int hi, i
   high = up ? 0 : 1;                       // lo -> hi steps need o[r-1]: low mapping
 }
 
-// Balanced symmetric separator solve (HELM_DUAL_XBAL).  X = R^{-1} is complex
-// symmetric (strip_setup.cu forms its lower blocks by mirroring), so
-//   x_q = sum_k X[q][k] g_k = sum_{k} X[q][k] g_k  with  X[q][k] = X[k][q]^T.
-// Every unordered block pair {p, k} is read by ONE segment CTA: CTA p reads the
-// blocks (p, (p + d) mod K), d = 0 .. xbal_last(p, K) -- half of the K^2 blocks,
-// spread evenly -- and from each forms the normal product X[p][k] g_k (summed
-// into its own separator) and, for d > 0, the transposed product X[p][k]^T g_p,
-// the contribution of this block to separator k.  After a counter barrier every
-// CTA sums its own separator (and its lower neighbour's) from the published
-// partial products in a fixed order.  HBM and L2 bytes of the stage are halved
-// and the neighbour exchange of x_{p-1} disappears.
-__host__ __device__ __forceinline__ int xbal_last(int p, int K) {
-  if (K & 1) return (K - 1) / 2;
-  return p < K / 2 ? K / 2 : K / 2 - 1;
-}
-
-// GSEP: the separator RHS g has its own shared-memory area (more separators
-// than segment rows, e.g. C2 with 32 segments); else it aliases xa.  A template
-// parameter, not a runtime choice: the kernel is at its register cap.
+// GSEP: the separator RHS g (K w entries) has its own shared-memory area when it
+// is longer than two segment vector areas (e.g. C2 with 28 segments of 8 rows);
+// else it spans xa and the adjacent fb, which are free from the epilogue of the
+// previous solve to phase 3 of this one.  A template parameter, not a runtime
+// choice: the kernel is at its register cap.
 template <bool GSEP, bool XF32>
 __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_constant__ DualArgs A) {
   using namespace dualk;
@@ -255,7 +231,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* bne = bcr + A.vec_elems;
   cplx* xpart = bne + A.vec_elems + (2 + kTcW) * A.mmax;   // [consumer warps][WM] partial sums of the transposed X part
   cplx* gsm_own = xpart + kXpartElems;              // GSEP: after cs / cps / tcs / xpart
-  cplx* gsm = GSEP ? gsm_own : xa;                  // separator RHS g (K x w), xa is dead before phase 3
+  cplx* gsm = GSEP ? gsm_own : xa;                  // separator RHS g (K x w): xa (+ fb), dead before phase 3
   cplx* cs = bne + A.vec_elems;                     // [mmax] corrections formed by the last epilogue (next RHS)
   cplx* cps = cs + A.mmax;                          // [mmax] forward-pass corr_prev rows (backward RHS), staged
   cplx* tcs = cps + A.mmax;                         // [kTcW mmax] transmission coefficients of the next epilogue, staged
@@ -316,18 +292,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
             // this solve's separator-inverse rows into L2 while phase 1 still runs
             const int w2 = tab[i2].w;
             const long ld = x_ld(K, w2);
-            if (HELM_DUAL_XBAL) {
-              const int last = xbal_last(p, K);
-              const int n1 = std::min(last + 1, K - p), n2 = last + 1 - n1;
-              for (int r = 0; r < w2; ++r) {
-                const cplx* row = tab[i2].xinv + ((long)p * w2 + r) * ld;
-                dprefetch_l2(row + (long)p * w2, (uint32_t)((long)n1 * w2 * sizeof(cplx)), polF);
-                if (n2 > 0) dprefetch_l2(row, (uint32_t)((long)n2 * w2 * sizeof(cplx)), polF);
-              }
-            } else {
-              for (int r = 0; r < w2; ++r)
-                dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
-            }
+            for (int r = 0; r < w2; ++r)
+              dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
           }
 #endif
           const int st = f % NST;
@@ -594,24 +560,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
         const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(float2));
         for (int r = tid; r < w; r += 32)
           dprefetch_l2(tab[i].xinv32 + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
-      } else if (HELM_DUAL_XBAL) {
-        // the blocks (p, p .. p + last) of block row p, wrapping around at K
-        const int last = xbal_last(p, K);
-        const int n1 = std::min(last + 1, K - p), n2 = last + 1 - n1;
-        for (int r = tid; r < w; r += 32) {
-          const cplx* row = tab[i].xinv + ((long)p * w + r) * ld;
-          // (normal eviction priority: pass B re-reads these blocks from L2)
-          if (HELM_DUAL_XBAL_PF == 1) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row + (long)p * w),
-                         "r"((uint32_t)((long)n1 * w * sizeof(cplx))) : "memory");
-            if (n2 > 0)
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((uint32_t)((long)n2 * w * sizeof(cplx)))
-                           : "memory");
-          } else if (HELM_DUAL_XBAL_PF == 2) {
-            dprefetch_l2(row + (long)p * w, (uint32_t)((long)n1 * w * sizeof(cplx)), pol_first);
-            if (n2 > 0) dprefetch_l2(row, (uint32_t)((long)n2 * w * sizeof(cplx)), pol_first);
-          }
-        }
       } else {
         const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(cplx));
         for (int r = tid; r < w; r += 32)
@@ -725,135 +673,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     pacc(14, cx0 - cg0);
     const long Kw = (long)K * w, xld = x_ld(K, w);
     const int cw = tid >> 5, ncw = ncons >> 5;
-    constexpr bool kBal = HELM_DUAL_XBAL && !XF32;
-    if constexpr (kBal) {
-      // ---- balanced symmetric separator solve (xbal_last above)
-      cplx* xq4 = vec0 + A.xbw_off;   // [4][2][WM] partial sums of the contributions
-      const int DC = K / 2 + 1;
-      cplx* xcb = D_.xc + (long)par * K * DC * D_.wmax;   // [K][DC][wmax]: slot 0 = normal sum, d = contribution
-      if (p < K) {
-        const int last = xbal_last(p, K);
-        const cplx* Xrow = tab[i].xinv + (long)p * w * xld;
-        const long long ca0 = pclk();
-        // pass A, normal products: rows r of block row p over the columns of its blocks
-        // (p, p .. p + last), wrapping at K -- 4 rows per warp, lanes over the columns,
-        // XCH loads per row in flight (long contiguous row segments from HBM)
-        {
-          constexpr int XCH = HELM_DUAL_XCH;
-          const long ncol = (long)(last + 1) * w, cbeg = (long)p * w;
-          for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
-            const cplx* Xr[4];
-            bool ok[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              ok[u] = rb + u < w;
-              Xr[u] = Xrow + (long)(ok[u] ? rb + u : 0) * xld;
-            }
-            cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-            for (long jj = lane; jj < ncol; jj += 32 * XCH) {
-              cplx xv[4][XCH], gv[XCH];
-#pragma unroll
-              for (int v = 0; v < XCH; ++v) {
-                const bool in = jj + 32 * v < ncol;
-                long col = cbeg + jj + 32 * v;
-                if (col >= Kw) col -= Kw;
-                gv[v] = in ? gsm[col] : cmk(0, 0);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  xv[u][v] = (ok[u] && in) ? (HELM_DUAL_XBAL_LDA == 0 ? ldcg(Xr[u] + col)
-                                              : ld_cg_hint(Xr[u] + col, HELM_DUAL_XBAL_LDA == 1 ? pol_first : pol_last))
-                                           : cmk(0, 0);
-              }
-#pragma unroll
-              for (int v = 0; v < XCH; ++v)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-#pragma unroll
-              for (int off = 16; off > 0; off >>= 1) {
-                acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
-                acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
-              }
-              if (lane == 0 && ok[u]) xcb[((long)p * DC) * D_.wmax + rb + u] = acc[u];
-            }
-          }
-        }
-        const long long cb0 = pclk();
-        pacc(15, cb0 - ca0);
-        // pass B, transposed products X[p][k]^T g_p of the off-diagonal blocks (d > 0),
-        // the block rows again (now from L2): lanes over the columns, rows in groups of
-        // 8; the tail columns 32 .. w-1 (w <= 36) by one load per group, lane l ->
-        // (row 8 gi + l / 4, column 32 + l % 4)
-        const cplx* gp_s = gsm + (long)p * w;
-        const int tc = 32 + (lane & 3), tr = lane >> 2;
-        for (int d = 1 + cw; d <= last; d += ncw) {
-          const int k = p + d < K ? p + d : p + d - K;
-          const cplx* B = Xrow + (long)k * w;
-          cplx t0 = cmk(0, 0), tt = cmk(0, 0);
-#pragma unroll 1
-          for (int r0 = 0; r0 < w; r0 += 8) {
-            cplx x0[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) x0[u] = (r0 + u < w && lane < w) ? ldcg(B + (long)(r0 + u) * xld + lane) : cmk(0, 0);
-            const cplx xt = (r0 + tr < w && tc < w) ? ldcg(B + (long)(r0 + tr) * xld + tc) : cmk(0, 0);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) cfma(t0, x0[u], r0 + u < w ? gp_s[r0 + u] : cmk(0, 0));
-            cfma(tt, xt, r0 + tr < w ? gp_s[r0 + tr] : cmk(0, 0));
-          }
-#pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {
-            tt.x += __shfl_xor_sync(0xffffffffu, tt.x, off);
-            tt.y += __shfl_xor_sync(0xffffffffu, tt.y, off);
-          }
-          cplx* dst = xcb + ((long)p * DC + d) * D_.wmax;
-          if (lane < w) dst[lane] = t0;
-          if (lane < 4 && tc < w) dst[tc] = tt;
-        }
-        if (!kProfStep) pacc(11, pclk() - cb0);
-      }
-      cbar();
-      const long long cw1 = pclk();
-      if (tid == 0) {
-        if (p < K) {
-          HELM_DUAL_FENCE();
-          red_release_add(&D_.cnt[2], 1u);
-        }
-        while (ld_relaxed(&D_.cnt[2]) < (unsigned)(K * (i + 1))) __nanosleep(20);
-        (void)ld_acquire(&D_.cnt[2]);
-      }
-      cbar();
-      pacc(4, pclk() - cw1);
-      pacc(13, pclk() - cw1);
-      // x_q = n_q + sum_d c[q - d][d] for q = p (x_p) and q = p - 1 (x_{p-1}); the
-      // contributions in four interleaved parts, combined in a fixed order
-      for (int e = tid; e < 8 * w; e += ncons) {
-        const int part = e / (2 * w), rem = e - part * 2 * w, which = rem / w, r = rem - which * w;
-        const int q = p - which;
-        cplx acc = cmk(0, 0);
-        if (q >= 0 && q < K)
-          for (int d = 1 + part; d <= K / 2; d += 4) {
-            const int src = q - d >= 0 ? q - d : q - d + K;
-            if (d <= xbal_last(src, K)) acc = cadd(acc, ldcg(xcb + ((long)src * DC + d) * D_.wmax + r));
-          }
-        xq4[(part * 2 + which) * WM + r] = acc;
-      }
-      cbar();
-      for (int e = tid; e < 2 * WM; e += ncons) {
-        const int which = e / WM, r = e - which * WM, q = p - which;
-        cplx v = cmk(0, 0);
-        if (r < w && q >= 0 && q < K) {
-          v = ldcg(xcb + ((long)q * DC) * D_.wmax + r);
-          for (int part = 0; part < 4; ++part) v = cadd(v, xq4[(part * 2 + which) * WM + r]);
-        }
-        (which ? xlo : xhi)[r] = v;
-      }
-      cbar();
-      pacc(2, pclk() - cx0);
-      if (p < K)
-        for (int e = tid; e < w; e += ncons) D_.xs[par * xss + (long)p * D_.wmax + e] = xhi[e];
-    } else {
 #ifdef HELM_DUAL_ABL_NOXMV
     if (false) {
 #else
@@ -1001,7 +820,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       pacc(13, pclk() - cw1);
       for (int e = tid; e < w; e += ncons) xlo[e] = ldcg(D_.xs + par * xss + (long)(p - 1) * D_.wmax + e);
       cbar();
-    }
     }
     const long long cvi = pclk();
     // phase-3 inputs: chain A  U_hi x_p;  chain B  -U_{lo-1}^T x_{p-1}
@@ -1234,7 +1052,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (!kProfStep) pacc(10, cpb - c0);
       mbar_wait(&sbar[1], i & 1);
       cbar();
-      if (!HELM_DUAL_XBAL) pacc(15, pclk() - cpb);   // couplings landed
+      pacc(15, pclk() - cpb);   // couplings landed
       seg_rhs(i);
 #if HELM_DUAL_GSRC
       {
@@ -1369,13 +1187,10 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   const long stage_elems = pk_size(wmax) + 8;   // padded packed block + a zero entry, 128-byte multiple
   size_t smem = sizeof(cplx) * 2 * NST * stage_elems + sizeof(uint64_t) * (4 * NST + 4) +
                 sizeof(cplx) * (7 * WM + 2 * pmax) + sizeof(DualTab) * nsolve_max + sizeof(int) * (WM + pmax) + 256;
-  const bool gsep = gsm_elems > vec_elems;
-  // balanced separator solve workspace (18 WM): the chain-B phase-3 area when it is
-  // large enough (free during the separator stage), else its own area at the end
-  const long xbw_elems = 18L * WM;
-  const long tail = 6 * vec_elems + (2L + kTcW) * mmax_all + kXpartElems + (gsep ? gsm_elems : 0);
-  const long xbw_off = vec_elems >= xbw_elems ? 3 * vec_elems : tail;
-  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (tail + (vec_elems >= xbw_elems ? 0 : xbw_elems));
+  // g aliases xa and, when it is longer, the adjacent fb (both are free from the
+  // epilogue to the end of the separator stage); its own area only beyond that
+  const bool gsep = gsm_elems > 2 * vec_elems;
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + (2L + kTcW) * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
   // inexact separator solve only when every direction of the batch asked for it
   bool xf32 = true;
   for (int d = 0; d < t; ++d) xf32 = xf32 && dirs[d]->sep_fp32 && dirs[d]->d_xinv32;
@@ -1389,7 +1204,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   size_t ncnt = 0;
   for (int d = 0; d < t; ++d) {
     coff[d] = ncnt;
-    ncnt += 3 + dirs[d]->P;
+    ncnt += 2 + dirs[d]->P;
   }
   size_t total = al(sizeof(unsigned) * ncnt);
   for (int d = 0; d < t; ++d) {
@@ -1399,7 +1214,6 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     total += al(sizeof(cplx) * 2L * h->P * h->wmax);
     total += al(sizeof(cplx) * (long)h->N * h->nc);
     total += al(sizeof(cplx) * (long)h->nc);
-    total += al(sizeof(cplx) * 2L * (h->P - 1) * ((h->P - 1) / 2 + 1) * h->wmax);
   }
   unsigned char* scratch = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&scratch, total, st);
@@ -1417,7 +1231,6 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   A.pmax = pmax;
   A.stage_elems = (int)stage_elems;
   A.mmax = mmax_all;
-  A.xbw_off = (int)xbw_off;
   A.prof = helm_sweep_prof_buffer();
   int base = 0;
   for (int d = 0; d < t; ++d) {
@@ -1434,13 +1247,12 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];
-    D.cnt = reinterpret_cast<unsigned*>(scratch) + coff[d]; D.flag = D.cnt + 3;
+    D.cnt = reinterpret_cast<unsigned*>(scratch) + coff[d]; D.flag = D.cnt + 2;
     D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
     D.corr_prev = (cplx*)q; q += al(sizeof(cplx) * (long)h->N * h->nc);
-    D.corr_next = (cplx*)q; q += al(sizeof(cplx) * (long)h->nc);
-    D.xc = (cplx*)q;
+    D.corr_next = (cplx*)q;
     D.wmax = h->wmax;
     D.cta_base = base;
     base += h->P;

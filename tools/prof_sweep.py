@@ -48,13 +48,27 @@ if os.environ.get("HELM_CYCLES"):
     L = hs.load()
     ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)  # upper bound
     stride = 24 if hs.sweep_kernel_name() == "k_sweep_dual" else 8
-    buf = torch.zeros(ctas * stride, dtype=torch.int64, device=dev)
+    if stride == 24:
+        ctas = sum(i.n_segments for i in info)   # the two-chain kernel: P CTAs per direction
+    buf = torch.zeros(ctas * stride + (ctas * 64 if stride == 24 else 0), dtype=torch.int64, device=dev)
     L.helm_sweep_profile.argtypes = [ctypes.c_void_p]
     L.helm_sweep_profile(ctypes.c_void_p(buf.data_ptr()))
     hs.sweep_apply(dirs, r, Z, ldr=0)
     torch.cuda.synchronize()
     L.helm_sweep_profile(ctypes.c_void_p(0))
-    b = buf.view(ctas, stride).cpu().numpy()
+    b = buf[:ctas * stride].view(ctas, stride).cpu().numpy()
+    if stride == 24 and os.environ.get("HELM_SKEW"):
+        import numpy as np
+        gt = buf[ctas * stride:].view(ctas, 64).cpu().numpy().astype(np.float64)
+        P = info[0].n_segments
+        ns = 63
+        for d in range(len(info)):
+            g = gt[d * P:(d + 1) * P, :ns]
+            late = g - g.min(axis=0, keepdims=True)       # ns behind the first CTA of the direction
+            print(f"  dir {d}: phase-1 end skew per solve (ns): mean max {late.max(axis=0).mean():.0f}, "
+                  f"mean {late.mean():.0f}; latest CTA counts: " +
+                  " ".join(f"{p}:{c}" for p, c in sorted(((p, int((late.argmax(axis=0) == p).sum())) for p in range(P)), key=lambda x: -x[1])[:6]))
+            print(f"    mean lateness by segment (ns): " + " ".join(f"{v:.0f}" for v in late.mean(axis=1)))
     if stride == 24:
         sel = b[b[:, 3] > 0]
         tp = sel[:, 8:12].mean(axis=0) / sel[:, 3].mean()
