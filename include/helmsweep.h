@@ -105,7 +105,8 @@ int helm_spmv(helm_problem_t p, const double* X, double* Y, int ncols, void* str
  *   gather     0 = "recent" (P:L93 literal rule), 1 = "core" ownership (A16)
  *   n_segments P >= 1 cross-row segments per strip for the partitioned
  *              (separator) strip solve; 0 = choose automatically (the
- *              largest P <= 36 whose segments have >= 8 cross rows: four
+ *              largest P <= 36 (<= 33 for strips wider than 36 nodes) whose
+ *              segments have >= 8 cross rows: four
  *              directions of 36 segment CTAs fill a B200)
  * Each strip's local block-tridiagonal matrix is factored once on the device
  * (block-Thomas per segment plus the separator Schur complement).
@@ -232,6 +233,8 @@ const char* helm_sweep_kernel_name(void);
  *   "setup_timing"     1: sweep_setup prints its phase times to stderr
  *   "orth_prof"        1: k_orth prints phase clock stamps to stderr
  *   "setup_chunks"     n > 1: sweep_setup pipelines its strips in n chunks on forked streams (0 / 1: one pass)
+ *   "sep_two_level"    1: sweep_setup also builds two-level separator panels (fine groups +
+ *                      coarse Schur system, >= 8 separators) and k_sweep_dual uses them
  * Every knob selects a different, parity-tested kernel or schedule for the same
  * arithmetic.  Not synchronised with calls running on other host threads.
  * Errors: HELM_EINVAL (unknown name or value). */

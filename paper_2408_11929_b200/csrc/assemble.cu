@@ -26,7 +26,7 @@ int helm_knob(int id) { return (id >= 0 && id < KNOB_COUNT) ? g_knobs[id].load()
 
 extern "C" int helm_set_knob(const char* name, int value) {
   static const char* names[KNOB_COUNT] = {"sweep_kernel", "general_reducer", "no_wide_xinv", "factor_generic",
-                                          "orth_unfused", "setup_timing", "orth_prof", "setup_chunks"};
+                                          "orth_unfused", "setup_timing", "orth_prof", "setup_chunks", "sep_two_level"};
   if (!name) return HELM_EINVAL;
   for (int k = 0; k < KNOB_COUNT; ++k)
     if (strcmp(name, names[k]) == 0) {

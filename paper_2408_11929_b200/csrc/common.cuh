@@ -15,8 +15,19 @@ typedef double2 cplx;
 __host__ __device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
 __host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
 __host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }
+// Products with an explicit FMA contraction (the compiler otherwise picks which of
+// the two products it fuses per call site, and that choice -- a last-bit
+// difference -- moved with unrelated code changes; C4's wide strips amplify it to
+// ~1e-10 against the oracle).  h_mul: an uncontracted product.
+__host__ __device__ __forceinline__ double h_mul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
 __host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
-  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return cmk(fma(a.x, b.x, -h_mul(a.y, b.y)), fma(a.x, b.y, h_mul(a.y, b.x)));
 }
 __host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cmk(a.x * s, a.y * s); }
 __host__ __device__ __forceinline__ cplx cconj(cplx a) { return cmk(a.x, -a.y); }
@@ -34,7 +45,7 @@ __host__ __device__ __forceinline__ void cfmaconj(cplx& acc, cplx a, cplx b) {
   acc.y = fma(a.x, b.y, acc.y);
   acc.y = fma(-a.y, b.x, acc.y);
 }
-__host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+__host__ __device__ __forceinline__ double cabs2(cplx a) { return fma(a.x, a.x, h_mul(a.y, a.y)); }
 __host__ __device__ __forceinline__ cplx cinv(cplx a) {
   double d = 1.0 / cabs2(a);
   return cmk(a.x * d, -a.y * d);
@@ -52,6 +63,7 @@ enum HelmKnob {
   KNOB_SETUP_TIMING,        // 1: sweep_setup prints its phase times to stderr
   KNOB_ORTH_PROF,           // 1: k_orth phase clock stamps to stderr
   KNOB_SETUP_CHUNKS,        // 0 auto, n: sweep_setup pipelines its strips in n chunks (1 = one pass)
+  KNOB_SEP_TWO_LEVEL,       // 1: sweep_setup builds the two-level separator panels and k_sweep_dual uses them
   KNOB_COUNT
 };
 int helm_knob(int id);
@@ -192,6 +204,14 @@ struct helm_sweep_s {
   cplx* d_facp = nullptr;
   cplx* d_fac2 = nullptr;
   std::vector<long> pfac_off; long* d_pfac_off = nullptr;
+  // two-level separator solve (k_sweep_dual): per strip s, separator
+  // k, two row panels (w rows of ld1, then w rows of ld2 complex) at
+  // sep2_off[s] + k * w_s * (ld1 + ld2); the plan (group / coarse structure) is
+  // the same for every strip.  NULL unless the sep_two_level knob is set (and K >= 8, w <= 36).
+  cplx* d_sep2 = nullptr;
+  std::vector<long> sep2_off; long* d_sep2_off = nullptr;
+  int* d_sep2_plan = nullptr;
+  int sep2_M = 0, sep2_ld1 = 0, sep2_ld2 = 0;
   // the band/factor arrays above are shared by every handle with the same
   // (problem, axis, N, overlap, P) -- e.g. LRL and RLR -- through this record
   struct SharedFactors* shared = nullptr;

@@ -37,6 +37,9 @@ struct SharedFactors {
   long factor_bytes;
   float2* xinv32 = nullptr;   // complex64 separator-inverse rows, made on the first sweep_set_precision(32)
   long xinv_elems = 0;
+  cplx* sep2 = nullptr;       // two-level separator panels
+  int* sep2_plan = nullptr;
+  int sep2_M = 0, sep2_ld1 = 0, sep2_ld2 = 0;
 };
 static std::vector<SharedFactors*> g_shared;
 static std::mutex g_shared_mu;   // setups of different axes may run on concurrent host threads
@@ -680,6 +683,7 @@ struct RedArgs {
   cplx* rscratch;  // per strip: 2 w^2 (R_{k,k+1} of the previous separator, temp)
   int* status;
   int s0;          // first strip of this launch
+  cplx* rraw = nullptr;   // two-level separator solve: the raw blocks R_kk, R_{k,k+1} per separator (stride 2 wmax^2)
 };
 
 // One CTA (96 threads) per strip walks the K = P-1 separators in order (the
@@ -694,6 +698,9 @@ static constexpr int kRedThreads = 384;
 #define HELM_RED_LPR 9      // threads per block row of k_reduced's Gauss-Jordan (kRowW * LPR <= 384)
 #endif
 static constexpr int kRedLPR = HELM_RED_LPR;
+#ifndef HELM_RED_OLDGJ
+#define HELM_RED_OLDGJ 0    // 1: k_reduced uses row_invert (2 threads per row, normalised pivot-row broadcast)
+#endif
 __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   __shared__ RowSmem sm;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -754,11 +761,25 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     build_D(S, ra.dg + band + (long)sk * ra.wmax, ra.al + band + (long)sk * ra.wmax, w);
     blk_lxr(S, Bh, Ub(0, BD_UT), Ub(0, BD_U), w, -1.0, true);
     blk_lxr(S, Bl, Ub(1, BD_U), Ub(1, BD_UT), w, -1.0, true);
+    if (ra.rraw) {
+      cplx* d = ra.rraw + ((long)s * (P - 1) + k) * 2 * ra.wmax * ra.wmax;
+      for (int e = threadIdx.x; e < w * w; e += blockDim.x) d[e] = S[e];   // R_kk
+      __syncthreads();
+    }
     // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
     if (k >= 1) blk_mm_tiled2(S, w, T1, w, true, T2, w, w, -1.0, true);
     long long c1 = pr ? clock64() : 0;
     if (pr) g_red_prof[0] += c1 - c0;
-    // Rinv_k (register-row Gauss-Jordan, kRedLPR threads per row; result in sm.mat, row stride kRowW)
+    // Rinv_k (register-row Gauss-Jordan; result in sm.mat, row stride kRowW)
+#if HELM_RED_OLDGJ
+    cplx a[kRowHW];
+#pragma unroll
+    for (int jj = 0; jj < kRowHW; ++jj) {
+      const int col = kLPR * jj + h;
+      a[jj] = (i < w && col < w) ? S[i * w + col] : cmk(0, 0);
+    }
+    if (row_invert(a, w, sm)) {
+#else
     cplx a[kRowW / kRedLPR];
     {
       const int ir = threadIdx.x / kRedLPR, hr = threadIdx.x % kRedLPR;
@@ -769,6 +790,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
       }
     }
     if (row_invert_g<kRedLPR>(a, w, sm)) {
+#endif
       if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
       return;
     }
@@ -788,11 +810,337 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     if (k <= P - 3) {
       // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1};  F_k = Rinv_k R_{k,k+1}
       blk_lxr(T1, Bx, Ub(1, BD_U), Ub(2, BD_U), w, -1.0, false);
+      if (ra.rraw) {
+        cplx* d = ra.rraw + (((long)s * (P - 1) + k) * 2 + 1) * ra.wmax * ra.wmax;
+        for (int e = threadIdx.x; e < w * w; e += blockDim.x) d[e] = T1[e];   // R_{k,k+1}
+      }
       blk_mm_tiled2(T2, w, sm.mat, kRowW, false, T1, w, w, 1.0, false);
       for (int e = threadIdx.x; e < w * w; e += blockDim.x) F[e] = T2[e];
     }
     __syncthreads();
     if (pr) g_red_prof[2] += clock64() - c2;
+  }
+}
+
+// ------------------------------------------------------------------ two-level separator solve (setup)
+// DESIGN.md §5 "Two-level separator solve".  The K separators of a strip are
+// split into M coarse separators and M + 1 groups of fine ones between them
+// (sep2_plan).  With R block tridiagonal (diagonal R_kk, couplings E_k = R_{k,k+1},
+// R_{k+1,k} = E_k^T), Y^g = (R restricted to group g)^{-1} and, for a fine
+// separator p of group g with coarse neighbours c_l = first - 1, c_r = last + 1,
+//   x_p = (Y^g g_g)_p - V_p x_{c_l} - W_p x_{c_r},   V_p = Y^g_{p,first} E_{c_l}^T,
+//                                                    W_p = Y^g_{p,last} E_last;
+// the coarse values solve the block-tridiagonal Schur system
+//   Rh x_C = gh,  gh_c = g_c - sum_j H_{c,j} g_j,
+//   H_{c,j} = E_{c-1}^T Y^{left}_{last,j} (j in the left group), E_c Y^{right}_{first,j} (right group),
+//   Rh_cc = R_cc - E_{c-1}^T Y^{left}_{last,last} E_{c-1} - E_c Y^{right}_{first,first} E_c^T,
+//   Rh_{c,c'} = -E_c Y^{g}_{first,last} E_last   (c' the next coarse, g the group between).
+// Every separator gets two row panels: panel 1 (its group's Y row, or for a
+// coarse one [H left | H right]) and panel 2 (Q_p = V_p Xc_{c_l,.} + W_p Xc_{c_r,.}
+// for a fine p, the row of Xc = Rh^{-1} for a coarse one), so that the apply
+// forms x_p from ~K / sqrt(K) blocks instead of the K blocks of a row of R^{-1}.
+static constexpr int kSep2MaxB = 8;                        // blocks per group (panel 1 of a coarse: <= 2 groups)
+static constexpr int kSep2PlanHdr = 64;                    // ints: [0] M, [1] groups, [2] nb1 max, [8..] gstart, [32..] glen
+static constexpr int kSep2PlanStride = 4 + 2 * kSep2MaxB;  // ints per separator: kind, n1, group / coarse index, -, idx1[]
+
+struct Sep2Args {
+  const int* w;
+  int wmax, P, s0;
+  const cplx* rraw;      // [s][k][2][wmax^2]: R_kk, E_k
+  const int* plan;       // sep2 plan (device)
+  cplx* ytmp;            // per (s, group): Li[B], Ri[B], Y[B^2] blocks of wmax^2
+  long ytmp_stride;      // cplx per (s, group)
+  cplx* vw;              // per (s, k): V_k, W_k
+  cplx* cd;              // per (s, coarse j): [0] left diagonal term, [1] right diagonal term, [2] Rh_{j,j+1}
+  cplx* xc;              // per s: Xc (M^2 blocks) and its temporaries (2M)
+  cplx* sep2;            // panels
+  const long* sep2_off;
+  int ld1, ld2;
+  int* status;
+};
+
+// C (+)= alpha op(A) op(B) on w x w blocks in shared memory (row stride w), 2 x 2 tiles
+__device__ inline void s2_mm(cplx* C, const cplx* A, bool ta, const cplx* B, bool tb, int w, double alpha, bool acc) {
+  const int nt = (w + 1) / 2;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+    const int i0 = (t / nt) * 2, j0 = (t % nt) * 2;
+    cplx c[2][2] = {{cmk(0, 0), cmk(0, 0)}, {cmk(0, 0), cmk(0, 0)}};
+    for (int r = 0; r < w; ++r) {
+      cplx av[2], bv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = i0 + u, j = j0 + u;
+        av[u] = i < w ? (ta ? A[r * w + i] : A[i * w + r]) : cmk(0, 0);
+        bv[u] = j < w ? (tb ? B[j * w + r] : B[r * w + j]) : cmk(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) cfma(c[u][v], av[u], bv[v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = i0 + u, j = j0 + v;
+        if (i < w && j < w) C[i * w + j] = acc ? cadd(C[i * w + j], cscale(c[u][v], alpha)) : cscale(c[u][v], alpha);
+      }
+  }
+  __syncthreads();
+}
+__device__ inline void s2_ld(cplx* d, const cplx* g, int w) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) d[e] = __ldcg(g + e);
+  __syncthreads();
+}
+__device__ inline void s2_st(cplx* g, const cplx* d, int w, bool trans = false) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int r = e / w, c = e - r * w;
+    g[e] = trans ? d[c * w + r] : d[e];
+  }
+  __syncthreads();
+}
+// dst (global, row stride w) = S^{-1}; S in shared memory (row stride w)
+__device__ inline int s2_inv(cplx* dst, const cplx* S, int w, RowSmem& sm) {
+  cplx a[kRowW / kRedLPR];
+  {
+    const int ir = threadIdx.x / kRedLPR, hr = threadIdx.x % kRedLPR;
+#pragma unroll
+    for (int jj = 0; jj < kRowW / kRedLPR; ++jj) {
+      const int col = kRedLPR * jj + hr;
+      a[jj] = (ir < w && col < w) ? S[ir * w + col] : cmk(0, 0);
+    }
+  }
+  if (row_invert_g<kRedLPR>(a, w, sm)) return 1;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int r = e / w, c = e - r * w;
+    dst[e] = sm.mat[r * kRowW + c];
+  }
+  __syncthreads();
+  return 0;
+}
+
+// Explicit inverse Y (nb x nb blocks, Y + (i nb + j) ws) of the block-tridiagonal
+// matrix with diagonal blocks D(j) and couplings E(j) = block (j, j+1), block
+// (j+1, j) = E(j)^T:  forward Schur complements L_j = D_j - E_{j-1}^T L_{j-1}^{-1} E_{j-1},
+// backward ones R_j = D_j - E_j R_{j+1}^{-1} E_j^T, diagonal blocks
+// Y_jj = (D_j - E_{j-1}^T L_{j-1}^{-1} E_{j-1} - E_j R_{j+1}^{-1} E_j^T)^{-1},
+// off-diagonal Y_ij = -L_i^{-1} E_i Y_{i+1,j} (i < j), Y_ji = Y_ij^T.
+// Li, Ri: nb blocks each (global scratch).  sA..sD: four w x w shared blocks.
+template <class DF, class EF>
+__device__ int s2_bt_inverse(int nb, int w, long ws, DF D, EF E, cplx* Li, cplx* Ri, cplx* Y, cplx* sA, cplx* sB,
+                             cplx* sC, cplx* sS, RowSmem& sm) {
+  // forward
+  s2_ld(sS, D(0), w);
+  if (s2_inv(Li, sS, w, sm)) return 1;
+  for (int j = 1; j < nb; ++j) {
+    s2_ld(sA, E(j - 1), w);
+    s2_ld(sB, Li + (j - 1) * ws, w);
+    s2_mm(sC, sB, false, sA, false, w, 1.0, false);      // L^{-1} E
+    s2_ld(sS, D(j), w);
+    s2_mm(sS, sA, true, sC, false, w, -1.0, true);       // - E^T L^{-1} E
+    if (s2_inv(Li + j * ws, sS, w, sm)) return 1;
+  }
+  // backward
+  s2_ld(sS, D(nb - 1), w);
+  if (s2_inv(Ri + (nb - 1) * ws, sS, w, sm)) return 1;
+  for (int j = nb - 2; j >= 1; --j) {
+    s2_ld(sA, E(j), w);
+    s2_ld(sB, Ri + (j + 1) * ws, w);
+    s2_mm(sC, sB, false, sA, true, w, 1.0, false);       // R^{-1} E^T
+    s2_ld(sS, D(j), w);
+    s2_mm(sS, sA, false, sC, false, w, -1.0, true);      // - E R^{-1} E^T
+    if (s2_inv(Ri + j * ws, sS, w, sm)) return 1;
+  }
+  // diagonal blocks
+  for (int j = 0; j < nb; ++j) {
+    s2_ld(sS, D(j), w);
+    if (j >= 1) {
+      s2_ld(sA, E(j - 1), w);
+      s2_ld(sB, Li + (j - 1) * ws, w);
+      s2_mm(sC, sB, false, sA, false, w, 1.0, false);
+      s2_mm(sS, sA, true, sC, false, w, -1.0, true);
+    }
+    if (j + 1 < nb) {
+      s2_ld(sA, E(j), w);
+      s2_ld(sB, Ri + (j + 1) * ws, w);
+      s2_mm(sC, sB, false, sA, true, w, 1.0, false);
+      s2_mm(sS, sA, false, sC, false, w, -1.0, true);
+    }
+    if (s2_inv(Y + (j * nb + j) * ws, sS, w, sm)) return 1;
+  }
+  // off-diagonal blocks, column by column upwards from the diagonal
+  for (int j = 1; j < nb; ++j) {
+    s2_ld(sS, Y + (j * nb + j) * ws, w);                   // Y_{i+1, j}
+    for (int i = j - 1; i >= 0; --i) {
+      s2_ld(sA, E(i), w);
+      s2_mm(sC, sA, false, sS, false, w, 1.0, false);      // E_i Y_{i+1,j}
+      s2_ld(sB, Li + i * ws, w);
+      s2_mm(sS, sB, false, sC, false, w, -1.0, false);     // Y_ij = -L_i^{-1} E_i Y_{i+1,j}
+      s2_st(Y + (i * nb + j) * ws, sS, w);
+      s2_st(Y + (j * nb + i) * ws, sS, w, true);
+    }
+  }
+  return 0;
+}
+
+__device__ __forceinline__ cplx* s2_panel1(const Sep2Args& a, int s, int k, int w) {
+  return a.sep2 + a.sep2_off[s] + (long)k * w * (a.ld1 + a.ld2);
+}
+__device__ __forceinline__ cplx* s2_panel2(const Sep2Args& a, int s, int k, int w) {
+  return s2_panel1(a, s, k, w) + (long)w * a.ld1;
+}
+// block (rows of) a w x w smem block into panel columns [col0, col0 + w)
+__device__ inline void s2_put(cplx* panel, int ld, int col0, const cplx* blk, int w) {
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int r = e / w, c = e - r * w;
+    panel[(long)r * ld + col0 + c] = blk[e];
+  }
+  __syncthreads();
+}
+
+// One CTA per (group, strip): Y^g, the fine separators' panel 1 and V / W, the
+// adjacent coarse separators' H parts and their Schur-system terms.
+static constexpr int kSep2Threads = 384;
+__global__ void __launch_bounds__(kSep2Threads) k_sep2_group(Sep2Args a) {
+  __shared__ RowSmem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.y + a.s0, g = blockIdx.x;
+  const int w = a.w[s], K = a.P - 1, M = a.plan[0];
+  const long ws = (long)a.wmax * a.wmax;
+  const int first = a.plan[8 + g], nb = a.plan[32 + g], last = first + nb - 1;
+  cplx* sA = reinterpret_cast<cplx*>(smem_raw);
+  cplx *sB = sA + ws, *sC = sB + ws, *sS = sC + ws, *sT = sS + ws;
+  const cplx* rr = a.rraw + (long)s * K * 2 * ws;
+  auto D = [&](int j) { return rr + (long)(first + j) * 2 * ws; };
+  auto E = [&](int j) { return rr + ((long)(first + j) * 2 + 1) * ws; };
+  cplx* Li = a.ytmp + ((long)s * (M + 1) + g) * a.ytmp_stride;
+  cplx* Ri = Li + kSep2MaxB * ws;
+  cplx* Y = Ri + kSep2MaxB * ws;
+  if (s2_bt_inverse(nb, w, ws, D, E, Li, Ri, Y, sA, sB, sC, sS, sm)) {
+    if (threadIdx.x == 0) atomicCAS(a.status, 0, -(s * 1024 + first + 1));
+    return;
+  }
+  const bool hasl = g > 0, hasr = g < M;
+  const int cl = first - 1, cr = last + 1;
+  for (int l = 0; l < nb; ++l) {
+    const int p = first + l;
+    cplx* p1 = s2_panel1(a, s, p, w);
+    for (int j = 0; j < nb; ++j) {
+      s2_ld(sS, Y + (l * nb + j) * ws, w);
+      s2_put(p1, a.ld1, j * w, sS, w);
+    }
+    cplx* v = a.vw + ((long)s * K + p) * 2 * ws;
+    if (hasl) {   // V_p = Y_{l,0} E_{cl}^T
+      s2_ld(sS, Y + (l * nb) * ws, w);
+      s2_ld(sA, rr + ((long)cl * 2 + 1) * ws, w);
+      s2_mm(sC, sS, false, sA, true, w, 1.0, false);
+      s2_st(v, sC, w);
+    }
+    if (hasr) {   // W_p = Y_{l,nb-1} E_last
+      s2_ld(sS, Y + (l * nb + nb - 1) * ws, w);
+      s2_ld(sA, E(nb - 1), w);
+      s2_mm(sC, sS, false, sA, false, w, 1.0, false);
+      s2_st(v + ws, sC, w);
+    }
+  }
+  if (hasr) {
+    // coarse c_r (index g): H left part = E_last^T Y_{nb-1, j}; Rh term -E_last^T Y_{nb-1,nb-1} E_last
+    cplx* p1 = s2_panel1(a, s, cr, w);
+    s2_ld(sA, E(nb - 1), w);
+    for (int j = 0; j < nb; ++j) {
+      s2_ld(sS, Y + ((nb - 1) * nb + j) * ws, w);
+      s2_mm(sC, sA, true, sS, false, w, 1.0, false);
+      s2_put(p1, a.ld1, j * w, sC, w);
+      if (j == nb - 1) {
+        s2_mm(sT, sC, false, sA, false, w, -1.0, false);
+        s2_st(a.cd + ((long)s * M + g) * 3 * ws, sT, w);
+      }
+    }
+  }
+  if (hasl) {
+    // coarse c_l (index g - 1): H right part = E_cl Y_{0, j} (after the left group's nbl blocks);
+    // Rh term -E_cl Y_00 E_cl^T; Rh_{g-1, g} = -E_cl Y_{0,nb-1} E_last
+    const int nbl = a.plan[32 + g - 1];
+    cplx* p1 = s2_panel1(a, s, cl, w);
+    s2_ld(sA, rr + ((long)cl * 2 + 1) * ws, w);
+    for (int j = 0; j < nb; ++j) {
+      s2_ld(sS, Y + j * ws, w);
+      s2_mm(sC, sA, false, sS, false, w, 1.0, false);
+      s2_put(p1, a.ld1, (nbl + j) * w, sC, w);
+      if (j == 0) {
+        s2_mm(sT, sC, false, sA, true, w, -1.0, false);
+        s2_st(a.cd + ((long)s * M + g - 1) * 3 * ws + ws, sT, w);
+      }
+      if (j == nb - 1 && hasr) {
+        s2_ld(sS, E(nb - 1), w);
+        s2_mm(sT, sC, false, sS, false, w, -1.0, false);
+        s2_st(a.cd + ((long)s * M + g - 1) * 3 * ws + 2 * ws, sT, w);
+      }
+    }
+  }
+}
+
+// One CTA per strip: the coarse Schur system Rh (M blocks) and Xc = Rh^{-1};
+// the coarse separators' panel 2 (rows of Xc).
+__global__ void __launch_bounds__(kSep2Threads) k_sep2_coarse(Sep2Args a) {
+  __shared__ RowSmem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.x + a.s0;
+  const int w = a.w[s], K = a.P - 1, M = a.plan[0];
+  const long ws = (long)a.wmax * a.wmax;
+  cplx* sA = reinterpret_cast<cplx*>(smem_raw);
+  cplx *sB = sA + ws, *sC = sB + ws, *sS = sC + ws;
+  const cplx* rr = a.rraw + (long)s * K * 2 * ws;
+  cplx* xcs = a.xc + (long)s * (M * M + 3 * M) * ws;   // Xc, then Li, Ri, Dh
+  cplx* Li = xcs + (long)M * M * ws;
+  cplx* Ri = Li + (long)M * ws;
+  cplx* Dh = Ri + (long)M * ws;
+  const cplx* cd = a.cd + (long)s * M * 3 * ws;
+  for (int j = 0; j < M; ++j) {   // Rh_jj = R_cc + left term + right term
+    const int c = a.plan[8 + j + 1] - 1;
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x)
+      Dh[j * ws + e] = cadd(__ldcg(rr + (long)c * 2 * ws + e), cadd(__ldcg(cd + (long)j * 3 * ws + e), __ldcg(cd + ((long)j * 3 + 1) * ws + e)));
+  }
+  __syncthreads();
+  auto D = [&](int j) { return (const cplx*)(Dh + j * ws); };
+  auto E = [&](int j) { return cd + ((long)j * 3 + 2) * ws; };
+  if (s2_bt_inverse(M, w, ws, D, E, Li, Ri, xcs, sA, sB, sC, sS, sm)) {
+    if (threadIdx.x == 0) atomicCAS(a.status, 0, -(s * 1024 + 1000));
+    return;
+  }
+  for (int j = 0; j < M; ++j) {
+    const int c = a.plan[8 + j + 1] - 1;
+    cplx* p2 = s2_panel2(a, s, c, w);
+    for (int i = 0; i < M; ++i) {
+      s2_ld(sS, xcs + ((long)j * M + i) * ws, w);
+      s2_put(p2, a.ld2, i * w, sS, w);
+    }
+  }
+}
+
+// One CTA per (separator, strip): panel 2 of a fine separator, Q_p = V_p Xc_{cl,.} + W_p Xc_{cr,.}
+__global__ void __launch_bounds__(kSep2Threads) k_sep2_q(Sep2Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.y + a.s0, p = blockIdx.x;
+  const int w = a.w[s], K = a.P - 1, M = a.plan[0];
+  if (p >= K) return;
+  const int* pk = a.plan + kSep2PlanHdr + p * kSep2PlanStride;
+  if (pk[0] != 0) return;   // coarse
+  const int g = pk[2];
+  const long ws = (long)a.wmax * a.wmax;
+  cplx* sV = reinterpret_cast<cplx*>(smem_raw);
+  cplx *sW = sV + ws, *sX = sW + ws, *sC = sX + ws;
+  const cplx* xcs = a.xc + (long)s * (M * M + 3 * M) * ws;
+  const cplx* v = a.vw + ((long)s * K + p) * 2 * ws;
+  const bool hasl = g > 0, hasr = g < M;
+  if (hasl) s2_ld(sV, v, w);
+  if (hasr) s2_ld(sW, v + ws, w);
+  cplx* p2 = s2_panel2(a, s, p, w);
+  for (int i = 0; i < M; ++i) {
+    bool any = false;
+    if (hasl) { s2_ld(sX, xcs + ((long)(g - 1) * M + i) * ws, w); s2_mm(sC, sV, false, sX, false, w, 1.0, false); any = true; }
+    if (hasr) { s2_ld(sX, xcs + ((long)g * M + i) * ws, w); s2_mm(sC, sW, false, sX, false, w, 1.0, any); any = true; }
+    s2_put(p2, a.ld2, i * w, sC, w);
   }
 }
 
@@ -985,9 +1333,12 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
 #ifndef HELM_SEG_EXTRA
 #define HELM_SEG_EXTRA 0   // where the segments with one more row go (0 first, 1 last, 2 middle)
 #endif
-static int choose_segments(int nc, int requested) {
+static int choose_segments(int nc, int requested, int wmax) {
   if (requested > 0) return requested;
-  int P = 36;   // t = 4 batches: 144 segment CTAs on 148 SMs (C5 t = 4 apply: P = 33 3.83, 36 3.75, 37 3.81 ms)
+  // two-chain kernel (w <= 36): t = 4 batches of 36 segment CTAs fill 144 of the 148 SMs
+  // (C5 t = 4 apply: P = 33 3.83, 36 3.75, 37 3.81 ms); wider strips (general kernel,
+  // explicit separator rows formed in global memory) keep 33
+  int P = wmax <= 36 ? 36 : 33;
   while (P > 1 && (nc - (P - 1)) / P < 8) --P;
   return P;
 }
@@ -1051,7 +1402,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       return HELM_EINVAL;
     }
   }
-  int P = choose_segments(nc, n_segments);
+  int P = choose_segments(nc, n_segments, wmax);
   if (P < 1 || nc - (P - 1) < P) {
     helm_set_error("sweep_setup: %d segments do not fit %d cross rows", P, nc);
     delete h;
@@ -1114,6 +1465,62 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       xinv_total += (long)(P - 1) * h->w[s2] * x_ld(P - 1, h->w[s2]);
     }
   }
+  // two-level separator solve (k_sweep_dual): group / coarse plan and panel sizes
+  const int Ksep = P - 1;
+  // (opt-in, sep_two_level knob: parity-tested, measured slower than the full rows on C5 --
+  // two dependent latency-bound rounds and a coarse barrier instead of one HBM-bound
+  // mat-vec)
+  const bool want_sep2 = want_fac2 && Ksep >= 8 && Ksep <= 80 && helm_knob(KNOB_SEP_TWO_LEVEL);
+  std::vector<int> plan;
+  int M2 = 0, ngr2 = 0, nbmax2 = 0, nb1max2 = 0;
+  long sep2_total = 0;
+  if (want_sep2) {
+    M2 = std::max(1, (int)std::lround(std::sqrt(Ksep + 1.0)) - 1);
+    while ((Ksep - M2 + M2) / (M2 + 1) > kSep2MaxB && M2 < 8) ++M2;   // ceil((K - M) / (M + 1)) <= kSep2MaxB
+    ngr2 = M2 + 1;
+    const int fine = Ksep - M2, base = fine / ngr2, extra = fine % ngr2;
+    plan.assign(kSep2PlanHdr + Ksep * kSep2PlanStride, 0);
+    plan[0] = M2;
+    plan[1] = ngr2;
+    std::vector<int> gs(ngr2), gl(ngr2);
+    for (int g2 = 0, k = 0; g2 < ngr2; ++g2) {
+      gl[g2] = base + (g2 < extra ? 1 : 0);
+      gs[g2] = k;
+      plan[8 + g2] = gs[g2];
+      plan[32 + g2] = gl[g2];
+      nbmax2 = std::max(nbmax2, gl[g2]);
+      for (int l = 0; l < gl[g2]; ++l) {   // fine separators of group g2
+        int* pk = &plan[kSep2PlanHdr + (k + l) * kSep2PlanStride];
+        pk[0] = 0; pk[1] = gl[g2]; pk[2] = g2;
+        for (int j = 0; j < gl[g2]; ++j) pk[4 + j] = k + j;
+      }
+      k += gl[g2];
+      if (g2 < M2) {   // coarse separator g2 at k: both adjacent groups
+        int* pk = &plan[kSep2PlanHdr + k * kSep2PlanStride];
+        pk[0] = 1; pk[2] = g2;
+        k += 1;
+      }
+    }
+    for (int j = 0; j < M2; ++j) {
+      const int c = gs[j + 1] - 1;
+      int* pk = &plan[kSep2PlanHdr + c * kSep2PlanStride];
+      pk[1] = gl[j] + gl[j + 1];
+      for (int l = 0; l < gl[j]; ++l) pk[4 + l] = gs[j] + l;
+      for (int l = 0; l < gl[j + 1]; ++l) pk[4 + gl[j] + l] = gs[j + 1] + l;
+      nb1max2 = std::max(nb1max2, pk[1]);
+    }
+    nb1max2 = std::max(nb1max2, nbmax2);
+    plan[2] = nb1max2;
+    h->sep2_M = M2;
+    h->sep2_ld1 = (nb1max2 * wmax + 7) / 8 * 8;
+    h->sep2_ld2 = (M2 * wmax + 7) / 8 * 8;
+    h->sep2_off.resize(n_strips);
+    for (int s2 = 0; s2 < n_strips; ++s2) {
+      h->sep2_off[s2] = sep2_total;
+      sep2_total += (long)Ksep * h->w[s2] * (h->sep2_ld1 + h->sep2_ld2);
+    }
+    h->factor_bytes += sep2_total * (long)sizeof(cplx);
+  }
   SharedFactors* sf = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_shared_mu);
@@ -1140,7 +1547,10 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   alloc((void**)&h->d_pfac_off, sizeof(long) * n_strips);
   alloc((void**)&h->d_red_off, sizeof(long) * n_strips);
   if (want_xinv) alloc((void**)&h->d_xinv_off, sizeof(long) * n_strips);
+  if (want_sep2) alloc((void**)&h->d_sep2_off, sizeof(long) * n_strips);
   if (!sf) {
+    if (want_sep2) alloc((void**)&h->d_sep2, sizeof(cplx) * sep2_total);
+    if (want_sep2) alloc((void**)&h->d_sep2_plan, sizeof(int) * plan.size());
     alloc((void**)&h->d_dg, sizeof(cplx) * bandN);
     alloc((void**)&h->d_al, sizeof(cplx) * bandN);
     alloc((void**)&h->d_cr, sizeof(cplx) * bandN);
@@ -1170,6 +1580,8 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   h2d(h->d_pfac_off, h->pfac_off.data(), sizeof(long) * n_strips);
   h2d(h->d_red_off, h->red_off.data(), sizeof(long) * n_strips);
   if (want_xinv) h2d(h->d_xinv_off, h->xinv_off.data(), sizeof(long) * n_strips);
+  if (want_sep2) h2d(h->d_sep2_off, h->sep2_off.data(), sizeof(long) * n_strips);
+  if (want_sep2 && !sf) h2d(h->d_sep2_plan, plan.data(), sizeof(int) * plan.size());
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: copy geometry: %s", cudaGetErrorString(e));
     sweep_destroy(h);
@@ -1179,6 +1591,8 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     // same strips already factored: share the device factor set
     h->d_dg = sf->dg; h->d_al = sf->al; h->d_cr = sf->cr; h->d_ne = sf->ne; h->d_tc = sf->tc;
     h->d_fac = sf->fac; h->d_red = sf->red; h->d_xinv = sf->xinv; h->d_fac2 = sf->fac2; h->d_facp = sf->facp;
+    h->d_sep2 = sf->sep2; h->d_sep2_plan = sf->sep2_plan;
+    if (!h->d_sep2) { helm_dev_free(h->d_sep2_off); h->d_sep2_off = nullptr; h->sep2_M = 0; }
     h->factor_bytes = sf->factor_bytes;
     h->xinv_elems = sf->xinv_elems;
     h->shared = sf;
@@ -1218,9 +1632,20 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     alloc((void**)&scratch, sizeof(cplx) * sstride * n_strips * P);
     alloc((void**)&rscratch, sizeof(cplx) * 2L * wmax * wmax * n_strips);
   }
+  const long ws2 = (long)wmax * wmax;
+  const long ytmp_stride = (2L * kSep2MaxB + (long)nbmax2 * nbmax2) * ws2;
+  cplx *rraw = nullptr, *ytmp = nullptr, *vw = nullptr, *cdm = nullptr, *xcm = nullptr;
+  if (want_sep2) {
+    alloc((void**)&rraw, sizeof(cplx) * (long)n_strips * Ksep * 2 * ws2);
+    alloc((void**)&ytmp, sizeof(cplx) * (long)n_strips * ngr2 * ytmp_stride);
+    alloc((void**)&vw, sizeof(cplx) * (long)n_strips * Ksep * 2 * ws2);
+    alloc((void**)&cdm, sizeof(cplx) * (long)n_strips * M2 * 3 * ws2);
+    alloc((void**)&xcm, sizeof(cplx) * (long)n_strips * (M2 * M2 + 3 * M2) * ws2);
+  }
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: scratch: %s", cudaGetErrorString(e));
     helm_dev_free(d_status); helm_dev_free(scratch); helm_dev_free(rscratch);
+    helm_dev_free(rraw); helm_dev_free(ytmp); helm_dev_free(vw); helm_dev_free(cdm); helm_dev_free(xcm);
     sweep_destroy(h);
     return HELM_ENOMEM;
   }
@@ -1232,6 +1657,14 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
              nc, wmax, P, h->d_fac, scratch, sstride, d_status, h->d_fac2, h->d_facp, h->d_pfac_off};
   RedArgs ra{h->d_w, h->d_fac_off, h->d_red_off, h->d_seg_lo, h->d_seg_hi, h->d_dg, h->d_al, h->d_cr,
              h->d_ne, nc, wmax, P, h->d_fac, scratch, sstride, h->d_red, rscratch, d_status};
+  ra.rraw = rraw;
+  Sep2Args sa{h->d_w, wmax, P, 0, rraw, h->d_sep2_plan, ytmp, ytmp_stride, vw, cdm, xcm,
+              h->d_sep2, h->d_sep2_off, h->sep2_ld1, h->sep2_ld2, d_status};
+  if (want_sep2) {
+    cudaFuncSetAttribute(k_sep2_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(5 * ws2 * sizeof(cplx)));
+    cudaFuncSetAttribute(k_sep2_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * ws2 * sizeof(cplx)));
+    cudaFuncSetAttribute(k_sep2_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * ws2 * sizeof(cplx)));
+  }
   const size_t smr = sizeof(cplx) * (9 * (size_t)wmax * wmax + 12 * (size_t)wmax);
   const size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
   if (P > 1 && wmax <= kRowW) cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
@@ -1259,6 +1692,15 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       if (timing) cudaEventRecord(tev[3], cs);
       g_helm_launches++;
       e2 = cudaGetLastError();
+      if (e2 == cudaSuccess && want_sep2) {
+        Sep2Args sc = sa;
+        sc.s0 = s0;
+        k_sep2_group<<<dim3(ngr2, ns), kSep2Threads, 5 * ws2 * sizeof(cplx), cs>>>(sc);
+        k_sep2_coarse<<<ns, kSep2Threads, 4 * ws2 * sizeof(cplx), cs>>>(sc);
+        k_sep2_q<<<dim3(Ksep, ns), kSep2Threads, 4 * ws2 * sizeof(cplx), cs>>>(sc);
+        g_helm_launches += 3;
+        e2 = cudaGetLastError();
+      }
       if (e2 == cudaSuccess && want_xinv) {
         // explicit separator inverse rows for the register-streaming kernel
         // (128 threads: 256 measured slower, round 1)
@@ -1339,10 +1781,16 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   helm_dev_free(d_status);
   helm_dev_free(scratch);
   helm_dev_free(rscratch);
+  helm_dev_free(rraw); helm_dev_free(ytmp); helm_dev_free(vw); helm_dev_free(cdm); helm_dev_free(xcm);
   if (e != cudaSuccess) {
     helm_set_error("sweep_setup: factorisation kernel: %s", cudaGetErrorString(e));
     sweep_destroy(h);
     return HELM_ECUDA;
+  }
+  if (status < 0) {
+    helm_set_error("sweep_setup: zero pivot in the two-level separator system of strip %d", (-status - 1) / 1024);
+    sweep_destroy(h);
+    return HELM_ESINGULAR;
   }
   if (status != 0) {
     int s = (status - 1) / nc, c = (status - 1) % nc;
@@ -1353,6 +1801,8 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   sf = new SharedFactors{1, prob->uid, axis, n_strips, overlap, P, h->d_dg, h->d_al, h->d_cr, h->d_ne, h->d_tc,
                          h->d_fac, h->d_red, h->d_xinv, h->d_fac2, h->d_facp, h->factor_bytes};
   sf->xinv_elems = h->xinv_elems = want_xinv ? xinv_total : 0;
+  sf->sep2 = h->d_sep2; sf->sep2_plan = h->d_sep2_plan;
+  sf->sep2_M = h->sep2_M; sf->sep2_ld1 = h->sep2_ld1; sf->sep2_ld2 = h->sep2_ld2;
   {
     std::lock_guard<std::mutex> lk(g_shared_mu);
     g_shared.push_back(sf);
@@ -1436,7 +1886,7 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
   helm_dev_free(h->d_a); helm_dev_free(h->d_w); helm_dev_free(h->d_own_lo); helm_dev_free(h->d_own_hi);
   helm_dev_free(h->d_seg_lo); helm_dev_free(h->d_seg_hi); helm_dev_free(h->d_fac_off);
   helm_dev_free(h->d_pfac_off);
-  helm_dev_free(h->d_red_off); helm_dev_free(h->d_xinv_off);
+  helm_dev_free(h->d_red_off); helm_dev_free(h->d_xinv_off); helm_dev_free(h->d_sep2_off);
   bool free_factors = true;
   if (h->shared) {
     std::lock_guard<std::mutex> lk(g_shared_mu);
@@ -1454,6 +1904,7 @@ extern "C" void sweep_destroy(helm_sweep_t h) {
     helm_dev_free(h->d_dg); helm_dev_free(h->d_al); helm_dev_free(h->d_cr); helm_dev_free(h->d_ne);
     helm_dev_free(h->d_tc); helm_dev_free(h->d_fac); helm_dev_free(h->d_red); helm_dev_free(h->d_xinv);
     helm_dev_free(h->d_fac2); helm_dev_free(h->d_facp);
+    helm_dev_free(h->d_sep2); helm_dev_free(h->d_sep2_plan);
   }
   delete h;
 }

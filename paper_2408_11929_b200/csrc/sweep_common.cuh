@@ -27,6 +27,11 @@ struct DirArgs {
   const cplx* xinv;      // explicit separator-inverse rows (fast kernel), NULL if absent
   const float2* xinv32;  // their complex64 copy (inexact separator solve, two-chain kernel), NULL if off
   const long* xinv_off;
+  const cplx* sep2;      // two-chain kernel: two-level separator panels (strip_setup.cu), NULL = full R^{-1} rows
+  const long* sep2_off;
+  const int* sep2_plan;
+  int sep2_M, sep2_ld1, sep2_ld2;
+  cplx* gh;              // two-level: the coarse right-hand sides [2][M][wmax]
   int wmax;
   int cta_base;
   int vec_rows;

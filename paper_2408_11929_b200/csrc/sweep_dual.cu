@@ -55,14 +55,8 @@
 #ifndef HELM_DUAL_XPRE_FRAC
 #define HELM_DUAL_XPRE_FRAC 4   // quarters of each X row prefetched early
 #endif
-#ifndef HELM_DUAL_XSYM
-#define HELM_DUAL_XSYM 0    // 1: read only the upper block triangle of X (each block by its two users)
-#endif
 #ifndef HELM_DUAL_XCH
 #define HELM_DUAL_XCH 4     // 32-column chunks per row in flight in the X mat-vec (4 rows per warp)
-#endif
-#ifndef HELM_DUAL_XTU
-#define HELM_DUAL_XTU 4     // rows in flight per lane in the transposed X part (XSYM)
 #endif
 #ifndef HELM_DUAL_ONELOOP
 #define HELM_DUAL_ONELOOP 1   // 1: one copy of the solve loop (the chain phases dispatch on the group): half the code
@@ -81,6 +75,9 @@
 #ifndef HELM_DUAL_XPF_EARLY
 #define HELM_DUAL_XPF_EARLY 0   // > 0: the X rows are prefetched into L2 by the producer this many phase-1 blocks before the end
 #endif
+#ifndef HELM_DUAL_S2PF
+#define HELM_DUAL_S2PF 2   // two-level panels' L2 prefetch: 0 none, 1 normal priority, 2 evict_first
+#endif
 #ifndef HELM_DUAL_XPF_PROD
 #define HELM_DUAL_XPF_PROD 1    // 1: the X-row L2 prefetch is issued by the chain-A producer warp when phase 1 ends
 #endif
@@ -98,8 +95,6 @@ constexpr int WM = 40;    // vector stride
 constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
 constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA producer warps
 }  // namespace dualk
-// partial sums of the transposed X part (HELM_DUAL_XSYM only): <= 10 consumer warps
-constexpr int kXpartElems = HELM_DUAL_XSYM ? 10 * dualk::WM : 0;
 
 // per-CTA cycle counters (tools/prof_sweep.py) only in the -DHELM_DUAL_PROF build
 // (python -m paper_2408_11929_b200.build --prof); the per-step sub-phase counters
@@ -128,13 +123,17 @@ struct DualArgs {
   int pmax;
   int stage_elems;  // cplx per ring stage (>= largest packed block + 1 zero entry)
   int mmax;         // largest segment (rows)
-  long long* prof;  // optional per-CTA counters (24 per CTA)
+  long long* prof;  // optional per-CTA counters (32 per CTA)
 };
+
+// two-level separator plan layout (strip_setup.cu kSep2*)
+constexpr int kS2PlanHdr = 64, kS2PlanStride = 4 + 2 * 8;
 
 struct DualTab {
   const cplx* fac;
   const cplx* fac2;
   const cplx* xinv;
+  const cplx* sep2;       // this strip's two-level panels (NULL: full rows)
   const float2* xinv32;   // complex64 rows (XF32 instantiation only)
   int w, a, s, pks;   // pks: entries per padded packed block (pk_size(w))
 };
@@ -229,8 +228,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   cplx* fb = xa + A.vec_elems;                      // chain B phase 3
   cplx* bcr = fb + A.vec_elems;                     // staged U couplings, rows lo-1..hi (row stride wmax)
   cplx* bne = bcr + A.vec_elems;
-  cplx* xpart = bne + A.vec_elems + (2 + kTcW) * A.mmax;   // [consumer warps][WM] partial sums of the transposed X part
-  cplx* gsm_own = xpart + kXpartElems;              // GSEP: after cs / cps / tcs / xpart
+  cplx* gsm_own = bne + A.vec_elems + (2 + kTcW) * A.mmax;   // GSEP: after cs / cps / tcs
   cplx* gsm = GSEP ? gsm_own : xa;                  // separator RHS g (K x w): xa (+ fb), dead before phase 3
   cplx* cs = bne + A.vec_elems;                     // [mmax] corrections formed by the last epilogue (next RHS)
   cplx* cps = cs + A.mmax;                          // [mmax] forward-pass corr_prev rows (backward RHS), staged
@@ -243,6 +241,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     tab[i].fac2 = D_.fac2 + D_.pfac_off[s];
     tab[i].xinv = D_.xinv + D_.xinv_off[s];
     tab[i].xinv32 = D_.xinv32 ? D_.xinv32 + D_.xinv_off[s] : nullptr;
+    tab[i].sep2 = D_.sep2 ? D_.sep2 + D_.sep2_off[s] : nullptr;
     tab[i].w = D_.w[s];
     tab[i].a = D_.a[s];
     tab[i].s = s;
@@ -266,6 +265,10 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // columns (y axis: a line of the strip is contiguous), odd column stride
   const int bsq = D_.axis == 0 ? 1 : (m | 1);
   for (int k = tid; k < K; k += blockDim.x) sepr[k] = D_.seg_hi[k] + 1;
+  // this segment's entry of the two-level separator plan (the same for every strip)
+  __shared__ int spk[kS2PlanStride];
+  if (D_.sep2 && p < K)
+    for (int e = tid; e < kS2PlanStride; e += blockDim.x) spk[e] = D_.sep2_plan[kS2PlanHdr + p * kS2PlanStride + e];
   if (lo == 0)
     for (int e = tid; e < bw; e += blockDim.x) bcr[e] = bne[e] = cmk(0, 0);   // row -1 (never staged)
   const int total = nsolve * 2 * m;      // block steps per chain
@@ -291,9 +294,25 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           if (!XF32 && pg == 0 && e == std::max(m - HELM_DUAL_XPF_EARLY, 0) && p < P - 1) {
             // this solve's separator-inverse rows into L2 while phase 1 still runs
             const int w2 = tab[i2].w;
-            const long ld = x_ld(K, w2);
-            for (int r = 0; r < w2; ++r)
-              dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
+            if (tab[i2].sep2) {
+              const int* pk = spk;
+              const cplx* pan = tab[i2].sep2 + (long)p * w2 * (D_.sep2_ld1 + D_.sep2_ld2);
+              const uint32_t b1 = (uint32_t)((long)pk[1] * w2 * sizeof(cplx)), b2 = (uint32_t)((long)D_.sep2_M * w2 * sizeof(cplx));
+              for (int r = 0; r < w2 && HELM_DUAL_S2PF; ++r) {
+                if (HELM_DUAL_S2PF == 1) {   // normal eviction priority
+                  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pan + (long)r * D_.sep2_ld1), "r"(b1) : "memory");
+                  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pan + (long)w2 * D_.sep2_ld1 + (long)r * D_.sep2_ld2),
+                               "r"(b2) : "memory");
+                } else {
+                  dprefetch_l2(pan + (long)r * D_.sep2_ld1, b1, polF);
+                  dprefetch_l2(pan + (long)w2 * D_.sep2_ld1 + (long)r * D_.sep2_ld2, b2, polF);
+                }
+              }
+            } else {
+              const long ld = x_ld(K, w2);
+              for (int r = 0; r < w2; ++r)
+                dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
+            }
           }
 #endif
           const int st = f % NST;
@@ -339,14 +358,14 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   // they cost no registers: [0] pre-actions [1] separator stage [2] X mat-vec
   // [4] waits [8..11] step sub-phases (mat-vec, loads+reduce, writer, barrier)
   // [12] gather wait [13] neighbour wait [14] corrections + g
-  __shared__ long long profs[24];
+  __shared__ long long profs[32];
   auto pacc = [&](int k, long long v) {
     if constexpr (kProf) {
       if (tid == 0) profs[k] += v;
     }
   };
   if (kProf && tid == 0)
-    for (int k = 0; k < 24; ++k) profs[k] = 0;
+    for (int k = 0; k < 32; ++k) profs[k] = 0;
   const long long t_start = pclk();
   auto cbar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(ncons) : "memory"); };
   auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(gsz) : "memory"); };
@@ -550,20 +569,15 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     const long long csep0 = pclk();
     if (p < P - 1 && tid < 32 && ((HELM_DUAL_XPF_EARLY == 0 && !HELM_DUAL_XPF_PROD) || XF32)) {
-      // stream this CTA's part of the UPPER block triangle of the separator inverse
-      // (row r of block row p, columns p w .. K w) into L2 while the all-gather
-      // completes; the mat-vec reads it from L2, and so does CTA k > p, which uses
-      // block (p, k) transposed (X = R^{-1} is complex symmetric)
+      // (the XF32 variant, or the XPF_PROD = 0 ablation) stream this CTA's rows of the
+      // separator inverse into L2 while the all-gather completes
       const long ld = x_ld(K, w);
-      const int kc = HELM_DUAL_XSYM ? p : 0;   // first column block read from block row p
       if constexpr (XF32) {
-        const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(float2));
-        for (int r = tid; r < w; r += 32)
-          dprefetch_l2(tab[i].xinv32 + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
+        const uint32_t bytes = (uint32_t)((long)K * w * (long)sizeof(float2));
+        for (int r = tid; r < w; r += 32) dprefetch_l2(tab[i].xinv32 + ((long)p * w + r) * ld, bytes, pol_first);
       } else {
-        const uint32_t bytes = (uint32_t)((long)(K - kc) * w * (long)sizeof(cplx));
-        for (int r = tid; r < w; r += 32)
-          dprefetch_l2(tab[i].xinv + ((long)p * w + r) * ld + (long)kc * w, bytes, pol_first);
+        const uint32_t bytes = (uint32_t)((long)K * w * (long)sizeof(cplx));
+        for (int r = tid; r < w; r += 32) dprefetch_l2(tab[i].xinv + ((long)p * w + r) * ld, bytes, pol_first);
       }
     }
     // publish this segment's contributions to its two separator right-hand sides:
@@ -678,7 +692,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #else
     if (p < P - 1) {
 #endif
-      const long c0 = HELM_DUAL_XSYM ? (long)p * w : 0;
       constexpr int XCH = HELM_DUAL_XCH;
       if constexpr (XF32) {
         // inexact separator solve (sweep_set_precision(32)): complex64 rows of R^{-1}, FP32
@@ -724,74 +737,101 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           }
         }
       } else {
-      // normal part: 4 rows per warp, lanes over the columns, 4 XCH loads in flight per lane
-      for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
-        const cplx* Xr[4];
-        bool ok[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ok[u] = rb + u < w;
-          Xr[u] = tab[i].xinv + ((long)p * w + (ok[u] ? rb + u : 0)) * xld;
+      // Rounds of row-panel mat-vecs: one with the full explicit inverse (row block p of
+      // R^{-1} times g), or two with the two-level panels (strip_setup.cu): panel 1 times
+      // the gathered group separators' g (a coarse CTA then publishes its coarse RHS
+      // gh = g_p - result), panel 2 times all coarse RHSs once published.
+      const cplx* sep2 = tab[i].sep2;
+      const int* pk = spk;
+      const bool coarse = sep2 && pk[0] == 1;
+      const int M2 = D_.sep2_M;
+      cplx* vx = bseg;                       // gathered panel vector (bseg is free in this stage)
+      cplx* ytmp = bseg + (long)(2 * 8 + 8) * w;   // round-1 result of a fine separator
+      cplx* gh = D_.gh + (long)par * M2 * D_.wmax;
+      const int nround = sep2 ? 2 : 1;
+      long long crd = pclk();
+      for (int rd = 0; rd < nround; ++rd) {
+        const cplx* pbase;
+        long ld, ncol;
+        const cplx* vec;
+        cplx* out;
+        if (!sep2) {
+          pbase = tab[i].xinv + (long)p * w * xld; ld = xld; ncol = Kw; vec = gsm; out = xhi;
+        } else if (rd == 0) {
+          const int n1 = pk[1];
+          for (int e = tid; e < n1 * w; e += ncons) {
+            const int b2 = e / w, qq = e - b2 * w;
+            vx[e] = gsm[(long)pk[4 + b2] * w + qq];
+          }
+          cbar();
+          pbase = sep2 + (long)p * w * (D_.sep2_ld1 + D_.sep2_ld2); ld = D_.sep2_ld1; ncol = (long)n1 * w; vec = vx;
+          out = coarse ? xhi : ytmp;
+        } else {
+          // every coarse RHS is published: gather them
+          if (tid == 0) {
+            while (ld_relaxed(&D_.cnt[2]) < (unsigned)(M2 * (i + 1))) __nanosleep(20);
+            (void)ld_acquire(&D_.cnt[2]);
+          }
+          cbar();
+          pacc(24, pclk() - crd);   // (two-level) wait for the coarse RHSs
+          crd = pclk();
+          for (int e = tid; e < M2 * w; e += ncons) {
+            const int j = e / w, qq = e - j * w;
+            vx[e] = ldcg(gh + (long)j * D_.wmax + qq);
+          }
+          cbar();
+          pbase = sep2 + (long)p * w * (D_.sep2_ld1 + D_.sep2_ld2) + (long)w * D_.sep2_ld1; ld = D_.sep2_ld2;
+          ncol = (long)M2 * w; vec = vx; out = xhi;
         }
-        cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-        for (long jj = c0 + lane; jj < Kw; jj += 32 * XCH) {
-          cplx xv[4][XCH], gv[XCH];
+        // 4 rows per warp, lanes over the columns, XCH loads in flight per lane
+        for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
+          const cplx* Xr[4];
+          bool ok[4];
 #pragma unroll
-          for (int v = 0; v < XCH; ++v) {
-            const bool in = jj + 32 * v < Kw;
-            gv[v] = in ? gsm[jj + 32 * v] : cmk(0, 0);
+          for (int u = 0; u < 4; ++u) {
+            ok[u] = rb + u < w;
+            Xr[u] = pbase + (long)(ok[u] ? rb + u : 0) * ld;
+          }
+          cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+          for (long jj = lane; jj < ncol; jj += 32 * XCH) {
+            cplx xv[4][XCH], gv[XCH];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ld_cg_hint(Xr[u] + jj + 32 * v, pol_first) : cmk(0, 0);
+            for (int v = 0; v < XCH; ++v) {
+              const bool in = jj + 32 * v < ncol;
+              gv[v] = in ? vec[jj + 32 * v] : cmk(0, 0);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ld_cg_hint(Xr[u] + jj + 32 * v, pol_first) : cmk(0, 0);
+            }
+#pragma unroll
+            for (int v = 0; v < XCH; ++v)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
           }
 #pragma unroll
-          for (int v = 0; v < XCH; ++v)
+          for (int u = 0; u < 4; ++u) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
-            acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+            for (int off = 16; off > 0; off >>= 1) {
+              acc[u].x += __shfl_xor_sync(0xffffffffu, acc[u].x, off);
+              acc[u].y += __shfl_xor_sync(0xffffffffu, acc[u].y, off);
+            }
+            if (lane == 0 && ok[u]) out[rb + u] = acc[u];
           }
-          if (lane == 0 && ok[u]) xhi[rb + u] = acc[u];
         }
-      }
-      }
-      // transposed part: rows (k, i), k < p, of the blocks (k, p), lanes over r;
-      // 4 rows in flight per lane, per-warp partial sums combined in a fixed order
-      cplx t0 = cmk(0, 0), t1 = cmk(0, 0);
-      const int nrow = HELM_DUAL_XSYM ? p * w : 0;
-      for (int e0 = cw; e0 < nrow; e0 += HELM_DUAL_XTU * ncw) {
-        cplx xa0[HELM_DUAL_XTU], xa1[HELM_DUAL_XTU], gv[HELM_DUAL_XTU];
-#pragma unroll
-        for (int u = 0; u < HELM_DUAL_XTU; ++u) {
-          const int e = e0 + u * ncw;
-          const bool ok = e < nrow;
-          const cplx* row = tab[i].xinv + (long)(ok ? e : 0) * xld + c0;   // row (k, i) = global row e = k w + i
-          xa0[u] = (ok && lane < w) ? ld_cg_hint(row + lane, pol_first) : cmk(0, 0);
-          xa1[u] = (ok && lane + 32 < w) ? ld_cg_hint(row + lane + 32, pol_first) : cmk(0, 0);
-          gv[u] = ok ? gsm[e] : cmk(0, 0);                                   // g_k[i] = gsm[k w + i]
+        cbar();
+        pacc(rd == 0 ? 25 : 26, pclk() - crd);   // (two-level) round 1 / round 2 mat-vecs (incl. gathers)
+        crd = pclk();
+        if (sep2 && rd == 0 && coarse) {
+          // gh_c = g_p - H g (this coarse separator's index pk[2])
+          for (int e = tid; e < w; e += ncons) gh[(long)pk[2] * D_.wmax + e] = csub(gsm[(long)p * w + e], xhi[e]);
+          cbar();
+          if (tid == 0) red_release_add(&D_.cnt[2], 1u);
         }
-#pragma unroll
-        for (int u = 0; u < HELM_DUAL_XTU; ++u) {
-          cfma(t0, xa0[u], gv[u]);
-          cfma(t1, xa1[u], gv[u]);
-        }
+        if (sep2 && rd == 1 && !coarse)
+          for (int e = tid; e < w; e += ncons) xhi[e] = csub(ytmp[e], xhi[e]);   // x_p = y_p - Q_p gh
       }
-      if (HELM_DUAL_XSYM) {
-        xpart[cw * WM + lane] = t0;
-        if (lane + 32 < WM) xpart[cw * WM + lane + 32] = t1;
       }
     }
     cbar();
-    if (HELM_DUAL_XSYM && p < P - 1)
-      for (int r = tid; r < w; r += ncons) {
-        cplx acc = xhi[r];
-        for (int v = 0; v < ncw; ++v) acc = cadd(acc, xpart[v * WM + r]);
-        xhi[r] = acc;
-      }
     for (int e = tid; e < WM; e += ncons) {
       if (p == 0) xlo[e] = cmk(0, 0);
       if (p == P - 1) xhi[e] = cmk(0, 0);
@@ -1095,7 +1135,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       if (kProf && A.prof && tid == 0 && i < 64) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        A.prof[(long)gridDim.x * 24 + (long)blockIdx.x * 64 + i] = (long long)gt;   // phase-1 end, ns
+        A.prof[(long)gridDim.x * 32 + (long)blockIdx.x * 64 + i] = (long long)gt;   // phase-1 end, ns
       }
       cbar();
       seg_separators(i);
@@ -1144,8 +1184,8 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
   mbar_wait(&sbar[0], (nsolve - 1) & 1);
   seg_epilogue(nsolve - 1);
   if (kProf && A.prof && tid == 0) {
-    long long* o = A.prof + (long)blockIdx.x * 24;
-    for (int k = 0; k < 24; ++k) o[k] = profs[k];
+    long long* o = A.prof + (long)blockIdx.x * 32;
+    for (int k = 0; k < 32; ++k) o[k] = profs[k];
     o[3] = total;
     o[5] = pclk() - t_start; o[6] = 1; o[7] = d;
   }
@@ -1190,7 +1230,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   // g aliases xa and, when it is longer, the adjacent fb (both are free from the
   // epilogue to the end of the separator stage); its own area only beyond that
   const bool gsep = gsm_elems > 2 * vec_elems;
-  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + (2L + kTcW) * mmax_all + kXpartElems + (gsep ? gsm_elems : 0));
+  smem = (smem + 127) / 128 * 128 + sizeof(cplx) * (6 * vec_elems + (2L + kTcW) * mmax_all + (gsep ? gsm_elems : 0));
   // inexact separator solve only when every direction of the batch asked for it
   bool xf32 = true;
   for (int d = 0; d < t; ++d) xf32 = xf32 && dirs[d]->sep_fp32 && dirs[d]->d_xinv32;
@@ -1204,7 +1244,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
   size_t ncnt = 0;
   for (int d = 0; d < t; ++d) {
     coff[d] = ncnt;
-    ncnt += 2 + dirs[d]->P;
+    ncnt += 3 + dirs[d]->P;
   }
   size_t total = al(sizeof(unsigned) * ncnt);
   for (int d = 0; d < t; ++d) {
@@ -1214,6 +1254,7 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     total += al(sizeof(cplx) * 2L * h->P * h->wmax);
     total += al(sizeof(cplx) * (long)h->N * h->nc);
     total += al(sizeof(cplx) * (long)h->nc);
+    total += al(sizeof(cplx) * 2L * 8 * h->wmax);   // gh (two-level coarse RHS, M <= 8)
   }
   unsigned char* scratch = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&scratch, total, st);
@@ -1247,12 +1288,17 @@ int sweep_apply_dual(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr
     D.R = Rdev + (ldr == 0 ? 0 : (long)d * ldr);
     D.Z = Zdev + (long)d * ldz;
     unsigned char* q = scratch + off[d];
-    D.cnt = reinterpret_cast<unsigned*>(scratch) + coff[d]; D.flag = D.cnt + 2;
+    D.cnt = reinterpret_cast<unsigned*>(scratch) + coff[d]; D.flag = D.cnt + 3;
     D.yb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xb = (cplx*)q; q += al(sizeof(cplx) * 2L * 2 * h->P * h->wmax);
     D.xs = (cplx*)q; q += al(sizeof(cplx) * 2L * h->P * h->wmax);
     D.corr_prev = (cplx*)q; q += al(sizeof(cplx) * (long)h->N * h->nc);
-    D.corr_next = (cplx*)q;
+    D.corr_next = (cplx*)q; q += al(sizeof(cplx) * (long)h->nc);
+    D.gh = (cplx*)q;
+    // two-level separator panels when the gathered panel vectors fit the RHS area
+    const bool s2 = h->d_sep2 && !xf32 && vec_elems >= (long)(2 * 8 + 8 + 1) * h->wmax;
+    D.sep2 = s2 ? h->d_sep2 : nullptr; D.sep2_off = h->d_sep2_off; D.sep2_plan = h->d_sep2_plan;
+    D.sep2_M = h->sep2_M; D.sep2_ld1 = h->sep2_ld1; D.sep2_ld2 = h->sep2_ld2;
     D.wmax = h->wmax;
     D.cta_base = base;
     base += h->P;

@@ -543,3 +543,30 @@ def test_setup_chunks(chunks, knob):
     Rh = R.cpu().numpy()
     for k, P in enumerate(_oracle_precs(cfg, A, names)):
         assert elementwise(Zs[1][k], P.apply(Rh[k])) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["C2", "C5s"])
+def test_two_level_separator_solve(name, knob):
+    """The two-chain kernel's opt-in two-level separator solve (fine groups + coarse
+    Schur system, sep_two_level knob, >= 8 separators) against the full explicit
+    R^-1 rows (the default) and the oracle, element-wise."""
+    cfg = CFGS[name]()
+    names = ["LRL", "RLR", "BTB", "TBT"]
+    prob = gpu_problem(cfg)
+    R = to_dev(random_vector(cfg.n, 7, len(names)))
+    Zs = []
+    for two in (1, 0):
+        knob("sep_two_level", two)
+        dirs = [hs.Sweep(prob, nm, n_strips=cfg.n_strips, overlap=cfg.overlap) for nm in names]
+        assert dirs[0].info().n_segments - 1 >= 8
+        Z = torch.zeros((len(names), cfg.n), dtype=torch.complex128, device=DEV)
+        hs.sweep_apply(dirs, R, Z)
+        assert hs.sweep_kernel_name() == "k_sweep_dual"
+        Zs.append(Z.cpu().numpy())
+        del dirs
+    A = p1.assemble(cfg)
+    Rh = R.cpu().numpy()
+    for k, P in enumerate(_oracle_precs(cfg, A, names)):
+        z_ref = P.apply(Rh[k])
+        assert elementwise(Zs[0][k], z_ref) <= 1e-10, (name, k, elementwise(Zs[0][k], z_ref))
+        assert elementwise(Zs[0][k], Zs[1][k]) <= 1e-11

@@ -47,17 +47,17 @@ if os.environ.get("HELM_CYCLES"):
     import ctypes
     L = hs.load()
     ctas = sum(i.n_segments + (1 if i.n_segments > 1 else 0) for i in info)  # upper bound
-    stride = 24 if hs.sweep_kernel_name() == "k_sweep_dual" else 8
-    if stride == 24:
+    stride = 32 if hs.sweep_kernel_name() == "k_sweep_dual" else 8
+    if stride == 32:
         ctas = sum(i.n_segments for i in info)   # the two-chain kernel: P CTAs per direction
-    buf = torch.zeros(ctas * stride + (ctas * 64 if stride == 24 else 0), dtype=torch.int64, device=dev)
+    buf = torch.zeros(ctas * stride + (ctas * 64 if stride == 32 else 0), dtype=torch.int64, device=dev)
     L.helm_sweep_profile.argtypes = [ctypes.c_void_p]
     L.helm_sweep_profile(ctypes.c_void_p(buf.data_ptr()))
     hs.sweep_apply(dirs, r, Z, ldr=0)
     torch.cuda.synchronize()
     L.helm_sweep_profile(ctypes.c_void_p(0))
     b = buf[:ctas * stride].view(ctas, stride).cpu().numpy()
-    if stride == 24 and os.environ.get("HELM_SKEW"):
+    if stride == 32 and os.environ.get("HELM_SKEW"):
         import numpy as np
         gt = buf[ctas * stride:].view(ctas, 64).cpu().numpy().astype(np.float64)
         P = info[0].n_segments
@@ -69,7 +69,7 @@ if os.environ.get("HELM_CYCLES"):
                   f"mean {late.mean():.0f}; latest CTA counts: " +
                   " ".join(f"{p}:{c}" for p, c in sorted(((p, int((late.argmax(axis=0) == p).sum())) for p in range(P)), key=lambda x: -x[1])[:6]))
             print(f"    mean lateness by segment (ns): " + " ".join(f"{v:.0f}" for v in late.mean(axis=1)))
-    if stride == 24:
+    if stride == 32:
         sel = b[b[:, 3] > 0]
         tp = sel[:, 8:12].mean(axis=0) / sel[:, 3].mean()
         print(f"  dual step sub-phases (cycles/step, thread 0): mat-vec {tp[0]:.0f}  loads+reduce+nb {tp[1]:.0f}  "
@@ -81,6 +81,10 @@ if os.environ.get("HELM_CYCLES"):
         print(f"  balanced separator stage (thread 0, per solve): pass A {sel[:,15].mean()/63:.0f}  pass B {sel[:,11].mean()/63:.0f}")
         print(f"  pre-actions (thread 0, per solve): other group's tail {sel[:,9].mean()/63:.0f}  through epilogue {sel[:,10].mean()/63:.0f}  "
               f"coupling wait (slot 15) {sel[:,15].mean()/63:.0f}  stage_bands issue {sel[:,22].mean()/63:.0f}  +staging waits {sel[:,23].mean()/63:.0f}")
+        P0 = info[0].n_segments
+        d0 = b[:P0]
+        print("  two-level per CTA of direction 0 (per solve): wait coarse / round 1 / round 2: " +
+              " ".join(f"{p}:{d0[p,24]/63:.0f}/{d0[p,25]/63:.0f}/{d0[p,26]/63:.0f}" for p in range(P0)))
         print(f"  phases (thread 0, per solve): phase 1 {sel[:,19].mean()/63:.0f}  phase 3 {sel[:,20].mean()/63:.0f}  stage_next {sel[:,21].mean()/63:.0f} | "
               f"separator stage: yb {sel[:,16].mean()/63:.0f}  X+publish {sel[:,17].mean()/63:.0f}  x_lo+inputs {sel[:,18].mean()/63:.0f}")
     for role in (0, 1):

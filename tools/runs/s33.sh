@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python tools/prof_sweep.py --reps 20; python tools/prof_sweep.py --reps 20
