@@ -33,6 +33,7 @@
 // register loads of an earlier revision cost ~1200 cycles per step in L1
 // wavefronts and exposed latency, tools/bench_dualstep.cu).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <cstring>
