@@ -259,6 +259,7 @@ struct RowSmem {
   unsigned redk[12];
   int redi[12];
   int pivrow[kRowW];
+  long long gjp[4];           // HELM_GJ_PROF: thread 0's per-phase pivot-loop cycles
 };
 
 __device__ long long g_red_prof[8];   // diagnostics (setup_timing knob): block 0 sub-phase cycles
@@ -293,12 +294,14 @@ __device__ __forceinline__ int row_invert_g(cplx (&a)[kRowW / LPR], int w, RowSm
   const bool active = i < w;
   bool used = false;
   int kstep = 0;
+#ifdef HELM_GJ_PROF
+  long long gp_s = 0, gp_p = 0, gp_u = 0;
+#endif
 #pragma unroll 1
   for (int k = 0; k < w; ++k) {
     const int kh = k % LPR, kj = k / LPR, par = k & 1;
 #ifdef HELM_GJ_PROF
-    const bool pr = blockIdx.x == 0 && tid == 0;
-    long long q0 = pr ? clock64() : 0;
+    const long long q0 = clock64();
 #endif
     const cplx mine = sel_idx(a, kj);
     const bool cand = active && !used && h == kh;
@@ -309,8 +312,8 @@ __device__ __forceinline__ int row_invert_g(cplx (&a)[kRowW / LPR], int w, RowSm
     if (active && h == kh) sm.pcol[par][i] = mine;
     __syncthreads();
 #ifdef HELM_GJ_PROF
-    long long q1 = pr ? clock64() : 0;
-    if (pr) g_red_prof[3] += q1 - q0;
+    const long long q1 = clock64();
+    gp_s += q1 - q0;
 #endif
     unsigned k0 = sm.redk[0];
     int p = sm.redi[0];
@@ -333,8 +336,8 @@ __device__ __forceinline__ int row_invert_g(cplx (&a)[kRowW / LPR], int w, RowSm
     }
     __syncthreads();
 #ifdef HELM_GJ_PROF
-    long long q2 = pr ? clock64() : 0;
-    if (pr) g_red_prof[4] += q2 - q1;
+    const long long q2 = clock64();
+    gp_p += q2 - q1;
 #endif
     const cplx dinv = sm.pdinv;
     if (i == p) {
@@ -355,9 +358,12 @@ __device__ __forceinline__ int row_invert_g(cplx (&a)[kRowW / LPR], int w, RowSm
       }
     }
 #ifdef HELM_GJ_PROF
-    if (pr) { __syncwarp(1u); g_red_prof[5] += clock64() - q2; }
+    gp_u += clock64() - q2;
 #endif
   }
+#ifdef HELM_GJ_PROF
+  if (tid == 0) { sm.gjp[0] += gp_s; sm.gjp[1] += gp_p; sm.gjp[2] += gp_u; }
+#endif
   __syncthreads();   // pivrow complete; everyone is done reading mat from the previous block
   if (active) {
 #pragma unroll
@@ -740,6 +746,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     }
     cp_async_commit();
   };
+  if (threadIdx.x == 0) sm.gjp[0] = sm.gjp[1] = sm.gjp[2] = 0;
   stage(0);
   for (int k = 0; k <= P - 2; ++k) {
     const int hk = ra.seg_hi[k];          // last row of segment k
@@ -819,6 +826,9 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
     }
     __syncthreads();
     if (pr) g_red_prof[2] += clock64() - c2;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g_red_prof[3] += sm.gjp[0]; g_red_prof[4] += sm.gjp[1]; g_red_prof[5] += sm.gjp[2];
   }
 }
 

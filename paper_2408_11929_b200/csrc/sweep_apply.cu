@@ -34,6 +34,9 @@
 
 #include "sweep_common.cuh"
 
+#ifndef HELM_GEN_XPF
+#define HELM_GEN_XPF 0     // 1: bulk L2 prefetch of the separator-inverse rows before the gather (C4 t = 1 / 4: 11.09 / 11.84 ms with, 10.55 / 11.02 without: 5 MB of rows per CTA overflow L2 and the issuing warp stalls in front of a barrier)
+#endif
 #ifndef HELM_GEN_XPIPE
 #define HELM_GEN_XPIPE 0   // 1: pipelined L2 prefetch of the separator-inverse rows (wide strips)
 #endif
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         thomas();
         const int K = D.P - 1;
         const long Kw = (long)K * w, xld = x_ld(K, w);
-        if (p < D.P - 1 && tid < 32) {
+        if (HELM_GEN_XPF && p < D.P - 1 && tid < 32) {
           // this CTA's rows of the separator inverse into L2 during the gather
           // (HELM_GEN_XPIPE: only the rows of the mat-vec's first pass; each warp then
           // prefetches its next pass's rows while it computes the current one, so wide
