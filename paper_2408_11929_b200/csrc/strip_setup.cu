@@ -724,7 +724,9 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   cplx* red = ra.red + ra.red_off[s];
   auto scr = [&](int p) { return ra.scratch + ((long)s * ra.P + p) * ra.scratch_stride; };
   const int P = ra.P;
+#if HELM_RED_OLDGJ
   const int i = threadIdx.x / kLPR, h = threadIdx.x % kLPR;
+#endif
   // cp.async the operands of separator k into buffer k & 1: Sinv_{h_k}, X_{k+1}[lo,lo],
   // X_{k+1}[lo,hi] and the couplings of rows h_k, s_k, h_{k+1}
   auto stage = [&](int k) {
@@ -1172,7 +1174,6 @@ __global__ void k_reduced_generic(RedArgs ra) {
   cplx* Tmp = Rprev + (long)ra.wmax * ra.wmax;
   auto Ub = [&](int c, int mode) { return Bidi{mode, ra.cr + band + (long)c * ra.wmax, ra.ne + band + (long)c * ra.wmax}; };
   auto scr = [&](int p) { return ra.scratch + ((long)s * ra.P + p) * ra.scratch_stride; };
-  const Bidi NONE{BD_NONE, nullptr, nullptr};
   const int P = ra.P;
   for (int k = 0; k <= P - 2; ++k) {
     const int hk = ra.seg_hi[k];          // last row of segment k

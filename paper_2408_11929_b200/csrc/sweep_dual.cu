@@ -50,12 +50,6 @@
 #ifndef HELM_DUAL_GSRC
 #define HELM_DUAL_GSRC 1   // 1: the separator-row source is staged into the g area at the pre-actions
 #endif
-#ifndef HELM_DUAL_XPRE
-#define HELM_DUAL_XPRE 0   // experiment: prefetch the next solve's X rows during phase 3 (1 evict_last, 2 normal, 3 evict_first)
-#endif
-#ifndef HELM_DUAL_XPRE_FRAC
-#define HELM_DUAL_XPRE_FRAC 4   // quarters of each X row prefetched early
-#endif
 #ifndef HELM_DUAL_XCH
 #define HELM_DUAL_XCH 4     // 32-column chunks per row in flight in the X mat-vec (4 rows per warp)
 #endif
@@ -69,12 +63,6 @@
 #define HELM_DUAL_FENCE() ((void)0)
 #else
 #define HELM_DUAL_FENCE() __threadfence()
-#endif
-#ifndef HELM_DUAL_BANDPF
-#define HELM_DUAL_BANDPF 0    // (measured 1% slower) 1: the next solve's couplings are prefetched into L2 at the start of phase 3
-#endif
-#ifndef HELM_DUAL_XPF_EARLY
-#define HELM_DUAL_XPF_EARLY 0   // > 0: the X rows are prefetched into L2 by the producer this many phase-1 blocks before the end
 #endif
 #ifndef HELM_DUAL_S2PF
 #define HELM_DUAL_S2PF 2   // two-level panels' L2 prefetch: 0 none, 1 normal priority, 2 evict_first
@@ -291,31 +279,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
           const int ph = e >= m ? 1 : 0, js = e - ph * m;
           const bool up = (pg == 0) == (ph == 0);
           const cplx* src = fbase + (long)(up ? lo + js : hi - js) * pw;
-#if HELM_DUAL_XPF_EARLY > 0
-          if (!XF32 && pg == 0 && e == std::max(m - HELM_DUAL_XPF_EARLY, 0) && p < P - 1) {
-            // this solve's separator-inverse rows into L2 while phase 1 still runs
-            const int w2 = tab[i2].w;
-            if (tab[i2].sep2) {
-              const int* pk = spk;
-              const cplx* pan = tab[i2].sep2 + (long)p * w2 * (D_.sep2_ld1 + D_.sep2_ld2);
-              const uint32_t b1 = (uint32_t)((long)pk[1] * w2 * sizeof(cplx)), b2 = (uint32_t)((long)D_.sep2_M * w2 * sizeof(cplx));
-              for (int r = 0; r < w2 && HELM_DUAL_S2PF; ++r) {
-                if (HELM_DUAL_S2PF == 1) {   // normal eviction priority
-                  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pan + (long)r * D_.sep2_ld1), "r"(b1) : "memory");
-                  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pan + (long)w2 * D_.sep2_ld1 + (long)r * D_.sep2_ld2),
-                               "r"(b2) : "memory");
-                } else {
-                  dprefetch_l2(pan + (long)r * D_.sep2_ld1, b1, polF);
-                  dprefetch_l2(pan + (long)w2 * D_.sep2_ld1 + (long)r * D_.sep2_ld2, b2, polF);
-                }
-              }
-            } else {
-              const long ld = x_ld(K, w2);
-              for (int r = 0; r < w2; ++r)
-                dprefetch_l2(tab[i2].xinv + ((long)p * w2 + r) * ld, (uint32_t)((long)K * w2 * sizeof(cplx)), polF);
-            }
-          }
-#endif
           const int st = f % NST;
           if (f >= (uint32_t)NST) mbar_wait(&empty[pg * NST + st], ((f / NST) - 1) & 1);
 #if HELM_DUAL_EPIREL
@@ -488,14 +451,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     int tdst, side;
     cplx* target;
     epi_target(i, tdst, side, target);
-#if HELM_DUAL_BANDPF
-    if (i + 1 < nsolve && tid >= 32 && tid < 34) {
-      // the next solve's couplings (staged by TMA at its pre-actions) into L2 now
-      const int c0 = lo > 0 ? lo - 1 : 0;
-      const long off = (long)tab[i + 1].s * band_stride + (long)c0 * bw;
-      dprefetch_l2((tid == 32 ? D_.cr : D_.ne) + off, (uint32_t)((hi - c0 + 1) * bw * sizeof(cplx)), pol_last);
-    }
-#endif
     const bool rhs = i + 1 < nsolve;
     const bool cpb = rhs && is_bwd(D_, i + 1) && step_of(D_, i + 1) > 0;
 #if HELM_DUAL_RHS_TMA
@@ -569,7 +524,7 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
     const int qp = prev_side(D_) == 0 ? 0 : w - 1;
     const int qn = next_side(D_) == 0 ? 0 : w - 1;
     const long long csep0 = pclk();
-    if (p < P - 1 && tid < 32 && ((HELM_DUAL_XPF_EARLY == 0 && !HELM_DUAL_XPF_PROD) || XF32)) {
+    if (p < P - 1 && tid < 32 && (!HELM_DUAL_XPF_PROD || XF32)) {
       // (the XF32 variant, or the XPF_PROD = 0 ablation) stream this CTA's rows of the
       // separator inverse into L2 while the all-gather completes
       const long ld = x_ld(K, w);
@@ -1145,22 +1100,6 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
       const long long csn = pclk();
 #ifndef HELM_DUAL_ABL_NONEXT
       stage_next(i);
-#if HELM_DUAL_XPRE
-      // experiment: stream the NEXT solve's separator-inverse rows into L2 during this
-      // solve's phase 3 (the factor stream then mostly hits L2), so the next
-      // separator stage finds part of them resident
-      if (i + 1 < nsolve && p < P - 1 && tid >= 32 * (2 * A.nw - 1)) {
-        const int wn = tab[i + 1].w;
-        const long ld = x_ld(K, wn);
-        const uint32_t bytes = (uint32_t)((long)K * wn * (long)sizeof(cplx) * HELM_DUAL_XPRE_FRAC / 4);
-        const uint64_t pol = HELM_DUAL_XPRE == 1 ? pol_last : (HELM_DUAL_XPRE == 2 ? 0ull : pol_first);
-        for (int r = tid - 32 * (2 * A.nw - 1); r < wn; r += 32) {
-          const cplx* src = tab[i + 1].xinv + ((long)p * wn + r) * ld;
-          if (HELM_DUAL_XPRE == 2) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-          else dprefetch_l2(src, bytes, pol);
-        }
-      }
-#endif
 #else
       if (tid == 0) mbar_expect_tx(&sbar[0], 0);
 #endif
