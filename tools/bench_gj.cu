@@ -1,0 +1,83 @@
+// bench_gj.cu -- the register-row Gauss-Jordan (row_gj.cuh) in isolation: cycles
+// per 35 x 35 complex inversion, one CTA alone (latency) and a full GPU of CTAs
+// (throughput), for row_invert (2 threads per row, normalised pivot row) and
+// row_invert_g<LPR> (raw pivot row, multipliers through shared memory).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr \
+//        -I paper_2408_11929_b200/csrc -I include tools/bench_gj.cu -o tools/bench_gj
+#include <cstdio>
+#include "row_gj.cuh"
+
+constexpr int W = 35, NMAT = 64;
+
+__device__ cplx hash_entry(int m, int i, int j) {
+  unsigned x = (unsigned)(m * 1315423911u) ^ (unsigned)(i * 2654435761u) ^ (unsigned)(j * 97531u);
+  x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+  const double r = (double)(x & 0xffff) / 65536.0 - 0.5, q = (double)((x >> 16) & 0xffff) / 65536.0 - 0.5;
+  return cmk(r + (i == j ? 4.0 : 0.0), q);
+}
+
+template <int MODE>   // 0: row_invert, k > 0: row_invert_g<k>
+__global__ void k_bench(long long* out, double* sink) {
+  __shared__ RowSmem sm;
+  if (threadIdx.x == 0) sm.gjp[0] = sm.gjp[1] = sm.gjp[2] = 0;
+  __syncthreads();
+  constexpr int LPR = MODE == 0 ? kLPR : MODE;
+  constexpr int HW = kRowW / LPR;
+  const int i = threadIdx.x / LPR, h = threadIdx.x % LPR;
+  double acc = 0;
+  long long t0 = clock64();
+  for (int m = 0; m < NMAT; ++m) {
+    cplx a[HW];
+#pragma unroll
+    for (int jj = 0; jj < HW; ++jj) {
+      const int col = LPR * jj + h;
+      a[jj] = (i < W && col < W) ? hash_entry(m + blockIdx.x, i, col) : cmk(0, 0);
+    }
+    int bad;
+    if constexpr (MODE == 0) bad = row_invert(a, W, sm);
+    else bad = row_invert_g<LPR>(a, W, sm);
+    acc += bad + sm.mat[(threadIdx.x % W) * kRowW].x;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) {
+    out[blockIdx.x] = t1 - t0;
+    if (blockIdx.x == 0) { out[gridDim.x] = sm.gjp[0]; out[gridDim.x + 1] = sm.gjp[1]; out[gridDim.x + 2] = sm.gjp[2]; }
+  }
+  if (acc == 12345.0) sink[0] = acc;
+}
+
+template <int MODE>
+void run(const char* name, int threads, int ctas) {
+  long long* d;
+  double* s;
+  cudaMalloc(&d, sizeof(long long) * (ctas + 3));
+  cudaMalloc(&s, 8);
+  k_bench<MODE><<<ctas, threads>>>(d, s);
+  cudaDeviceSynchronize();
+  k_bench<MODE><<<ctas, threads>>>(d, s);
+  cudaDeviceSynchronize();
+  long long* h = new long long[ctas + 3];
+  cudaMemcpy(h, d, sizeof(long long) * (ctas + 3), cudaMemcpyDeviceToHost);
+  double mean = 0;
+  for (int c = 0; c < ctas; ++c) mean += h[c];
+  mean /= ctas;
+  printf("%-22s threads %3d ctas %4d: %8.0f cycles per inversion per CTA (%.0f per pivot)%s", name, threads, ctas,
+         mean / NMAT, mean / NMAT / W, cudaGetLastError() == cudaSuccess ? "" : "  [error]");
+  if (h[ctas] + h[ctas + 1] + h[ctas + 2] > 0)   // (-DHELM_GJ_PROF, row_invert_g only; thread 0 of CTA 0)
+    printf("  | per pivot: search %.0f publish %.0f update %.0f", h[ctas] / (2.0 * NMAT * W), h[ctas + 1] / (2.0 * NMAT * W),
+           h[ctas + 2] / (2.0 * NMAT * W));
+  printf("\n");
+  delete[] h;
+  cudaFree(d);
+  cudaFree(s);
+}
+
+int main() {
+  for (int ctas : {1, 148 * 5}) {
+    run<0>("row_invert (LPR 2)", 96, ctas);
+    run<2>("row_invert_g<2>", 96, ctas);
+    run<4>("row_invert_g<4>", 160, ctas);
+    run<9>("row_invert_g<9>", 352, ctas);
+  }
+  return 0;
+}
