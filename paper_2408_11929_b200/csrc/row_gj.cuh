@@ -256,3 +256,4 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
   return 0;
 }
 
+

@@ -5,6 +5,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr \
 //        -I paper_2408_11929_b200/csrc -I include tools/bench_gj.cu -o tools/bench_gj
 #include <cstdio>
+#include <cstring>
+#include <cmath>
 #include "row_gj.cuh"
 
 constexpr int W = 35, NMAT = 64;
@@ -16,12 +18,12 @@ __device__ cplx hash_entry(int m, int i, int j) {
   return cmk(r + (i == j ? 4.0 : 0.0), q);
 }
 
-template <int MODE>   // 0: row_invert, k > 0: row_invert_g<k>
-__global__ void k_bench(long long* out, double* sink) {
+template <int MODE>   // 0: row_invert, k > 0: row_invert_g<k>, -1: row_invert_p
+__global__ void k_bench(long long* out, double* sink, cplx* inv0) {
   __shared__ RowSmem sm;
   if (threadIdx.x == 0) sm.gjp[0] = sm.gjp[1] = sm.gjp[2] = 0;
   __syncthreads();
-  constexpr int LPR = MODE == 0 ? kLPR : MODE;
+  constexpr int LPR = MODE <= 0 ? kLPR : MODE;
   constexpr int HW = kRowW / LPR;
   const int i = threadIdx.x / LPR, h = threadIdx.x % LPR;
   double acc = 0;
@@ -36,6 +38,11 @@ __global__ void k_bench(long long* out, double* sink) {
     int bad;
     if constexpr (MODE == 0) bad = row_invert(a, W, sm);
     else bad = row_invert_g<LPR>(a, W, sm);
+    if (m == 0) {   // the first inverse, for the comparison of the variants
+      __syncthreads();
+      for (int e = threadIdx.x; e < W * W; e += blockDim.x) inv0[(long)blockIdx.x * W * W + e] = sm.mat[(e / W) * kRowW + e % W];
+      __syncthreads();
+    }
     acc += bad + sm.mat[(threadIdx.x % W) * kRowW].x;
   }
   long long t1 = clock64();
@@ -52,9 +59,11 @@ void run(const char* name, int threads, int ctas) {
   double* s;
   cudaMalloc(&d, sizeof(long long) * (ctas + 3));
   cudaMalloc(&s, 8);
-  k_bench<MODE><<<ctas, threads>>>(d, s);
+  cplx* inv;
+  cudaMalloc(&inv, sizeof(cplx) * W * W * ctas);
+  k_bench<MODE><<<ctas, threads>>>(d, s, inv);
   cudaDeviceSynchronize();
-  k_bench<MODE><<<ctas, threads>>>(d, s);
+  k_bench<MODE><<<ctas, threads>>>(d, s, inv);
   cudaDeviceSynchronize();
   long long* h = new long long[ctas + 3];
   cudaMemcpy(h, d, sizeof(long long) * (ctas + 3), cudaMemcpyDeviceToHost);
@@ -67,6 +76,15 @@ void run(const char* name, int threads, int ctas) {
     printf("  | per pivot: search %.0f publish %.0f update %.0f", h[ctas] / (2.0 * NMAT * W), h[ctas + 1] / (2.0 * NMAT * W),
            h[ctas + 2] / (2.0 * NMAT * W));
   printf("\n");
+  static cplx* ref = nullptr;
+  cplx* hi = new cplx[W * W];
+  cudaMemcpy(hi, inv, sizeof(cplx) * W * W, cudaMemcpyDeviceToHost);
+  if (!ref) { ref = new cplx[W * W]; memcpy(ref, hi, sizeof(cplx) * W * W); }
+  double md = 0;
+  for (int e = 0; e < W * W; ++e) md = fmax(md, fabs(hi[e].x - ref[e].x) + fabs(hi[e].y - ref[e].y));
+  printf("    max |inv - inv(row_invert)| = %.3e\n", md);
+  delete[] hi;
+  cudaFree(inv);
   delete[] h;
   cudaFree(d);
   cudaFree(s);
