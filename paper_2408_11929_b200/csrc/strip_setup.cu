@@ -1010,9 +1010,11 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   // k >= j, of its column block and mirrors them into (j, k), so the backward
   // recurrence stops at k = j (a third less work than the full column block)
   auto mirror = [&](int k, const cplx* blk) {   // block (j, k) = block(k, j)^T
+    // consecutive threads write consecutive entries of a row of block (j, k) (coalesced;
+    // the transposed reads are from shared memory)
     for (int e = threadIdx.x; e < w2; e += NT) {
-      const int r = rowof(e), c = e - r * w;
-      X[((long)j * w + c) * ld + (long)k * w + r] = blk[e];
+      const int c = rowof(e), r = e - c * w;
+      X[((long)j * w + c) * ld + (long)k * w + r] = blk[r * w + c];
     }
   };
   // forward: k = j: Rinv_j; k > j: Z_k = -G_k Z_{k-1}
@@ -1069,8 +1071,8 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
   auto mirror = [&](int k) {
     __syncthreads();
     const cplx* b = blk(k);
-    for (long e = threadIdx.x; e < w2; e += blockDim.x) {
-      const long r = e / w, c = e % w;
+    for (long e = threadIdx.x; e < w2; e += blockDim.x) {   // (coalesced writes, strided L1/L2 reads)
+      const long c = e / w, r = e % w;
       X[((long)j * w + c) * ld + (long)k * w + r] = b[r * ld + c];
     }
   };

@@ -81,6 +81,8 @@ if os.environ.get("HELM_CYCLES"):
         print(f"  balanced separator stage (thread 0, per solve): pass A {sel[:,15].mean()/63:.0f}  pass B {sel[:,11].mean()/63:.0f}")
         print(f"  pre-actions (thread 0, per solve): other group's tail {sel[:,9].mean()/63:.0f}  through epilogue {sel[:,10].mean()/63:.0f}  "
               f"coupling wait (slot 15) {sel[:,15].mean()/63:.0f}  stage_bands issue {sel[:,22].mean()/63:.0f}  +staging waits {sel[:,23].mean()/63:.0f}")
+        print(f"  pre-action tail (thread 0, per solve): seg_rhs {sel[:,27].mean()/63:.0f}  +source staging issue {sel[:,28].mean()/63:.0f}  "
+              f"+barrier {sel[:,29].mean()/63:.0f}")
         P0 = info[0].n_segments
         d0 = b[:P0]
         print("  two-level per CTA of direction 0 (per solve): wait coarse / round 1 / round 2: " +
