@@ -197,19 +197,41 @@ __device__ inline int gj_invert(cplx* A, int w, int* piv, cplx* col, double* red
     }
     __syncthreads();
     // eliminate column k from all other rows: a warp per row, lanes along the
-    // row (no index division, contiguous shared-memory access)
+    // row (no index division, contiguous shared-memory access); the pivot row is
+    // held in registers (w <= 128: four entries per lane), read once per pivot
     {
       const int lane = tid & 31, nwarp = (int)(blockDim.x >> 5);
-      for (int i = tid >> 5; i < w; i += nwarp) {
-        if (i == k) continue;
-        const cplx f = col[i];
-        for (int j = lane; j < w; j += 32) {
-          const long e = (long)i * w + j;
-          cplx a = (j == k) ? cmk(0.0, 0.0) : A[e];
-          const cplx r = A[k * w + j];
-          a.x -= f.x * r.x - f.y * r.y;
-          a.y -= f.x * r.y + f.y * r.x;
-          A[e] = a;
+      if (w <= 128) {
+        cplx rr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rr[u] = lane + 32 * u < w ? A[k * w + lane + 32 * u] : cmk(0.0, 0.0);
+        for (int i = tid >> 5; i < w; i += nwarp) {
+          if (i == k) continue;
+          const cplx f = col[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = lane + 32 * u;
+            if (j < w) {
+              const long e = (long)i * w + j;
+              cplx a = (j == k) ? cmk(0.0, 0.0) : A[e];
+              a.x -= f.x * rr[u].x - f.y * rr[u].y;
+              a.y -= f.x * rr[u].y + f.y * rr[u].x;
+              A[e] = a;
+            }
+          }
+        }
+      } else {
+        for (int i = tid >> 5; i < w; i += nwarp) {
+          if (i == k) continue;
+          const cplx f = col[i];
+          for (int j = lane; j < w; j += 32) {
+            const long e = (long)i * w + j;
+            cplx a = (j == k) ? cmk(0.0, 0.0) : A[e];
+            const cplx r = A[k * w + j];
+            a.x -= f.x * r.x - f.y * r.y;
+            a.y -= f.x * r.y + f.y * r.x;
+            A[e] = a;
+          }
         }
       }
     }
