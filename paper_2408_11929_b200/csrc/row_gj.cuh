@@ -21,7 +21,7 @@ static_assert(kRowW % kLPR == 0 && kRowW * kLPR <= kRowThreads, "row layout");
 struct RowSmem {
   cplx mat[kRowW * kRowW];    // natural-order inverse of the current block / Y
   cplx tmat[kRowW * kRowW];   // U_c Y (kind 0, X[lo,hi] chain)
-  cplx prow[kRowW];
+  cplx prow[2 * kRowW];       // row_invert_r: index 2 (slot + rot) + h, rot < kRowHW
   cplx pcol[2][kRowW];        // row_invert_g: pivot-column entries (multipliers), by step parity
   cplx pdinv;                 // row_invert_g: 1 / pivot
   unsigned redk[12];
@@ -256,4 +256,96 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
   return 0;
 }
 
-
+// row_invert with rotating register slots (no register selects): during the
+// pass of pivot pairs m0 .. m0 + UP - 1, slot jj holds column LPR ((jj + m0) mod
+// HW) + h, so the pivot column of pivot k = LPR (m0 + u) + kh is the
+// compile-time slot u; after each pass the slots rotate by UP (HW / UP passes
+// restore the natural order).  The pivot row is published at index
+// LPR (jj + m0) + h of the doubled sm.prow (no wrap-around arithmetic).  Same
+// pivot rule and elementary operations as row_invert: bitwise the same inverse.
+#ifndef HELM_ROW_UP
+#define HELM_ROW_UP 3
+#endif
+template <int UP>
+__device__ __forceinline__ int row_invert_r(cplx (&a)[kRowHW], int w, RowSmem& sm) {
+  static_assert(kRowHW % UP == 0, "the slots rotate by UP");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i = tid / kLPR, h = tid % kLPR;
+  const bool active = i < w;
+  bool used = false;
+  int kstep = 0;
+#pragma unroll 1
+  for (int m0 = 0; m0 < kRowHW; m0 += UP) {
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+#pragma unroll
+      for (int kh = 0; kh < kLPR; ++kh) {
+        const int k = kLPR * (m0 + u) + kh;
+        if (k < w) {
+          const cplx mine = a[u];
+          const double mag = (active && !used && h == kh) ? cabs2(mine) : 0.0;
+          const unsigned key = (active && !used && h == kh) ? (unsigned)__double2hiint(mag) + 1u : 0u;
+          const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+          const unsigned who = __ballot_sync(0xffffffffu, key == kmax);
+          if (lane == 0 && warp < kRowWarps) { sm.redk[warp] = kmax; sm.redi[warp] = warp * (32 / kLPR) + (__ffs(who) - 1) / kLPR; }
+          __syncthreads();
+          unsigned k0 = sm.redk[0];
+          int p = sm.redi[0];
+#pragma unroll
+          for (int q = 1; q < kRowWarps; ++q)
+            if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
+          if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
+          cplx akk;
+          {
+            const int src = (lane & ~(kLPR - 1)) | kh;
+            akk.x = __shfl_sync(0xffffffffu, mine.x, src);
+            akk.y = __shfl_sync(0xffffffffu, mine.y, src);
+          }
+          cplx* prow = sm.prow + kLPR * m0 + h;
+          if (i == p) {
+            const cplx dinv = cinv(akk);
+#pragma unroll
+            for (int jj = 0; jj < kRowHW; ++jj) {
+              const cplx v = (jj == u && h == kh) ? cmk(1.0, 0.0) : a[jj];
+              a[jj] = cmul(v, dinv);
+              prow[kLPR * jj] = a[jj];
+            }
+            if (h == kh) prow[kLPR * u] = cmk(1.0 + dinv.x, dinv.y);
+            used = true;
+            kstep = k;
+            if (h == 0) sm.pivrow[k] = p;
+          }
+          __syncthreads();
+          if (active && i != p) {
+            const cplx f = akk;
+#pragma unroll
+            for (int jj = 0; jj < kRowHW; ++jj) {   // a -= f r, four fused multiply-adds
+              const cplx r = prow[kLPR * jj];
+              a[jj].x = fma(-f.x, r.x, a[jj].x);
+              a[jj].x = fma(f.y, r.y, a[jj].x);
+              a[jj].y = fma(-f.x, r.y, a[jj].y);
+              a[jj].y = fma(-f.y, r.x, a[jj].y);
+            }
+          }
+        }
+      }
+    }
+    cplx t[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) t[u] = a[u];
+#pragma unroll
+    for (int jj = 0; jj + UP < kRowHW; ++jj) a[jj] = a[jj + UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) a[kRowHW - UP + u] = t[u];
+  }
+  __syncthreads();   // pivrow complete; everyone is done reading mat from the previous block
+  if (active) {
+#pragma unroll
+    for (int jj = 0; jj < kRowHW; ++jj) {
+      const int j = kLPR * jj + h;
+      if (j < w) sm.mat[kstep * kRowW + sm.pivrow[j]] = a[jj];
+    }
+  }
+  __syncthreads();
+  return 0;
+}

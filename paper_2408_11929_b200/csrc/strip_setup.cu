@@ -318,6 +318,14 @@ __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem
 #ifndef HELM_FAC_G
 #define HELM_FAC_G 0        // 1: k_factor_rows uses row_invert_g (raw pivot-row broadcast)
 #endif
+#ifndef HELM_FAC_ROT
+#define HELM_FAC_ROT 0      // 1: rotating register slots (row_invert_r: 1.6x per CTA alone, slower in the setup at the register cap)
+#endif
+__device__ __forceinline__ int fac_invert(cplx (&a)[kRowHW], int w, RowSmem& sm) {
+  if (HELM_FAC_G) return row_invert_g<kLPR>(a, w, sm);
+  if (HELM_FAC_ROT) return row_invert_r<HELM_ROW_UP>(a, w, sm);
+  return row_invert(a, w, sm);
+}
 #ifndef HELM_FAC_MINB
 #define HELM_FAC_MINB 5   // 5 CTAs per SM (a few spills) beat 4 without
 #endif
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
   if (kind == 0) {
     for (int c = lo; c <= hi; ++c) {
       row_schur(a, w, B(fa.dg, c), B(fa.al, c), B(fa.cr, c - 1), B(fa.ne, c - 1), c > lo, true, sm);
-      if (HELM_FAC_G ? row_invert_g<kLPR>(a, w, sm) : row_invert(a, w, sm)) {
+      if (fac_invert(a, w, sm)) {
         if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
         return;
       }
@@ -414,7 +422,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
   } else {
     for (int c = hi; c >= lo; --c) {
       row_schur(a, w, B(fa.dg, c), B(fa.al, c), B(fa.cr, c), B(fa.ne, c), c < hi, false, sm);
-      if (HELM_FAC_G ? row_invert_g<kLPR>(a, w, sm) : row_invert(a, w, sm)) {
+      if (fac_invert(a, w, sm)) {
         if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
         return;
       }
