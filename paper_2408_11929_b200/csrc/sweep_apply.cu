@@ -37,6 +37,15 @@
 #ifndef HELM_GEN_XPF
 #define HELM_GEN_XPF 0     // 1: bulk L2 prefetch of the separator-inverse rows before the gather (C4 t = 1 / 4: 11.09 / 11.84 ms with, 10.55 / 11.02 without: 5 MB of rows per CTA overflow L2 and the issuing warp stalls in front of a barrier)
 #endif
+#ifndef HELM_GEN_XUN
+#define HELM_GEN_XUN 1     // iterations of the separator mat-vec's column loop unrolled (4 * XCH loads per lane each)
+#endif
+constexpr int kGenXun = HELM_GEN_XUN;
+#ifndef HELM_GEN_XCH
+#define HELM_GEN_XCH 6     // 32-column chunks per row and iteration (4 rows per warp: 24 loads per lane in flight;
+                           // C4 t = 1: XCH/XUN 4/1 8.96, 4/2 8.13-8.77, 4/4 8.12, 8/1 8.31, 6/1 8.03 ms)
+#endif
+constexpr int kGenXch = HELM_GEN_XCH;
 #ifndef HELM_GEN_XPIPE
 #define HELM_GEN_XPIPE 0   // 1: pipelined L2 prefetch of the separator-inverse rows (wide strips)
 #endif
@@ -65,9 +74,12 @@ __device__ __forceinline__ const cplx* ring_peek(const Ring& rg, uint32_t k) {
   mbar_wait(&rg.full[sidx], (k / rg.nstage) & 1);
   return rg.stage + (long)sidx * rg.stage_elems;
 }
-// consumers: after cbar(), release `count` consumed tiles
+// consumers: release `count` consumed tiles.  Every consumer warp arrives once per
+// stage (the empty barriers are initialised with the number of consumer warps), so a
+// warp that is done with a tile frees its share without a CTA barrier.
 __device__ __forceinline__ void ring_release(Ring& rg, int count) {
-  if (threadIdx.x == 0)
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0)
     for (int c = 0; c < count; ++c) mbar_arrive(&rg.empty[(rg.kc + c) % rg.nstage]);
   rg.kc += count;
 }
@@ -180,10 +192,22 @@ struct StepIO {
   cplx* tAn; cplx* tBn;               // next inputs
 };
 
+// KP: complex entries per lane and block row (8 lanes per row: KP >= ceil(w / 8)).
+// The combined input t = tA + tB is read once per block step into registers and
+// serves every 36-row tile of the block; the tiles need no CTA barrier between
+// them (each warp releases its share of a ring stage when it is done with it), only
+// the end of the step does (the writers' next input).
+template <int KP>
 __device__ __forceinline__ void block_step(Ring& rg, int w, int ncons, const StepIO& io, Prof& pf) {
   const int tid = threadIdx.x;
   const int ri = tid >> 3, q = tid & 7;
   const int nt = ntile_of(w, rg.R_t);
+  cplx tv[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    const int k = q + 8 * i;
+    tv[i] = k < w ? cadd(io.tA[k], io.tB[k]) : cmk(0, 0);
+  }
   for (int tt = 0; tt < nt; ++tt) {
     const int r0 = tt * rg.R_t;
     const int rows = min(rg.R_t, w - r0);
@@ -202,17 +226,22 @@ __device__ __forceinline__ void block_step(Ring& rg, int w, int ncons, const Ste
     long long c0 = clock64();
     const cplx* B = ring_peek(rg, rg.kc);
     long long c1 = clock64();
-    cplx acc0 = cmk(0, 0), acc1 = cmk(0, 0);
+    cplx a0 = cmk(0, 0), a1 = cmk(0, 0), a2 = cmk(0, 0), a3 = cmk(0, 0);
     if (ri < rows) {
-      const cplx* Br = B + ri * w;
-      int k = q;
-      for (; k + 8 < w; k += 16) {
-        cfma(acc0, Br[k], cadd(io.tA[k], io.tB[k]));
-        cfma(acc1, Br[k + 8], cadd(io.tA[k + 8], io.tB[k + 8]));
+      const cplx* Br = B + ri * w + q;
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        if (q + 8 * i < w) {
+          const cplx b = Br[8 * i];
+          if ((i & 3) == 0) cfma(a0, b, tv[i]);
+          else if ((i & 3) == 1) cfma(a1, b, tv[i]);
+          else if ((i & 3) == 2) cfma(a2, b, tv[i]);
+          else cfma(a3, b, tv[i]);
+        }
       }
-      if (k < w) cfma(acc0, Br[k], cadd(io.tA[k], io.tB[k]));
     }
-    cplx acc = cadd(acc0, acc1);
+    cplx acc = cadd(cadd(a0, a1), cadd(a2, a3));
+    ring_release(rg, 1);   // this warp is done with the tile (its entries are in registers)
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
@@ -232,11 +261,11 @@ __device__ __forceinline__ void block_step(Ring& rg, int w, int ncons, const Ste
       }
     }
     long long c2 = clock64();
-    cbar(ncons);
-    ring_release(rg, 1);
-    long long c3 = clock64();
-    pf.peek += c1 - c0; pf.comp += c2 - c1; pf.bar += c3 - c2; pf.steps++;
+    pf.peek += c1 - c0; pf.comp += c2 - c1; pf.steps++;
   }
+  long long c2 = clock64();
+  cbar(ncons);
+  pf.bar += clock64() - c2;
 }
 
 // two-block step for the reducer forward chain: out = A*u - B*v  (tile-interleaved A, B)
@@ -278,6 +307,7 @@ __device__ __forceinline__ void block_step2(Ring& rg, int w, int ncons, const cp
 
 // ------------------------------------------------------------------ kernel
 // blockDim = ncons consumer threads (8 lanes per block row) + 1 producer warp.
+template <int KP>
 __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ ApplyArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -319,7 +349,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
   if (tid == 0) {
     for (int s = 0; s < A.nstage; ++s) {
       mbar_init(&rg.full[s], 1);
-      mbar_init(&rg.empty[s], 1);
+      mbar_init(&rg.empty[s], ncons >> 5);   // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -421,7 +451,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
           } else {
             io.next = 0; io.bn = nullptr; io.crn = nullptr; io.nen = nullptr;
           }
-          block_step(rg, w, ncons, io, pf);
+          block_step<KP>(rg, w, ncons, io, pf);
           cur ^= 1;
         }
         for (int c = hi - 1; c >= lo; --c) {  // backward
@@ -435,7 +465,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
           } else {
             io.next = 0; io.bn = nullptr; io.crn = nullptr; io.nen = nullptr;
           }
-          block_step(rg, w, ncons, io, pf);
+          block_step<KP>(rg, w, ncons, io, pf);
           cur ^= 1;
         }
       };
@@ -545,6 +575,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         cbar(ncons);
         // x_p = X_p g: 4 rows per warp, 16 independent loads in flight per lane
         const int cw = tid >> 5, ncw = ncons >> 5, lane = tid & 31;
+        const long long cx0 = clock64();
         if (p < D.P - 1) {
           for (int rb = 4 * cw; rb < w; rb += 4 * ncw) {
             const cplx* Xr[4];
@@ -559,18 +590,19 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
                                D.xinv + D.xinv_off[s] + ((long)p * w + rb + 4 * ncw + lane) * xld),
                            "r"((uint32_t)(Kw * (long)sizeof(cplx))) : "memory");
             cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-#pragma unroll 2
-            for (long jj = lane; jj < Kw; jj += 128) {   // two iterations' loads in flight
-              cplx xv[4][4], gv[4];
+#pragma unroll kGenXun
+            for (long jj = lane; jj < Kw; jj += 32 * kGenXch) {   // kGenXun iterations' loads in flight
+              cplx xv[4][kGenXch], gv[kGenXch];
 #pragma unroll
-              for (int v = 0; v < 4; ++v) {
+              for (int v = 0; v < kGenXch; ++v) {
                 const bool in = jj + 32 * v < Kw;
-                gv[v] = in ? g[jj + 32 * v] : cmk(0, 0);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) xv[u][v] = (ok[u] && in) ? ldcg(Xr[u] + jj + 32 * v) : cmk(0, 0);
               }
 #pragma unroll
-              for (int v = 0; v < 4; ++v)
+              for (int v = 0; v < kGenXch; ++v) gv[v] = jj + 32 * v < Kw ? g[jj + 32 * v] : cmk(0, 0);
+#pragma unroll
+              for (int v = 0; v < kGenXch; ++v)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) cfma(acc[u], xv[u][v], gv[v]);
             }
@@ -590,6 +622,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
           if (p == D.P - 1) xhi[e] = cmk(0, 0);
         }
         cbar(ncons);
+        pf.xmv += clock64() - cx0;
         // publish x_p (gather row and the next solve's corrections), take x_{p-1}
         if (p < D.P - 1) {
           for (int e = tid; e < w; e += ncons) D.xs[par * xss + (long)p * D.wmax + e] = xhi[e];
@@ -736,7 +769,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
         io.tB = tbuf;  // zeros
         io.out = z + k * D.wmax; io.ybase = z + k * D.wmax; io.mode = 1;
         io.next = 0; io.bn = nullptr; io.crn = nullptr; io.nen = nullptr; io.tAn = nullptr; io.tBn = nullptr;
-        block_step(rg, w, ncons, io, pf);
+        block_step<KP>(rg, w, ncons, io, pf);
       }
       // (d) publish x_sep
       for (int e = tid; e < K * w; e += ncons) {
@@ -762,7 +795,7 @@ __global__ void __launch_bounds__(320, 1) k_sweep_apply(const __grid_constant__ 
   if (A.prof && tid == 0) {
     long long* o = A.prof + (long)blockIdx.x * 8;
     o[0] = pf.peek; o[1] = pf.comp; o[2] = pf.bar; o[3] = pf.steps; o[4] = pf.xwait;
-    o[5] = clock64() - t_start; o[6] = reducer ? 1 : 0; o[7] = d;
+    o[5] = clock64() - t_start; o[6] = reducer ? 1 : 0; o[7] = pf.xmv;   // X mat-vec cycles (segment CTAs)
   }
 }
 
@@ -886,7 +919,7 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   int nsolve_max = 1;
   for (int d = 0; d < t; ++d) nsolve_max = std::max(nsolve_max, dirs[d]->is_double ? 2 * dirs[d]->N - 1 : dirs[d]->N);
   nsolve_max = (nsolve_max + 1) & ~1;  // keeps the vector areas after the table 16-byte aligned
-  const long tail = sizeof(cplx) * (7L * wmax + 2L * pmax + 8) + 24L * nsolve_max + 32;
+  const long tail = sizeof(cplx) * (7L * wmax + 2L * pmax + 8) + (long)sizeof(SolveTab) * nsolve_max + 32;
   const long stage_bytes = sizeof(cplx) * stage_elems;
   int vec_global = 0;
   long fixed = 256 + tail + sizeof(cplx) * 4 * vec_elems;
@@ -963,12 +996,20 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
     e = cudaMemsetAsync(D.cnt, 0, sizeof(unsigned) * (2 + h->P), st);
     if (e != cudaSuccess) break;
   }
+  // entries per lane and block row (8 lanes per row): the instantiation for the widest strip of the batch
+  const void* kfun = wmax <= 40 ? (const void*)k_sweep_apply<5>
+                     : wmax <= 104 ? (const void*)k_sweep_apply<13> : (const void*)k_sweep_apply<15>;
+  if (wmax > 120) {
+    helm_set_error("sweep_apply: strips wider than 120 nodes are not supported (w=%d)", wmax);
+    cudaFreeAsync(scratch, st);
+    return HELM_EINVAL;
+  }
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_sweep_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 0, occ = 0;
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_apply, threads, smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfun, threads, smem);
   if (e == cudaSuccess && occ * nsm < ctas) {
     helm_set_error("sweep_apply: %d CTAs cannot be co-resident (%d SMs x %d); reduce n_segments", ctas, nsm, occ);
     cudaFreeAsync(scratch, st);
@@ -976,7 +1017,7 @@ int sweep_apply_dev(const helm_sweep_t* dirs, int t, const cplx* Rdev, long ldr,
   }
   if (e == cudaSuccess) {
     void* args[] = {(void*)&A};
-    e = cudaLaunchCooperativeKernel((void*)k_sweep_apply, dim3(ctas), dim3(threads), args, smem, st);
+    e = cudaLaunchCooperativeKernel(kfun, dim3(ctas), dim3(threads), args, smem, st);
     g_helm_launches++;
   }
   cudaFreeAsync(scratch, st);

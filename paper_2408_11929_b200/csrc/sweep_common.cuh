@@ -53,7 +53,7 @@ struct ApplyArgs {
 
 // per-thread profiling accumulators (thread 0 reports)
 struct Prof {
-  long long peek = 0, comp = 0, bar = 0, steps = 0, xwait = 0;
+  long long peek = 0, comp = 0, bar = 0, steps = 0, xwait = 0, xmv = 0;
 };
 
 // ------------------------------------------------------------------ PTX helpers

@@ -100,4 +100,5 @@ if os.environ.get("HELM_CYCLES"):
               f"steps {(sel[:,5]-sel[:,0]-sel[:,1]).mean():.3e} -> {(sel[:,5]-sel[:,0]-sel[:,1]).mean()/st:.0f} cyc/step")
         print(f"{'reducer' if role else 'segment'} CTAs={len(sel)} steps={st:.0f} total={sel[:,5].mean():.3e} cyc | "
               f"per step: pre|peek {sel[:,0].mean()/st:.0f} comp {sel[:,1].mean()/st:.0f} bar {sel[:,2].mean()/st:.0f} | "
-              f"xwait total {sel[:,4].mean():.3e} ({sel[:,4].mean()/sel[:,5].mean()*100:.1f}%)")
+              f"xwait total {sel[:,4].mean():.3e} ({sel[:,4].mean()/sel[:,5].mean()*100:.1f}%) | "
+              f"X mat-vec total {sel[:,7].mean():.3e} ({sel[:,7].mean()/sel[:,5].mean()*100:.1f}%)")
