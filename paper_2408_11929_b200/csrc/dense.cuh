@@ -109,6 +109,61 @@ __device__ inline void blk_mm_tiled(cplx* C, int ldc, const cplx* A, int lda, bo
   __syncthreads();
 }
 
+// FP64 tensor-core variant: C (+)= alpha * op(A) B on 8 x 8 output tiles, one warp per
+// tile, k in steps of 4 (mma.sync.m8n8k4.f64: lane l holds A[l/4][l%4], B[l%4][l/4] and
+// C[l/4][2 (l%4) + {0, 1}]).  The complex product is four real ones on the interleaved
+// operands: Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br; one 16-byte operand load per lane and
+// matrix feeds all four (the 4 x 4 register-tiled DFMA product needs eight loads per 16
+// complex products and ran at ~0.2 of the FP64 peak in the setup kernels; tools/bench_dmma.cu:
+// a 35^3 complex product takes 3.5-4.0 k SM-cycles from shared memory, the tensor pipe's
+// peak is 37.2 TFLOP/s).  Every warp of the CTA must call it (whole warps execute the mma).
+// Rows / columns / k >= w read as zero.  C must not alias A or B.  Ends with __syncthreads().
+// A variant with two tiles and two k-split accumulator sets per warp measured slower.
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ inline void blk_mm_dmma(cplx* C, int ldc, const cplx* A, int lda, bool transA, const cplx* B, int ldb,
+                                   int w, double alpha, bool accumulate) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (w + 7) >> 3;
+  const int lr = lane >> 2, lk = lane & 3;
+  for (int t = warp; t < nt * nt; t += nw) {
+    const int i0 = (t / nt) * 8, j0 = (t % nt) * 8;
+    const int ia = i0 + lr, jb = j0 + lr;
+    const bool aok = ia < w, bok = jb < w;
+    const cplx* Ap = transA ? A + ia : A + (long)ia * lda;
+    const long as = transA ? lda : 1;
+    const cplx* Bp = B + jb;
+    double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll 3
+    for (int k0 = 0; k0 < w; k0 += 4) {
+      const int k = k0 + lk;
+      const bool kok = k < w;
+      const cplx a = (aok && kok) ? Ap[(long)k * as] : cmk(0, 0);
+      const cplx b = (bok && kok) ? Bp[(long)k * ldb] : cmk(0, 0);
+      dmma_884(cr0, cr1, a.x, b.x);
+      dmma_884(cr0, cr1, -a.y, b.y);
+      dmma_884(ci0, ci1, a.x, b.y);
+      dmma_884(ci0, ci1, a.y, b.x);
+    }
+    if (aok) {
+      const int j = j0 + 2 * lk;
+      cplx* Cp = C + (long)ia * ldc + j;
+      if (j < w) {
+        const cplx v = cmk(alpha * cr0, alpha * ci0);
+        Cp[0] = accumulate ? cadd(Cp[0], v) : v;
+      }
+      if (j + 1 < w) {
+        const cplx v = cmk(alpha * cr1, alpha * ci1);
+        Cp[1] = accumulate ? cadd(Cp[1], v) : v;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // 2 x 2-tiled variant for large CTAs (324 tiles at w = 35)
 __device__ inline void blk_mm_tiled2(cplx* C, int ldc, const cplx* A, int lda, bool transA, const cplx* B, int ldb,
                                      int w, double alpha, bool accumulate) {

@@ -315,6 +315,9 @@ __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem
   }
 }
 
+#ifndef HELM_SETUP_DMMA
+#define HELM_SETUP_DMMA 1   // block products of the setup kernels on the FP64 tensor cores (dense.cuh blk_mm_dmma)
+#endif
 #ifndef HELM_FAC_G
 #define HELM_FAC_G 0        // 1: k_factor_rows uses row_invert_g (raw pivot-row broadcast)
 #endif
@@ -980,6 +983,12 @@ __global__ void k_reduced_generic(RedArgs ra) {
 // (strip, column block j):  Z_j = Rinv_j E_j, Z_k = -G_k Z_{k-1} (k > j),
 // X_{K-1} = Z_{K-1}, X_k = Z_k - F_k X_{k+1}.  Storage per strip:
 // X[k] is w x (K w) row-major (the rows of separator k), contiguous.
+// Shared-memory leading dimensions of the tensor-core product's operands (dense.cuh
+// blk_mm_dmma): A fragments (2 rows x 4 k per quarter-warp) are conflict-free when
+// lda = 4 mod 8, B fragments (4 k x 2 columns) when ldb = 2 or 6 mod 8.
+__host__ __device__ inline int dmma_lda(int w) { return w + ((4 - w % 8) + 8) % 8; }
+__host__ __device__ inline int dmma_ldb(int w) { int l = w; while (l % 8 != 2 && l % 8 != 6) ++l; return l; }
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -990,28 +999,43 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   const long w2 = (long)w * w;
   const cplx* red = ra.red + ra.red_off[s];
   cplx* X = xinv + xinv_off[s];
-  // three rotating w x w column blocks (current X_k / Z_k, next, prefetch target)
-  // and a double-buffered factor block, all staged one step ahead with cp.async
-  cplx* vb[3] = {reinterpret_cast<cplx*>(smem_raw), reinterpret_cast<cplx*>(smem_raw) + w2,
-                 reinterpret_cast<cplx*>(smem_raw) + 2 * w2};
-  cplx* Mb = vb[2] + w2;
+  // three rotating w x w column blocks (current X_k / Z_k, next, prefetch target; leading
+  // dimension lb) and a double-buffered factor block (leading dimension la), all staged
+  // one step ahead with cp.async
+  const int la = dmma_lda(w), lb = dmma_ldb(w);
+  const long sb = (long)w * lb, sa = (long)w * la;
+  cplx* vb[3] = {reinterpret_cast<cplx*>(smem_raw), reinterpret_cast<cplx*>(smem_raw) + sb,
+                 reinterpret_cast<cplx*>(smem_raw) + 2 * sb};
+  cplx* Mb = vb[2] + sb;
   const long ld = x_ld(K, w);   // row stride (128-byte aligned rows)
   auto blkX = [&](int k, int r, int c) -> cplx& { return X[((long)k * w + r) * ld + (long)j * w + c]; };
   const float invw = 1.0f / (float)w;   // e -> e / w by div_w (no integer division)
   auto rowof = [&](int e) { return div_w(e, invw); };
   auto mm = [&](cplx* C, const cplx* A, const cplx* B, bool acc) {
-    if (NT >= 256) blk_mm_tiled2(C, w, A, w, false, B, w, w, -1.0, acc);
-    else blk_mm_tiled(C, w, A, w, false, B, w, w, -1.0, acc);
+#if defined(HELM_RINV_ABL) && HELM_RINV_ABL == 1
+    __syncthreads();   // ablation (timing only): no product
+#else
+    blk_mm_dmma(C, lb, A, la, false, B, lb, w, -1.0, acc);
+#endif
   };
   auto stage_M = [&](int k, int which) {   // which = 1: G_k (forward), 2: F_k (backward)
     const cplx* G = red + ((long)k * 3 + which) * w2;
-    cplx* d = Mb + (k & 1) * w2;
-    for (int e = threadIdx.x; e < w2; e += NT) cp_async16(d + e, G + e);
+    cplx* d = Mb + (k & 1) * sa;
+    for (int e = threadIdx.x; e < w2; e += NT) {
+      const int r = rowof(e);
+      cp_async16(d + r * la + (e - r * w), G + e);
+    }
   };
   auto stage_Z = [&](int k, cplx* d) {
     for (int e = threadIdx.x; e < w2; e += NT) {
       const int r = rowof(e), c = e - r * w;
-      cp_async16(d + e, &blkX(k, r, c));
+      cp_async16(d + r * lb + c, &blkX(k, r, c));
+    }
+  };
+  auto store = [&](int k, const cplx* blk) {
+    for (int e = threadIdx.x; e < w2; e += NT) {
+      const int r = rowof(e), c = e - r * w;
+      blkX(k, r, c) = blk[r * lb + c];
     }
   };
   // X = R^{-1} is complex symmetric (R is): this CTA forms the blocks (k, j),
@@ -1022,7 +1046,7 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
     // the transposed reads are from shared memory)
     for (int e = threadIdx.x; e < w2; e += NT) {
       const int c = rowof(e), r = e - c * w;
-      X[((long)j * w + c) * ld + (long)k * w + r] = blk[r * w + c];
+      X[((long)j * w + c) * ld + (long)k * w + r] = blk[r * lb + c];
     }
   };
   // forward: k = j: Rinv_j; k > j: Z_k = -G_k Z_{k-1}
@@ -1030,8 +1054,8 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
   int ic = 0;
   for (int e = threadIdx.x; e < w2; e += NT) {
     const cplx v = red[(long)j * 3 * w2 + e];
-    vb[0][e] = v;
     const int r = rowof(e);
+    vb[0][r * lb + (e - r * w)] = v;
     blkX(j, r, e - r * w) = v;
   }
   for (int k = j + 1; k < K; ++k) {
@@ -1039,8 +1063,10 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
     __syncthreads();
     if (k + 1 < K) { stage_M(k + 1, 1); cp_async_commit(); }
     cplx* nx = vb[(ic + 1) % 3];
-    mm(nx, Mb + (k & 1) * w2, vb[ic], false);
-    for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = nx[e]; }
+    mm(nx, Mb + (k & 1) * sa, vb[ic], false);
+#if !(defined(HELM_RINV_ABL) && HELM_RINV_ABL == 2)
+    store(k, nx);
+#endif
     ic = (ic + 1) % 3;
   }
   // backward: vb[ic] holds X_{K-1}[:, j] = Z_{K-1}[:, j];  X_k = Z_k - F_k X_{k+1}, k >= j
@@ -1052,9 +1078,11 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
     __syncthreads();
     cplx* z = vb[(ic + 1) % 3];
     if (k - 1 >= j) { stage_M(k - 1, 2); stage_Z(k - 1, vb[(ic + 2) % 3]); cp_async_commit(); }
-    mm(z, Mb + (k & 1) * w2, vb[ic], true);
-    for (int e = threadIdx.x; e < w2; e += NT) { const int r = rowof(e); blkX(k, r, e - r * w) = z[e]; }
+    mm(z, Mb + (k & 1) * sa, vb[ic], true);
+#if !(defined(HELM_RINV_ABL) && HELM_RINV_ABL == 2)
+    store(k, z);
     if (k > j) mirror(k, z);
+#endif
     ic = (ic + 1) % 3;
   }
 }
@@ -1438,7 +1466,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     cudaFuncSetAttribute(k_sep2_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * ws2 * sizeof(cplx)));
   }
   const size_t smr = sizeof(cplx) * (9 * (size_t)wmax * wmax + 12 * (size_t)wmax);
-  const size_t sm3 = sizeof(cplx) * 5 * wmax * wmax;
+  const size_t sm3 = sizeof(cplx) * (size_t)wmax * (3 * dmma_ldb(wmax) + 2 * dmma_lda(wmax));
   if (P > 1 && wmax <= kRowW) cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
   if (P > 1 && want_xinv && wmax <= kXinvMaxW)
     cudaFuncSetAttribute(k_reduced_inverse<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
