@@ -164,6 +164,52 @@ __device__ inline void blk_mm_dmma(cplx* C, int ldc, const cplx* A, int lda, boo
   __syncthreads();
 }
 
+// The same product with every output tile of the warp held in registers until all
+// warps are done with the operands (MAXT >= tiles per warp): C may alias A or B.
+template <int MAXT>
+__device__ __forceinline__ void blk_mm_dmma_reg(cplx* C, int ldc, const cplx* A, int lda, const cplx* B, int ldb, int w,
+                                                double alpha) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (w + 7) >> 3;
+  const int lr = lane >> 2, lk = lane & 3;
+  double c[MAXT][4];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u) {
+    c[u][0] = c[u][1] = c[u][2] = c[u][3] = 0.0;
+    const int t = warp + u * nw;
+    if (t < nt * nt) {   // warp-uniform
+      const int ia = (t / nt) * 8 + lr, jb = (t % nt) * 8 + lr;
+      const bool aok = ia < w, bok = jb < w;
+      const cplx* Ap = A + ia * lda;
+      const cplx* Bp = B + jb;
+#pragma unroll 3
+      for (int k0 = 0; k0 < w; k0 += 4) {
+        const int k = k0 + lk;
+        const bool kok = k < w;
+        const cplx a = (aok && kok) ? Ap[k] : cmk(0, 0);
+        const cplx b = (bok && kok) ? Bp[k * ldb] : cmk(0, 0);
+        dmma_884(c[u][0], c[u][1], a.x, b.x);
+        dmma_884(c[u][0], c[u][1], -a.y, b.y);
+        dmma_884(c[u][2], c[u][3], a.x, b.y);
+        dmma_884(c[u][2], c[u][3], a.y, b.x);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u) {
+    const int t = warp + u * nw;
+    if (t < nt * nt) {
+      const int ia = (t / nt) * 8 + lr, j = (t % nt) * 8 + 2 * lk;
+      if (ia < w) {
+        if (j < w) C[ia * ldc + j] = cmk(alpha * c[u][0], alpha * c[u][2]);
+        if (j + 1 < w) C[ia * ldc + j + 1] = cmk(alpha * c[u][1], alpha * c[u][3]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // 2 x 2-tiled variant for large CTAs (324 tiles at w = 35)
 __device__ inline void blk_mm_tiled2(cplx* C, int ldc, const cplx* A, int lda, bool transA, const cplx* B, int ldb,
                                      int w, double alpha, bool accumulate) {

@@ -25,6 +25,15 @@
 #include "p1_entries.cuh"
 #include "sweep_common.cuh"
 
+#ifndef HELM_SETUP_DMMA
+#define HELM_SETUP_DMMA 1   // block products of the setup kernels on the FP64 tensor cores (dense.cuh blk_mm_dmma)
+#endif
+#if HELM_SETUP_DMMA
+#define SETUP_MM blk_mm_dmma
+#else
+#define SETUP_MM blk_mm_tiled
+#endif
+
 static constexpr int kXinvMaxW = 36;   // explicit separator inverse for the register-streaming kernel
 
 // Factor sets are shared between handles that describe the same strips (LRL and
@@ -217,7 +226,7 @@ __global__ void k_factor_segments(FacArgs fa) {
   for (int c = hi - 1; c >= lo; --c) {
     // tmp = U_c Y_{c+1}  (into XLH as scratch), then nxt = -Sinv_c tmp
     blk_lxr(XLH, cur, Ub(c, BD_U), NONE, w, 1.0, false);
-    blk_mm_tiled(nxt, w, fac + (long)c * w2, w, false, XLH, w, w, -1.0, false);
+    SETUP_MM(nxt, w, fac + (long)c * w2, w, false, XLH, w, w, -1.0, false);
     cplx* t = cur; cur = nxt; nxt = t;
   }
   blk_copy(XLH, cur, w);
@@ -237,6 +246,7 @@ __global__ void k_factor_segments(FacArgs fa) {
 // Pivot choice (largest |a_ik| among the rows not yet used, ties to the lower
 // row) and the elementary operations are those of gj_invert.
 #include "row_gj.cuh"
+
 
 __device__ long long g_red_prof[8];   // diagnostics (setup_timing knob): block 0 sub-phase cycles
 
@@ -315,9 +325,6 @@ __device__ __forceinline__ void row_store_packed(cplx* dst, int w, const RowSmem
   }
 }
 
-#ifndef HELM_SETUP_DMMA
-#define HELM_SETUP_DMMA 1   // block products of the setup kernels on the FP64 tensor cores (dense.cuh blk_mm_dmma)
-#endif
 #ifndef HELM_FAC_G
 #define HELM_FAC_G 0        // 1: k_factor_rows uses row_invert_g (raw pivot-row broadcast)
 #endif
@@ -364,6 +371,18 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
 #endif
       const cplx* cr = B(fa.cr, c);
       const cplx* ne = B(fa.ne, c);
+      // Sinv_c (stored by this CTA in the top-down pass) is read into registers first: its
+      // L2 latency passes behind the coupling product below
+      constexpr int kPre = (kRowW * kRowW + kRowThreads - 1) / kRowThreads;
+      cplx pre[kPre];
+      {
+        const cplx* src = fac + (long)c * w2;
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          const int e = threadIdx.x + u * kRowThreads;
+          pre[u] = e < w2 ? __ldcg(src + e) : cmk(0, 0);
+        }
+      }
       if (i < w) {
         const cplx ci = __ldg(cr + i);
         const cplx ni = i + 1 < w ? __ldg(ne + i) : cmk(0, 0);
@@ -374,18 +393,25 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
         }
       }
       __syncthreads();
-      // mat is free now: Sinv_c into it, then Y_c = -Sinv_c tmat with 4 x 4 register
-      // tiles (each shared-memory operand load feeds four products; a row per
-      // thread fed one, and the loop was bound by shared-memory bandwidth)
+      // mat is free now: Sinv_c into it, then Y_c = -Sinv_c tmat
       {
-        const cplx* src = fac + (long)c * w2;
         const float invw = 1.0f / (float)w;
-        for (int e = threadIdx.x; e < w2; e += blockDim.x) {
-          const int r = div_w(e, invw);
-          sm.mat[r * kRowW + (e - r * w)] = __ldcg(src + e);
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+          const int e = threadIdx.x + u * kRowThreads;
+          if (e < w2) {
+            const int r = div_w(e, invw);
+            sm.mat[r * kRowW + (e - r * w)] = pre[u];
+          }
         }
       }
       __syncthreads();
+#if HELM_SETUP_DMMA
+      // Y_c = -Sinv_c tmat on the FP64 tensor cores, the warp's output tiles in registers
+      // until every warp has read Sinv_c (the result replaces it in sm.mat)
+      blk_mm_dmma_reg<(((kRowW + 7) / 8) * ((kRowW + 7) / 8) + kRowWarps - 1) / kRowWarps>(sm.mat, kRowW, sm.mat, kRowW,
+                                                                                           sm.tmat, kRowW, w, -1.0);
+#else
       {
         const int nt = (w + 3) >> 2;
         const int t = threadIdx.x;
@@ -420,6 +446,7 @@ __global__ void __launch_bounds__(kRowThreads, HELM_FAC_MINB) k_factor_rows(FacA
         }
       }
       __syncthreads();
+#endif
     }
     row_store(scr + 3 * w2, w, sm);
   } else {
@@ -468,6 +495,11 @@ static constexpr int kRedThreads = 384;
 static constexpr int kRedLPR = HELM_RED_LPR;
 #ifndef HELM_RED_OLDGJ
 #define HELM_RED_OLDGJ 0    // 1: k_reduced uses row_invert (2 threads per row, normalised pivot-row broadcast)
+#endif
+#if HELM_SETUP_DMMA
+#define RED_MM blk_mm_dmma
+#else
+#define RED_MM blk_mm_tiled2
 #endif
 __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   __shared__ RowSmem sm;
@@ -538,7 +570,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
       __syncthreads();
     }
     // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
-    if (k >= 1) blk_mm_tiled2(S, w, T1, w, true, T2, w, w, -1.0, true);
+    if (k >= 1) RED_MM(S, w, T1, w, true, T2, w, w, -1.0, true);
     long long c1 = pr ? clock64() : 0;
     if (pr) g_red_prof[0] += c1 - c0;
     // Rinv_k (register-row Gauss-Jordan; result in sm.mat, row stride kRowW)
@@ -576,7 +608,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
         S[e] = T1[q2 * w + p2];
       }
       __syncthreads();
-      blk_mm_tiled2(G, w, sm.mat, kRowW, false, S, w, w, 1.0, false);
+      RED_MM(G, w, sm.mat, kRowW, false, S, w, w, 1.0, false);
     }
     if (k <= P - 3) {
       // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1};  F_k = Rinv_k R_{k,k+1}
@@ -585,7 +617,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
         cplx* d = ra.rraw + (((long)s * (P - 1) + k) * 2 + 1) * ra.wmax * ra.wmax;
         for (int e = threadIdx.x; e < w * w; e += blockDim.x) d[e] = T1[e];   // R_{k,k+1}
       }
-      blk_mm_tiled2(T2, w, sm.mat, kRowW, false, T1, w, w, 1.0, false);
+      RED_MM(T2, w, sm.mat, kRowW, false, T1, w, w, 1.0, false);
       for (int e = threadIdx.x; e < w * w; e += blockDim.x) F[e] = T2[e];
     }
     __syncthreads();
@@ -596,6 +628,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduced(RedArgs ra) {
   }
 }
 
+#undef RED_MM
 // ------------------------------------------------------------------ two-level separator solve (setup)
 // DESIGN.md §5 "Two-level separator solve".  The K separators of a strip are
 // split into M coarse separators and M + 1 groups of fine ones between them
@@ -950,7 +983,7 @@ __global__ void k_reduced_generic(RedArgs ra) {
     blk_lxr(S, scr(k + 1) + 2 * w2, Ub(sk, BD_U), Ub(sk, BD_UT), w, -1.0, true);
     if (k >= 1) {
       // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
-      blk_mm_tiled(S, w, Rprev, w, true, red + (long)(k - 1) * 3 * w2 + 2 * w2, w, w, -1.0, true);
+      SETUP_MM(S, w, Rprev, w, true, red + (long)(k - 1) * 3 * w2 + 2 * w2, w, w, -1.0, true);
     }
     if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
       if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
@@ -964,12 +997,12 @@ __global__ void k_reduced_generic(RedArgs ra) {
         Tmp[e] = Rprev[q * w + p];
       }
       __syncthreads();
-      blk_mm_tiled(G, w, Rinv, w, false, Tmp, w, w, 1.0, false);
+      SETUP_MM(G, w, Rinv, w, false, Tmp, w, w, 1.0, false);
     }
     if (k <= P - 3) {
       // R_{k,k+1} = - U_sk X_{k+1}[lo,hi] U_{hk1}
       blk_lxr(Rprev, scr(k + 1) + 3 * w2, Ub(sk, BD_U), Ub(hk1, BD_U), w, -1.0, false);
-      blk_mm_tiled(F, w, Rinv, w, false, Rprev, w, w, 1.0, false);
+      SETUP_MM(F, w, Rinv, w, false, Rprev, w, w, 1.0, false);
     }
   }
 }
@@ -1115,10 +1148,10 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
   for (long e = threadIdx.x; e < w2; e += blockDim.x) blk(j)[(e / w) * ld + e % w] = red[(long)j * 3 * w2 + e];
   __syncthreads();
   for (int k = j + 1; k < K; ++k)
-    blk_mm_tiled(blk(k), (int)ld, red + ((long)k * 3 + 1) * w2, w, false, blk(k - 1), (int)ld, w, -1.0, false);
+    SETUP_MM(blk(k), (int)ld, red + ((long)k * 3 + 1) * w2, w, false, blk(k - 1), (int)ld, w, -1.0, false);
   if (K - 1 > j) mirror(K - 1);
   for (int k = K - 2; k >= j; --k) {
-    blk_mm_tiled(blk(k), (int)ld, red + ((long)k * 3 + 2) * w2, w, false, blk(k + 1), (int)ld, w, -1.0, true);
+    SETUP_MM(blk(k), (int)ld, red + ((long)k * 3 + 2) * w2, w, false, blk(k + 1), (int)ld, w, -1.0, true);
     if (k > j) mirror(k);
   }
 }
