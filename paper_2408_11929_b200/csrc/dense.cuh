@@ -353,3 +353,158 @@ __device__ inline int gj_invert(cplx* A, int w, int* piv, cplx* col, double* red
   (void)redi;
   return 0;
 }
+
+// Blocked in-place Gauss-Jordan inversion with partial (row) pivoting, panels of 8 pivots.
+// The elementary operations and the pivot rule are gj_invert's; only their order differs:
+// within a panel the eliminations touch the panel's columns only (they then hold N = T e_J,
+// the accumulated transformation T of the panel's pivot steps applied to the unit vectors),
+// and every other column c gets the panel's row interchanges and steps afterwards,
+// A[:, c] <- A[:, c] + (N - I_J) A[J, c]: the rows J outside the panel are saved to ybuf
+// and cleared, then A += N ybuf on the FP64 tensor cores (mma.sync.m8n8k4: M = w, K = 8,
+// N = w - 8).  97% of the flops of a 99 x 99 inversion move from a shared-memory-bound
+// rank-1 sweep per pivot (five CTA barriers each) to the tensor pipe.  The panel itself
+// (w x 8) is factored by the first ceil(w / 32) warps, a thread per row, synchronised by a
+// named barrier (four per pivot) instead of CTA barriers; a single warp with four rows per
+// lane measured slower.
+// ybuf: 8 * w entries of shared memory; col: unused (kept for the call signature).
+// Whole CTA (whole warps).  Returns 1 (to all threads) if a pivot is zero.
+__device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* ybuf, double* redv, int* flag) {
+  constexpr int NB = 8;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int warp = tid >> 5, nw = nthr >> 5, lane = tid & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int nt = (w + 7) >> 3;
+  const int npw = (w + 31) >> 5;   // warps of the panel group (w <= 32 * warps of the CTA)
+  (void)col; (void)redv;
+  if (tid == 0) *flag = 0;
+  __syncthreads();
+  for (int j0 = 0; j0 < w; j0 += NB) {
+    const int nb = min(NB, w - j0);
+    // ---- the panel's columns, all rows: the first ceil(w / 32) warps, a thread per row,
+    // synchronised among themselves by a named barrier (the other warps wait below)
+    if (warp < npw) {
+      const int i = tid;                       // this thread's row
+      const bool row = i < w;
+      double* rv = reinterpret_cast<double*>(ybuf);        // [npw] warp maxima (ybuf is free here)
+      int* ri = reinterpret_cast<int*>(ybuf + 4);          // [npw] their rows
+      auto pbar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(npw * 32) : "memory"); };
+      for (int k = j0; k < j0 + nb; ++k) {
+        double best = (row && i >= k) ? cabs2(A[i * w + k]) : -1.0;
+        int bi = i;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { rv[warp] = best; ri[warp] = bi; }
+        pbar();
+        best = rv[0]; bi = ri[0];
+        for (int q = 1; q < npw; ++q)
+          if (rv[q] > best) { best = rv[q]; bi = ri[q]; }   // ties: the lower row (warps in row order)
+        if (!(best > 0.0)) {   // uniform over the group
+          if (tid == 0) *flag = 1;
+          break;
+        }
+        const int p = bi;
+        if (tid == 0) piv[k] = p;
+        if (p != k && tid < nb) {
+          const cplx t = A[k * w + j0 + tid];
+          A[k * w + j0 + tid] = A[p * w + j0 + tid];
+          A[p * w + j0 + tid] = t;
+        }
+        pbar();
+        const cplx dinv = cinv(A[k * w + k]);
+        const cplx f = row ? A[i * w + k] : cmk(0.0, 0.0);   // this row's multiplier
+        cplx av[NB];
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj) av[jj] = (row && jj < nb) ? A[i * w + j0 + jj] : cmk(0.0, 0.0);
+        pbar();
+        if (i == k) {
+#pragma unroll
+          for (int jj = 0; jj < NB; ++jj)
+            if (jj < nb) A[k * w + j0 + jj] = cmul(j0 + jj == k ? cmk(1.0, 0.0) : av[jj], dinv);
+        }
+        pbar();
+        if (row && i != k) {
+#pragma unroll
+          for (int jj = 0; jj < NB; ++jj) {
+            if (jj < nb) {
+              const cplx r = A[k * w + j0 + jj];
+              cplx a = (j0 + jj == k) ? cmk(0.0, 0.0) : av[jj];
+              a.x -= f.x * r.x - f.y * r.y;
+              a.y -= f.x * r.y + f.y * r.x;
+              A[i * w + j0 + jj] = a;
+            }
+          }
+        }
+        pbar();
+      }
+    }
+    __syncthreads();
+    if (*flag) return 1;
+    // ---- the panel's row interchanges on every other column (a thread per column, in order)
+    for (int c = tid; c < w; c += nthr) {
+      if (c >= j0 && c < j0 + nb) continue;
+      for (int k = j0; k < j0 + nb; ++k) {
+        const int p = piv[k];
+        if (p != k) {
+          const cplx t = A[k * w + c];
+          A[k * w + c] = A[p * w + c];
+          A[p * w + c] = t;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- ybuf = A[J, :] outside the panel (zero inside), rows J cleared there
+    for (int e = tid; e < NB * w; e += nthr) {
+      const int kk = e / w, c = e - kk * w;
+      const bool inpanel = c >= j0 && c < j0 + nb;
+      cplx y = cmk(0.0, 0.0);
+      if (kk < nb && !inpanel) {
+        y = A[(j0 + kk) * w + c];
+        A[(j0 + kk) * w + c] = cmk(0.0, 0.0);
+      }
+      ybuf[e] = y;
+    }
+    __syncthreads();
+    // A += N ybuf on 8 x 8 tiles (one warp per tile), all tile columns but the panel's own
+    const int tjp = j0 >> 3;
+    for (int t = warp; t < nt * nt; t += nw) {
+      const int ti = t / nt, tj = t - ti * nt;
+      if (tj == tjp) continue;   // warp-uniform
+      const int ia = ti * 8 + lr, jb = tj * 8 + lr;
+      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const int k = k0 + lk;
+        const cplx a = (ia < w && k < nb) ? A[ia * w + j0 + k] : cmk(0, 0);
+        const cplx b = jb < w ? ybuf[k * w + jb] : cmk(0, 0);
+        dmma_884(cr0, cr1, a.x, b.x);
+        dmma_884(cr0, cr1, -a.y, b.y);
+        dmma_884(ci0, ci1, a.x, b.y);
+        dmma_884(ci0, ci1, a.y, b.x);
+      }
+      if (ia < w) {
+        const int j = tj * 8 + 2 * lk;
+        cplx* Cp = A + ia * w + j;
+        if (j < w) Cp[0] = cadd(Cp[0], cmk(cr0, ci0));
+        if (j + 1 < w) Cp[1] = cadd(Cp[1], cmk(cr1, ci1));
+      }
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, in reverse order (a thread per row)
+  for (int i = tid; i < w; i += nthr) {
+    for (int k = w - 1; k >= 0; --k) {
+      const int p = piv[k];
+      if (p != k) {
+        const cplx t = A[i * w + k];
+        A[i * w + k] = A[i * w + p];
+        A[i * w + p] = t;
+      }
+    }
+  }
+  __syncthreads();
+  return 0;
+}

@@ -28,6 +28,11 @@
 #ifndef HELM_SETUP_DMMA
 #define HELM_SETUP_DMMA 1   // block products of the setup kernels on the FP64 tensor cores (dense.cuh blk_mm_dmma)
 #endif
+#ifndef HELM_GJ_BLOCKED
+#define HELM_GJ_BLOCKED 1   // shared-memory Gauss-Jordan (wide strips): panels of 8 pivots, the other columns updated on the tensor cores
+#endif
+#define WIDE_GJ(S, w, piv, colv, ybuf, redv, flag) \
+  ((ybuf) ? gj_invert_blk(S, w, piv, colv, ybuf, redv, flag) : gj_invert(S, w, piv, colv, redv, nullptr, flag))
 #if HELM_SETUP_DMMA
 #define SETUP_MM blk_mm_dmma
 #else
@@ -182,7 +187,12 @@ __global__ void k_factor_segments(FacArgs fa) {
   const int w = fa.w[s];
   cplx* S = reinterpret_cast<cplx*>(smem_raw);
   cplx* colv = S + w * w;
-  double* redv = reinterpret_cast<double*>(colv + w);
+  // gj_invert_blk needs the panel's pivot rows (8 w entries): used when the launch's shared memory holds them
+  unsigned dsm;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
+  const bool gjblk = HELM_GJ_BLOCKED && dsm >= sizeof(cplx) * ((size_t)w * w + 9 * (size_t)w) + sizeof(int) * (w + 4) + 64;
+  cplx* ybuf = gjblk ? colv + w : nullptr;
+  double* redv = reinterpret_cast<double*>(colv + w + (gjblk ? 8 * w : 0));
   int* flag = reinterpret_cast<int*>(redv + 4);
   int* piv = flag + 4;
   const int lo = fa.seg_lo[pseg], hi = fa.seg_hi[pseg];
@@ -196,7 +206,7 @@ __global__ void k_factor_segments(FacArgs fa) {
   for (int c = lo; c <= hi; ++c) {
     build_D(S, fa.dg + band + (long)c * fa.wmax, fa.al + band + (long)c * fa.wmax, w);
     if (c > lo) blk_lxr(S, fac + (long)(c - 1) * w2, Ub(c - 1, BD_UT), Ub(c - 1, BD_U), w, -1.0, true);
-    if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
+    if (WIDE_GJ(S, w, piv, colv, ybuf, redv, flag)) {
       if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
       return;
     }
@@ -213,7 +223,7 @@ __global__ void k_factor_segments(FacArgs fa) {
   for (int c = hi; c >= lo; --c) {
     build_D(S, fa.dg + band + (long)c * fa.wmax, fa.al + band + (long)c * fa.wmax, w);
     if (c < hi) blk_lxr(S, ping, Ub(c, BD_U), Ub(c, BD_UT), w, -1.0, true);
-    if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
+    if (WIDE_GJ(S, w, piv, colv, ybuf, redv, flag)) {
       if (threadIdx.x == 0) atomicCAS(fa.status, 0, s * fa.nc + c + 1);
       return;
     }
@@ -959,7 +969,12 @@ __global__ void k_reduced_generic(RedArgs ra) {
   const long w2 = (long)w * w;
   cplx* S = reinterpret_cast<cplx*>(smem_raw);
   cplx* colv = S + w * w;
-  double* redv = reinterpret_cast<double*>(colv + w);
+  // gj_invert_blk needs the panel's pivot rows (8 w entries): used when the launch's shared memory holds them
+  unsigned dsm;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
+  const bool gjblk = HELM_GJ_BLOCKED && dsm >= sizeof(cplx) * ((size_t)w * w + 9 * (size_t)w) + sizeof(int) * (w + 4) + 64;
+  cplx* ybuf = gjblk ? colv + w : nullptr;
+  double* redv = reinterpret_cast<double*>(colv + w + (gjblk ? 8 * w : 0));
   int* flag = reinterpret_cast<int*>(redv + 4);
   int* piv = flag + 4;
   const long band = (long)s * ra.nc * ra.wmax;
@@ -985,7 +1000,7 @@ __global__ void k_reduced_generic(RedArgs ra) {
       // - R_{k,k-1} Rinv_{k-1} R_{k-1,k} = - R_{k-1,k}^T F_{k-1}
       SETUP_MM(S, w, Rprev, w, true, red + (long)(k - 1) * 3 * w2 + 2 * w2, w, w, -1.0, true);
     }
-    if (gj_invert(S, w, piv, colv, redv, nullptr, flag)) {
+    if (WIDE_GJ(S, w, piv, colv, ybuf, redv, flag)) {
       if (threadIdx.x == 0) atomicCAS(ra.status, 0, s * ra.nc + sk + 1);
       return;
     }
@@ -1482,7 +1497,8 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
     sweep_destroy(h);
     return HELM_ENOMEM;
   }
-  size_t smem = sizeof(cplx) * ((size_t)wmax * wmax + wmax) + sizeof(int) * (wmax + 4) + 64;
+  size_t smem = sizeof(cplx) * ((size_t)wmax * wmax + 9 * (size_t)wmax) + sizeof(int) * (wmax + 4) + 64;   // blocked Gauss-Jordan
+  if (smem > 227u * 1024u) smem = sizeof(cplx) * ((size_t)wmax * wmax + wmax) + sizeof(int) * (wmax + 4) + 64;   // w > 115: unblocked
   cudaFuncSetAttribute(k_factor_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_reduced_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int threads = wmax * wmax >= 1024 ? 512 : 256;
