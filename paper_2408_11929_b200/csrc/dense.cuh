@@ -366,9 +366,14 @@ __device__ inline int gj_invert(cplx* A, int w, int* piv, cplx* col, double* red
 // (w x 8) is factored by the first ceil(w / 32) warps, a thread per row, synchronised by a
 // named barrier (four per pivot) instead of CTA barriers; a single warp with four rows per
 // lane measured slower.
-// ybuf: 8 * w entries of shared memory; col: unused (kept for the call signature).
+// A has leading dimension ld.  ybuf: 8 * w entries of shared memory; col, redv: unused (kept
+// for the call signature).
 // Whole CTA (whole warps).  Returns 1 (to all threads) if a pivot is zero.
-__device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* ybuf, double* redv, int* flag) {
+// For the 35 x 35 blocks of the narrow strips it measured 2.3x SLOWER than the register-row
+// Gauss-Jordan (row_gj.cuh: 100 k against 44 k cycles per inversion in k_reduced, segment
+// factors 9.5 against 5.1 ms per axis): five group barriers per pivot against two, and a
+// product of only 20 tiles per panel.  Used for strips wider than 36 nodes only.
+__device__ inline int gj_invert_blk(cplx* A, int ld, int w, int* piv, cplx* col, cplx* ybuf, double* redv, int* flag) {
   constexpr int NB = 8;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, nw = nthr >> 5, lane = tid & 31;
@@ -389,7 +394,7 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
       int* ri = reinterpret_cast<int*>(ybuf + 4);          // [npw] their rows
       auto pbar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(npw * 32) : "memory"); };
       for (int k = j0; k < j0 + nb; ++k) {
-        double best = (row && i >= k) ? cabs2(A[i * w + k]) : -1.0;
+        double best = (row && i >= k) ? cabs2(A[i * ld + k]) : -1.0;
         int bi = i;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -409,32 +414,32 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
         const int p = bi;
         if (tid == 0) piv[k] = p;
         if (p != k && tid < nb) {
-          const cplx t = A[k * w + j0 + tid];
-          A[k * w + j0 + tid] = A[p * w + j0 + tid];
-          A[p * w + j0 + tid] = t;
+          const cplx t = A[k * ld + j0 + tid];
+          A[k * ld + j0 + tid] = A[p * ld + j0 + tid];
+          A[p * ld + j0 + tid] = t;
         }
         pbar();
-        const cplx dinv = cinv(A[k * w + k]);
-        const cplx f = row ? A[i * w + k] : cmk(0.0, 0.0);   // this row's multiplier
+        const cplx dinv = cinv(A[k * ld + k]);
+        const cplx f = row ? A[i * ld + k] : cmk(0.0, 0.0);   // this row's multiplier
         cplx av[NB];
 #pragma unroll
-        for (int jj = 0; jj < NB; ++jj) av[jj] = (row && jj < nb) ? A[i * w + j0 + jj] : cmk(0.0, 0.0);
+        for (int jj = 0; jj < NB; ++jj) av[jj] = (row && jj < nb) ? A[i * ld + j0 + jj] : cmk(0.0, 0.0);
         pbar();
         if (i == k) {
 #pragma unroll
           for (int jj = 0; jj < NB; ++jj)
-            if (jj < nb) A[k * w + j0 + jj] = cmul(j0 + jj == k ? cmk(1.0, 0.0) : av[jj], dinv);
+            if (jj < nb) A[k * ld + j0 + jj] = cmul(j0 + jj == k ? cmk(1.0, 0.0) : av[jj], dinv);
         }
         pbar();
         if (row && i != k) {
 #pragma unroll
           for (int jj = 0; jj < NB; ++jj) {
             if (jj < nb) {
-              const cplx r = A[k * w + j0 + jj];
+              const cplx r = A[k * ld + j0 + jj];
               cplx a = (j0 + jj == k) ? cmk(0.0, 0.0) : av[jj];
               a.x -= f.x * r.x - f.y * r.y;
               a.y -= f.x * r.y + f.y * r.x;
-              A[i * w + j0 + jj] = a;
+              A[i * ld + j0 + jj] = a;
             }
           }
         }
@@ -449,9 +454,9 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
       for (int k = j0; k < j0 + nb; ++k) {
         const int p = piv[k];
         if (p != k) {
-          const cplx t = A[k * w + c];
-          A[k * w + c] = A[p * w + c];
-          A[p * w + c] = t;
+          const cplx t = A[k * ld + c];
+          A[k * ld + c] = A[p * ld + c];
+          A[p * ld + c] = t;
         }
       }
     }
@@ -462,8 +467,8 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
       const bool inpanel = c >= j0 && c < j0 + nb;
       cplx y = cmk(0.0, 0.0);
       if (kk < nb && !inpanel) {
-        y = A[(j0 + kk) * w + c];
-        A[(j0 + kk) * w + c] = cmk(0.0, 0.0);
+        y = A[(j0 + kk) * ld + c];
+        A[(j0 + kk) * ld + c] = cmk(0.0, 0.0);
       }
       ybuf[e] = y;
     }
@@ -478,7 +483,7 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
 #pragma unroll
       for (int k0 = 0; k0 < NB; k0 += 4) {
         const int k = k0 + lk;
-        const cplx a = (ia < w && k < nb) ? A[ia * w + j0 + k] : cmk(0, 0);
+        const cplx a = (ia < w && k < nb) ? A[ia * ld + j0 + k] : cmk(0, 0);
         const cplx b = jb < w ? ybuf[k * w + jb] : cmk(0, 0);
         dmma_884(cr0, cr1, a.x, b.x);
         dmma_884(cr0, cr1, -a.y, b.y);
@@ -487,7 +492,7 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
       }
       if (ia < w) {
         const int j = tj * 8 + 2 * lk;
-        cplx* Cp = A + ia * w + j;
+        cplx* Cp = A + ia * ld + j;
         if (j < w) Cp[0] = cadd(Cp[0], cmk(cr0, ci0));
         if (j + 1 < w) Cp[1] = cadd(Cp[1], cmk(cr1, ci1));
       }
@@ -499,9 +504,9 @@ __device__ inline int gj_invert_blk(cplx* A, int w, int* piv, cplx* col, cplx* y
     for (int k = w - 1; k >= 0; --k) {
       const int p = piv[k];
       if (p != k) {
-        const cplx t = A[i * w + k];
-        A[i * w + k] = A[i * w + p];
-        A[i * w + p] = t;
+        const cplx t = A[i * ld + k];
+        A[i * ld + k] = A[i * ld + p];
+        A[i * ld + p] = t;
       }
     }
   }

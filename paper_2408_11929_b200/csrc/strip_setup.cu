@@ -32,7 +32,7 @@
 #define HELM_GJ_BLOCKED 1   // shared-memory Gauss-Jordan (wide strips): panels of 8 pivots, the other columns updated on the tensor cores
 #endif
 #define WIDE_GJ(S, w, piv, colv, ybuf, redv, flag) \
-  ((ybuf) ? gj_invert_blk(S, w, piv, colv, ybuf, redv, flag) : gj_invert(S, w, piv, colv, redv, nullptr, flag))
+  ((ybuf) ? gj_invert_blk(S, w, w, piv, colv, ybuf, redv, flag) : gj_invert(S, w, piv, colv, redv, nullptr, flag))
 #if HELM_SETUP_DMMA
 #define SETUP_MM blk_mm_dmma
 #else
