@@ -36,7 +36,7 @@ enum {
   HELM_OK = 0,
   HELM_EINVAL = 1,      /* invalid argument (sizes, strips too thin, t out of range, tol) */
   HELM_EDIM = 2,        /* mismatched dimensions between handles */
-  HELM_ESINGULAR = 3,   /* zero pivot while factoring a strip block */
+  HELM_ESINGULAR = 3,   /* zero or non-finite (NaN / Inf) pivot while factoring a strip block */
   HELM_ECUDA = 4,       /* CUDA runtime error or no device */
   HELM_ENOMEM = 5,      /* device allocation failed */
   HELM_ENOCONV = 6,     /* maxit reached; x holds the last iterate */

@@ -87,7 +87,7 @@ __device__ __forceinline__ int row_invert_g(cplx (&a)[kRowW / LPR], int w, RowSm
 #pragma unroll
     for (int q = 1; q < NWR; ++q)
       if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
-    if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
+    if (k0 <= 1u || k0 > 0x7FF00000u) return 1;   // all candidates zero (key 1 = +0.0), or a NaN / Inf entry (exponent all ones)
     if (i == p) {
 #pragma unroll
       for (int jj = 0; jj < HW; ++jj) sm.prow[LPR * jj + h] = a[jj];
@@ -207,7 +207,7 @@ __device__ __forceinline__ int row_invert(cplx (&a)[kRowHW], int w, RowSmem& sm)
 #pragma unroll
     for (int q = 1; q < kRowWarps; ++q)
       if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
-    if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
+    if (k0 <= 1u || k0 > 0x7FF00000u) return 1;   // all candidates zero (key 1 = +0.0), or a NaN / Inf entry (exponent all ones)
 #endif
     // pivot element to every lane of the pivot row; multiplier to every lane of the others
     cplx akk;
@@ -294,7 +294,7 @@ __device__ __forceinline__ int row_invert_r(cplx (&a)[kRowHW], int w, RowSmem& s
 #pragma unroll
           for (int q = 1; q < kRowWarps; ++q)
             if (sm.redk[q] > k0) { k0 = sm.redk[q]; p = sm.redi[q]; }
-          if (k0 <= 1u) return 1;   // all candidates zero (key 1 = +0.0)
+          if (k0 <= 1u || k0 > 0x7FF00000u) return 1;   // all candidates zero (key 1 = +0.0), or a NaN / Inf entry (exponent all ones)
           cplx akk;
           {
             const int src = (lane & ~(kLPR - 1)) | kh;

@@ -570,3 +570,25 @@ def test_two_level_separator_solve(name, knob):
         z_ref = P.apply(Rh[k])
         assert elementwise(Zs[0][k], z_ref) <= 1e-10, (name, k, elementwise(Zs[0][k], z_ref))
         assert elementwise(Zs[0][k], Zs[1][k]) <= 1e-11
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_setup_reports_unfactorable_strip(wide):
+    """Failure detection: a NaN wave speed poisons a strip block, no pivot
+    compares > 0, and sweep_setup returns HELM_ESINGULAR instead of factors full of NaN --
+    on the register-row Gauss-Jordan (strips <= 36 nodes) and on the blocked shared-memory
+    one (wider strips)."""
+    if wide:
+        cfg = small_problem(160, 48, 12.0, seed=31, variable_c=True, n_strips=2, overlap=1)
+    else:
+        cfg = small_problem(40, 33, 25.0, seed=5, variable_c=True, n_strips=5, overlap=1)
+    c = cfg.c.copy().ravel()
+    c[c.size // 2] = np.nan
+    prob = hs.Problem(cfg.nx, cfg.ny, cfg.h, cfg.omega, torch.tensor(c, dtype=torch.float64, device=DEV))
+    with pytest.raises(hs.HelmError) as ei:
+        hs.Sweep(prob, "LRL", n_strips=cfg.n_strips, overlap=cfg.overlap, n_segments=3)
+    assert ei.value.code == 3, ei.value   # HELM_ESINGULAR
+    # the library is still usable afterwards
+    good = gpu_problem(cfg)
+    d = hs.Sweep(good, "LRL", n_strips=cfg.n_strips, overlap=cfg.overlap, n_segments=3)
+    assert d.info().wmax > 36 if wide else d.info().wmax <= 36
