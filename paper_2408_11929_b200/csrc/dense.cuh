@@ -164,6 +164,72 @@ __device__ inline void blk_mm_dmma(cplx* C, int ldc, const cplx* A, int lda, boo
   __syncthreads();
 }
 
+// Shared-memory leading dimensions of the tensor-core product's operands: A fragments
+// (2 rows x 4 k per quarter-warp) are conflict-free when lda = 4 mod 8, B fragments
+// (4 k x 2 columns) when ldb = 2 or 6 mod 8.
+__host__ __device__ inline int dmma_lda(int w) { return w + ((4 - w % 8) + 8) % 8; }
+__host__ __device__ inline int dmma_ldb(int w) { int l = w; while (l % 8 != 2 && l % 8 != 6) ++l; return l; }
+constexpr int kDmmaPanel = 32, kDmmaPanelLd = 34;   // column panel of the staged product and its leading dimension
+
+// C (+)= alpha A B for operands in global memory (wide blocks: w x w does not fit shared
+// memory three times): A is staged whole into sA (w x dmma_lda(w)), B in panels of 32
+// columns into sB (w x 34), each output tile by one warp as in blk_mm_dmma.  C must not
+// alias A or B.  Whole CTA; ends with __syncthreads().
+__device__ inline void blk_mm_dmma_staged(cplx* C, int ldc, const cplx* A, int lda, const cplx* B, int ldb, int w,
+                                          double alpha, bool accumulate, cplx* sA, cplx* sB) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int warp = tid >> 5, nw = nthr >> 5, lane = tid & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int la = dmma_lda(w);
+  const int ntr = (w + 7) >> 3;
+  for (int e = tid; e < w * w; e += nthr) {
+    const int r = e / w, c = e - r * w;
+    sA[r * la + c] = __ldcg(A + (long)r * lda + c);
+  }
+  for (int c0 = 0; c0 < w; c0 += kDmmaPanel) {
+    const int nc = min(kDmmaPanel, w - c0);
+    __syncthreads();   // the previous panel's readers are done (and, the first time, sA is complete below)
+    for (int e = tid; e < w * kDmmaPanel; e += nthr) {
+      const int r = e >> 5, cc = e & 31;
+      sB[r * kDmmaPanelLd + cc] = cc < nc ? __ldcg(B + (long)r * ldb + c0 + cc) : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    const int ntc = (nc + 7) >> 3;
+    for (int t = warp; t < ntr * ntc; t += nw) {
+      const int ti = t / ntc, tj = t - ti * ntc;
+      const int ia = ti * 8 + lr, jb = tj * 8 + lr;
+      const bool aok = ia < w;
+      const cplx* Ap = sA + ia * la;
+      const cplx* Bp = sB + jb;
+      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll 4
+      for (int k0 = 0; k0 < w; k0 += 4) {
+        const int k = k0 + lk;
+        const bool kok = k < w;
+        const cplx a = (aok && kok) ? Ap[k] : cmk(0, 0);
+        const cplx b = kok ? Bp[k * kDmmaPanelLd] : cmk(0, 0);
+        dmma_884(cr0, cr1, a.x, b.x);
+        dmma_884(cr0, cr1, -a.y, b.y);
+        dmma_884(ci0, ci1, a.x, b.y);
+        dmma_884(ci0, ci1, a.y, b.x);
+      }
+      if (aok) {
+        const int j = c0 + tj * 8 + 2 * lk;
+        cplx* Cp = C + (long)ia * ldc + j;
+        if (j < w) {
+          const cplx v = cmk(alpha * cr0, alpha * ci0);
+          Cp[0] = accumulate ? cadd(Cp[0], v) : v;
+        }
+        if (j + 1 < w) {
+          const cplx v = cmk(alpha * cr1, alpha * ci1);
+          Cp[1] = accumulate ? cadd(Cp[1], v) : v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // The same product with every output tile of the warp held in registers until all
 // warps are done with the operands (MAXT >= tiles per warp): C may alias A or B.
 template <int MAXT>

@@ -1031,11 +1031,6 @@ __global__ void k_reduced_generic(RedArgs ra) {
 // (strip, column block j):  Z_j = Rinv_j E_j, Z_k = -G_k Z_{k-1} (k > j),
 // X_{K-1} = Z_{K-1}, X_k = Z_k - F_k X_{k+1}.  Storage per strip:
 // X[k] is w x (K w) row-major (the rows of separator k), contiguous.
-// Shared-memory leading dimensions of the tensor-core product's operands (dense.cuh
-// blk_mm_dmma): A fragments (2 rows x 4 k per quarter-warp) are conflict-free when
-// lda = 4 mod 8, B fragments (4 k x 2 columns) when ldb = 2 or 6 mod 8.
-__host__ __device__ inline int dmma_lda(int w) { return w + ((4 - w % 8) + 8) % 8; }
-__host__ __device__ inline int dmma_ldb(int w) { int l = w; while (l % 8 != 2 && l % 8 != 6) ++l; return l; }
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
@@ -1141,7 +1136,8 @@ __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, 
 // X_k = Z_k - F_k X_{k+1} (k < K-1); the products are 4x4 register-tiled with
 // operands from L1/L2.  The CTA only reads blocks it wrote itself (same SM: the
 // write-through L1 stays coherent after the barrier ending each product).
-__global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* xinv, const long* xinv_off) {
+__global__ void __launch_bounds__(512, 1) k_reduced_inverse_glb(RedArgs ra, cplx* xinv, const long* xinv_off) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = blockIdx.y + ra.s0, j = blockIdx.x;
   const int K = ra.P - 1;
   if (j >= K) return;
@@ -1151,6 +1147,18 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
   cplx* X = xinv + xinv_off[s];
   const long ld = x_ld(K, w);
   auto blk = [&](int k) { return X + (long)k * w * ld + (long)j * w; };   // block (k, j), row stride ld
+  // the products stage their operands in shared memory (the factor block whole, the column
+  // block in panels of 32 columns) when the launch provides it; straight from L1 / L2 the
+  // tensor pipe ran at 0.23 of its peak (every warp re-reads its operand rows and columns)
+  unsigned dsm;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
+  const bool staged = dsm >= sizeof(cplx) * (size_t)w * (dmma_lda(w) + kDmmaPanelLd);
+  cplx* sA = reinterpret_cast<cplx*>(smem_raw);
+  cplx* sB = sA + (long)w * dmma_lda(w);
+  auto mm = [&](cplx* C, const cplx* A, const cplx* B, bool acc) {
+    if (staged) blk_mm_dmma_staged(C, (int)ld, A, w, B, (int)ld, w, -1.0, acc, sA, sB);
+    else SETUP_MM(C, (int)ld, A, w, false, B, (int)ld, w, -1.0, acc);
+  };
   // blocks (k, j), k >= j, mirrored into (j, k) (X is symmetric; see k_reduced_inverse)
   auto mirror = [&](int k) {
     __syncthreads();
@@ -1162,11 +1170,10 @@ __global__ void __launch_bounds__(256) k_reduced_inverse_glb(RedArgs ra, cplx* x
   };
   for (long e = threadIdx.x; e < w2; e += blockDim.x) blk(j)[(e / w) * ld + e % w] = red[(long)j * 3 * w2 + e];
   __syncthreads();
-  for (int k = j + 1; k < K; ++k)
-    SETUP_MM(blk(k), (int)ld, red + ((long)k * 3 + 1) * w2, w, false, blk(k - 1), (int)ld, w, -1.0, false);
+  for (int k = j + 1; k < K; ++k) mm(blk(k), red + ((long)k * 3 + 1) * w2, blk(k - 1), false);
   if (K - 1 > j) mirror(K - 1);
   for (int k = K - 2; k >= j; --k) {
-    SETUP_MM(blk(k), (int)ld, red + ((long)k * 3 + 2) * w2, w, false, blk(k + 1), (int)ld, w, -1.0, true);
+    mm(blk(k), red + ((long)k * 3 + 2) * w2, blk(k + 1), true);
     if (k > j) mirror(k);
   }
 }
@@ -1553,7 +1560,12 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
       if (e2 == cudaSuccess && want_xinv) {
         // explicit separator inverse rows for the register-streaming kernel
         // (128 threads: 256 measured slower, round 1)
-        if (wmax > kXinvMaxW) k_reduced_inverse_glb<<<dim3(P - 1, ns), 256, 0, cs>>>(rc, h->d_xinv, h->d_xinv_off);
+        if (wmax > kXinvMaxW) {
+          size_t smg = sizeof(cplx) * (size_t)wmax * (dmma_lda(wmax) + kDmmaPanelLd);   // staged operands
+          if (smg > 227u * 1024u) smg = 0;
+          else cudaFuncSetAttribute(k_reduced_inverse_glb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg);
+          k_reduced_inverse_glb<<<dim3(P - 1, ns), 512, smg, cs>>>(rc, h->d_xinv, h->d_xinv_off);
+        }
         else k_reduced_inverse<128><<<dim3(P - 1, ns), 128, sm3, cs>>>(rc, h->d_xinv, h->d_xinv_off);
         if (timing) cudaEventRecord(tev[4], cs);
         g_helm_launches++;
