@@ -70,6 +70,13 @@
 #ifndef HELM_DUAL_XPF_PROD
 #define HELM_DUAL_XPF_PROD 1    // 1: the X-row L2 prefetch is issued by the chain-A producer warp when phase 1 ends
 #endif
+#ifndef HELM_DUAL_FPF
+#define HELM_DUAL_FPF 7     // n > 0: the producers prefetch the factor block n steps ahead into L2 (C5 t = 4: off 3.74,
+                            // 4: 3.74, 5: 3.72, 6: 3.71, 7: 3.69, 8: 3.70, 9: 3.73, 10: 3.74, 16: 3.78 ms)
+#endif
+#ifndef HELM_DUAL_FPF_P1
+#define HELM_DUAL_FPF_P1 1  // 1: only phase-1 blocks are prefetched (phase 3 too: the same 3.69 ms)
+#endif
 #ifndef HELM_DUAL_EPIREL
 #define HELM_DUAL_EPIREL 1    // 1: the epilogue counter is released by chain B's producer lane (not thread 0 before a barrier)
 #endif
@@ -302,6 +309,19 @@ __global__ void __launch_bounds__(dualk::MAXT, 1) k_sweep_dual(const __grid_cons
 #endif
           uint64_t* bar = &full[pg * NST + st];
           const uint32_t bytes = (uint32_t)(pw * sizeof(cplx));
+#if HELM_DUAL_FPF
+          {
+            // L2 prefetch of the factor block HELM_DUAL_FPF steps ahead (same solve): the ring
+            // holds only NST - 1 blocks in flight, ~3.5 k cycles of lookahead against HBM
+            // latency spikes under load
+            const int ea = e + HELM_DUAL_FPF;
+            if (ea < (HELM_DUAL_FPF_P1 ? m : 2 * m)) {
+              const int pha = ea >= m ? 1 : 0, jsa = ea - pha * m;
+              const bool upa = (pg == 0) == (pha == 0);
+              dprefetch_l2(fbase + (long)(upa ? lo + jsa : hi - jsa) * pw, bytes, pha == 0 ? polL : polF);
+            }
+          }
+#endif
           mbar_expect_tx(bar, bytes);
           bulk_g2s_hint(ring + ((long)pg * NST + st) * A.stage_elems, src, bytes, bar, ph == 0 ? polL : polF);
         }
