@@ -1032,6 +1032,10 @@ __global__ void k_reduced_generic(RedArgs ra) {
 // X_{K-1} = Z_{K-1}, X_k = Z_k - F_k X_{k+1}.  Storage per strip:
 // X[k] is w x (K w) row-major (the rows of separator k), contiguous.
 
+#ifndef HELM_RINV_THREADS
+#define HELM_RINV_THREADS 256   // C5 separator inverse per axis: 128: 1.43, 192: 1.33, 256: 1.17, 512: 1.20, 800: 1.23 ms
+#endif
+constexpr int kRinvThreads = HELM_RINV_THREADS;
 template <int NT>
 __global__ void __launch_bounds__(NT) k_reduced_inverse(RedArgs ra, cplx* xinv, const long* xinv_off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1525,7 +1529,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
   const size_t sm3 = sizeof(cplx) * (size_t)wmax * (3 * dmma_ldb(wmax) + 2 * dmma_lda(wmax));
   if (P > 1 && wmax <= kRowW) cudaFuncSetAttribute(k_reduced, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
   if (P > 1 && want_xinv && wmax <= kXinvMaxW)
-    cudaFuncSetAttribute(k_reduced_inverse<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+    cudaFuncSetAttribute(k_reduced_inverse<kRinvThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
   const bool rows_kernel = wmax <= kRowW && !helm_knob(KNOB_FACTOR_GENERIC);
   // strips [s0, s0 + ns): segment factors, separator factors, separator-inverse rows
   auto run_chunk = [&](cudaStream_t cs, int s0, int ns, cudaEvent_t fac_done) {
@@ -1566,7 +1570,7 @@ extern "C" int sweep_setup(helm_problem_t prob, int axis, int order, int n_strip
           else cudaFuncSetAttribute(k_reduced_inverse_glb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg);
           k_reduced_inverse_glb<<<dim3(P - 1, ns), 512, smg, cs>>>(rc, h->d_xinv, h->d_xinv_off);
         }
-        else k_reduced_inverse<128><<<dim3(P - 1, ns), 128, sm3, cs>>>(rc, h->d_xinv, h->d_xinv_off);
+        else k_reduced_inverse<kRinvThreads><<<dim3(P - 1, ns), kRinvThreads, sm3, cs>>>(rc, h->d_xinv, h->d_xinv_off);
         if (timing) cudaEventRecord(tev[4], cs);
         g_helm_launches++;
         e2 = cudaGetLastError();

@@ -88,7 +88,10 @@ constexpr int LPR = 4;    // lanes per block row
 constexpr int OWN = 7;    // owned rows per warp (8 slots, 1 halo)
 constexpr int KPL = 9;    // complex entries per lane per block row (w <= 36)
 constexpr int WM = 40;    // vector stride
-constexpr int NST = 4;    // TMA ring stages per chain (NST-1 blocks in flight)
+#ifndef HELM_DUAL_NST
+#define HELM_DUAL_NST 4
+#endif
+constexpr int NST = HELM_DUAL_NST;    // TMA ring stages per chain (NST-1 blocks in flight)
 constexpr int MAXT = 5 * 64 + 64;   // 2 groups of <= 5 warps (w <= 35) + 2 TMA producer warps
 }  // namespace dualk
 
