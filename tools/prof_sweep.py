@@ -18,7 +18,10 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--warm", type=int, default=2)
 ap.add_argument("--nseg", type=int, default=0)
 ap.add_argument("--names", default="", help="comma-separated directions (overrides --t)")
+ap.add_argument("--knob", action="append", default=[], help="name=value (helm_set_knob), repeatable")
 a = ap.parse_args()
+for kv in a.knob:
+    hs.set_knob(kv.split("=")[0], int(kv.split("=")[1]))
 
 cfg = make_config(a.config)
 names = a.names.split(",") if a.names else {1: ["LRL"], 2: ["LRL", "BTB"], 4: ["LRL", "RLR", "BTB", "TBT"]}[a.t]
