@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--clock-interval-ms", type=int, default=50, help="nvidia-smi sampling period during the timed region")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "directions"],
                     help="N > 1: independent replicas per rank (default), or the direction-parallel "
                          "solve (mpgmres_solve_dist: the t directions split over the ranks of a group, "
@@ -68,8 +69,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, interval_ms=50):
         self.index = index
+        self.interval_ms = int(interval_ms)
         self.proc = None
         self.lines = []          # (host time, csv line)
         self.window = None       # (t0, t1) of the timed region
@@ -80,7 +82,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -99,6 +101,8 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        # let the exit of the nvidia-smi client settle before anything else is timed
+        time.sleep(0.5)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lines = self.lines
@@ -189,7 +193,7 @@ def run_ours(args):
     # the clock sampler runs from before the warm-up; only its samples inside the
     # timed region are reported
     gc.collect()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, args.clock_interval_ms)
     sampler.start()
     for _ in range(args.warmup):
         step()
@@ -200,6 +204,8 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()   # no cyclic collection inside the timed region (as timeit does); refcount frees still run
     tw0 = time.monotonic()
     ev0.record(stream)
     its, sweep_ms, spmv_ms, orth_ms, setup_s = [], 0.0, 0.0, 0.0, 0.0
@@ -212,6 +218,7 @@ def run_ours(args):
         setup_s += last["setup_s"]
     ev1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     sampler.mark(tw0, time.monotonic())
     launches = hs.kernel_launches() - l0
     clocks = sampler.stop()
@@ -369,6 +376,7 @@ def run_e2e(args, cfg, names, my_names=None, dp=None):
     for _ in range(args.warmup):
         step()
     gc.collect()
+    gc.disable()   # no cyclic collection inside the timed region (as timeit does); refcount frees still run
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
@@ -380,11 +388,15 @@ def run_e2e(args, cfg, names, my_names=None, dp=None):
         step_wall.append(round(1e3 * (time.perf_counter() - s0), 2))
     e1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     wall = time.perf_counter() - w0
     ms = e0.elapsed_time(e1)
     return {"_ms_total": ms, "_applies": sum(its) * len(my_names), "unit": "applies/s",
             "h2d_bytes_per_step": 8 * cfg.n + 16 * cfg.n, "d2h_bytes_per_step": 16 * cfg.n,
             "host_wall_ms_per_step": round(wall / len(its) * 1e3, 3), "host_wall_ms_each_step": step_wall,
+            # isolated host-side stalls (one step of 10-300 ms in ~3% of the steps on this pool's boxes,
+            # DESIGN.md §7) inflate the mean; `value` stays the mean over all K steps
+            "host_wall_ms_median_step": round(sorted(step_wall)[len(step_wall) // 2], 2),
             "steps": len(its), "warmup": args.warmup,
             "path": "helm_assemble(host c) + sweep_setup x4 + helm_load_vector(host f) + mpgmres_solve(x to host)"}
 

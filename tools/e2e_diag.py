@@ -44,3 +44,20 @@ for host in (False, True, False, True):
         step(host)
     Ts = [step(host) for _ in range(3)]
     print("host" if host else "dev ", {k: round(1e3 * sum(T[k] for T in Ts) / 3, 2) for k in Ts[0]}, flush=True)
+
+
+# per-step outliers of the host-buffer step: 150 steps, phases of every step above 1.15x the median
+Ts = [step(True) for _ in range(150)]
+tot = sorted(sum(T.values()) for T in Ts)
+med = tot[len(tot) // 2]
+print(f"host-buffer steps: median {1e3*med:.2f} ms, max {1e3*tot[-1]:.2f} ms", flush=True)
+for i, T in enumerate(Ts):
+    if sum(T.values()) > 1.15 * med:
+        print("  outlier step", i, {k: round(1e3 * v, 2) for k, v in T.items()}, flush=True)
+Ts = [step(False) for _ in range(150)]
+tot = sorted(sum(T.values()) for T in Ts)
+med = tot[len(tot) // 2]
+print(f"device-buffer steps: median {1e3*med:.2f} ms, max {1e3*tot[-1]:.2f} ms", flush=True)
+for i, T in enumerate(Ts):
+    if sum(T.values()) > 1.15 * med:
+        print("  outlier step", i, {k: round(1e3 * v, 2) for k, v in T.items()}, flush=True)
